@@ -1,0 +1,214 @@
+/*
+ * tgl.h -- C ABI of libtgl.so: the TGL hot path (arXiv 2203.14883) on B200 (sm_100a).
+ *
+ *   tgl_tcsr_build   Temporal-CSR construction         PAPER.md L256-L257 (Sec. 3.1, "The T-CSR
+ *                                                      Data Structure"), Fig. 3 (L249-L254)
+ *   tgl_sample       parallel temporal sampler         Alg. 1 (L217-L243), Sec. 3.1 "Sampling"
+ *                                                      (L260-L262), "Parallel Sampling" (L265-L268)
+ *   tgl_gather       mini-batch row gather             Fig. 2 step 2 (L201), node memory / mailbox
+ *                                                      (L154-L175, L210), edge features (Table 3)
+ *   tgl_shard_*      node-sharded exchange helpers      (not in the paper)
+ *
+ * Conventions (every entry point):
+ *   - Data pointers are DEVICE pointers unless marked (host).  `stream` is a cudaStream_t passed
+ *     as void* (NULL = legacy default stream); all device work is enqueued on it, stream-ordered.
+ *   - The caller owns every buffer: inputs, outputs and workspaces.  The library never allocates
+ *     device memory on the sampling / gather path.  A tgl_tcsr handle is a small host struct that
+ *     BORROWS the caller's T-CSR arrays (they must outlive it) plus one 4-byte device error word
+ *     allocated at handle creation.
+ *   - Return value: TGL_OK (0) or a negative TGL_E* code.  Nothing throws across the ABI.
+ *     Host-checkable argument errors return immediately with no device work enqueued.
+ *     Data errors detected on the device by tgl_sample / tgl_gather are STICKY: they never stop
+ *     the stream; tgl_check() reads and clears them.  tgl_tcsr_build validates synchronously.
+ *   - Element types: node ids and edge ids int32, timestamps float32, CSR offsets int64.
+ *     E_s = n_edges * (1 + add_reverse) must be < 2^32; n_nodes < 2^31.
+ *   - Floating point: every window bound is one IEEE-754 binary32 op, round-to-nearest-even,
+ *     no FMA contraction, no flush-to-zero (R#12), so results are bit-identical to the
+ *     CPU oracle.
+ *   - Requires a device of compute capability 10.0 (B200, sm_100a): otherwise TGL_ENOTSUP.
+ */
+#ifndef TGL_H_
+#define TGL_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#if defined(__GNUC__)
+#define TGL_API __attribute__((visibility("default")))
+#else
+#define TGL_API
+#endif
+
+#define TGL_ABI_VERSION 1
+
+enum {
+    TGL_OK = 0,
+    TGL_EINVAL = -1,     /* bad argument: NULL pointer, L<1, S<1, S>TGL_MAX_SNAPSHOTS, k<1 or
+                            k>TGL_MAX_FANOUT, S>1 with non-finite snapshot_len, E_s >= 2^32,
+                            V >= 2^31; device-detected: non-finite or negative edge time at build,
+                            non-finite root time at sampling (R#20, R#21) */
+    TGL_ERANGE = -2,     /* node / row id out of range (device-detected) */
+    TGL_EUNSORTED = -3,  /* build input not chronological (device-detected) */
+    TGL_ECAPACITY = -4,  /* an output buffer is smaller than tgl_sample_capacity() says */
+    TGL_EWORKSPACE = -5, /* workspace smaller than the *_workspace() query says */
+    TGL_ECUDA = -6,      /* CUDA runtime error (launch failure, ...) */
+    TGL_ENCCL = -7,      /* reserved: collective failure in the node-sharded mode */
+    TGL_ENOTSUP = -8     /* device is not sm_100 */
+};
+
+#define TGL_MAX_SNAPSHOTS 16
+#define TGL_MAX_FANOUT 1024
+#define TGL_MAX_GATHER_TABLES 8
+
+typedef struct tgl_tcsr tgl_tcsr; /* opaque, host-side */
+
+typedef enum { TGL_MOST_RECENT = 0, TGL_UNIFORM = 1 } tgl_strategy;
+
+TGL_API int tgl_abi_version(void);
+TGL_API const char *tgl_strerror(int code);
+
+/* ------------------------------------------------------------------ T-CSR */
+
+/* Bytes of device workspace tgl_tcsr_build needs (host query, no device work). */
+TGL_API int tgl_tcsr_build_workspace(int64_t n_edges, int32_t n_nodes, int add_reverse,
+                             size_t *bytes /* host, out */);
+
+/*
+ * Build the T-CSR of a chronological edge stream.
+ *
+ * Inputs (device): src[n_edges], dst[n_edges] int32 in [0, n_nodes); ts[n_edges] float32,
+ *   finite, >= 0, non-decreasing (the stream is chronological); eid[n_edges] int32 or
+ *   NULL (NULL -> eid_i = i).
+ * Logical edge stream (R#19): add_reverse = 0 -> logical edge i = (owner src_i, neighbour dst_i);
+ *   add_reverse = 1 -> logical edges 2i = src_i->dst_i and 2i+1 = dst_i->src_i, both with
+ *   ts_i and eid_i.  E_s = n_edges * (1 + add_reverse).
+ * Outputs (device, caller-allocated): indptr[n_nodes+1] int64 (exclusive scan of owner degrees),
+ *   nbr[E_s] int32, ts_out[E_s] float32, eid_out[E_s] int32: the logical edges grouped by owner,
+ *   each node's list in stream order -- hence time-sorted without a sort -- with ties
+ *   broken by stream order (R#8).  Bit-identical to the oracle's counting sort.
+ * workspace: >= tgl_tcsr_build_workspace() bytes of device memory, 256-byte aligned.
+ * Synchronous validation: the call blocks on `stream` once to read the device validation word;
+ *   on ERANGE / EINVAL / EUNSORTED no handle is returned and outputs are unspecified.
+ * On success *out (host) receives a handle that borrows indptr/nbr/ts_out/eid_out.
+ */
+TGL_API int tgl_tcsr_build(const int32_t *src, const int32_t *dst, const float *ts, const int32_t *eid,
+                   int64_t n_edges, int32_t n_nodes, int add_reverse,
+                   int64_t *indptr, int32_t *nbr, float *ts_out, int32_t *eid_out,
+                   void *workspace, size_t ws_bytes, void *stream, tgl_tcsr **out /* host */);
+
+/* Wrap already-built T-CSR arrays (e.g. received from another rank) in a handle.  No
+ * validation beyond NULL / size checks.  n_stored = E_s = indptr[n_nodes]. */
+TGL_API int tgl_tcsr_wrap(const int64_t *indptr, const int32_t *nbr, const float *ts, const int32_t *eid,
+                  int32_t n_nodes, int64_t n_stored, tgl_tcsr **out /* host */);
+
+TGL_API int tgl_tcsr_destroy(tgl_tcsr *g);
+
+/* Host query of a handle's sizes. */
+TGL_API int tgl_tcsr_info(const tgl_tcsr *g, int32_t *n_nodes /* host */, int64_t *n_stored /* host */);
+
+/* ------------------------------------------------------------------ sampler (Alg. 1) */
+
+/*
+ * One (layer l, snapshot s) message-flow block (the MFG of P:L268), CSR by destination root.
+ * Block (l, s) lives at out[l*S + s].  Its destination side (roots) is the caller's roots for
+ * l = 0 and block (l-1, s)'s (nbr, ts_edge) in output order for l >= 1 (Alg. 1, R#3, R#4,
+ * no dedup R#14).  For root r: edges offsets[r] .. offsets[r+1]-1, in ascending slot (= time)
+ * order (R#13), each (nbr = source node, eid, dt = t_root (-) t_edge).
+ * The caller allocates every array with the capacities tgl_sample_capacity() reports and sets
+ * cap_roots / cap_edges; the library writes n_roots_dev / nnz_dev (device scalars), so no host
+ * synchronisation is needed between layers.
+ */
+typedef struct {
+    int64_t cap_roots;    /* in: capacity of offsets is cap_roots + 1 */
+    int64_t cap_edges;    /* in: capacity of nbr / eid / dt / ts_edge */
+    int64_t *offsets;     /* [n_roots + 1] int64 */
+    int32_t *nbr;         /* [nnz] sampled neighbour (MFG source node) */
+    int32_t *eid;         /* [nnz] edge id of the sampled temporal edge */
+    float *dt;            /* [nnz] t_root (-) t_edge, fp32, > 0 (no leak) */
+    float *ts_edge;       /* [nnz] t_edge; REQUIRED when l < L-1 (next layer's root times), else
+                             may be NULL (then not written) */
+    int64_t *n_roots_dev; /* out: device scalar, number of destination roots of this block */
+    int64_t *nnz_dev;     /* out: device scalar, number of sampled edges of this block */
+} tgl_block;
+
+/*
+ * Capacities for tgl_sample (host query): roots_cap[l] = n_roots * prod_{j<l} fanouts[j],
+ * edges_cap[l] = roots_cap[l] * fanouts[l] (per block), and the workspace bytes.
+ */
+TGL_API int tgl_sample_capacity(int64_t n_roots, int32_t n_layers, const int32_t *fanouts /* host [L] */,
+                        int32_t n_snapshots, tgl_strategy strategy, float snapshot_len,
+                        int64_t *roots_cap /* host [L] */, int64_t *edges_cap /* host [L] */,
+                        size_t *ws_bytes /* host */);
+
+/*
+ * Alg. 1 over n_roots roots (node roots[i], time root_ts[i]), L = n_layers layers with fanouts
+ * k_l, S = n_snapshots dynamic snapshots of length snapshot_len (+INFINITY allowed iff S == 1).
+ *
+ * Window of a root (R#1-R#3, R#12):  l = 0: U_s = t (s = 0) or t (-) (s (x) t_s),
+ *   L_s = t (-) ((s+1) (x) t_s);  l >= 1: U = the hop root's own time, L inherited.
+ *   Candidates = slots of the node's list with L <= ts < U (strictly before the root).
+ * Selection (R#5, R#6): TGL_MOST_RECENT -> the min(k, c) latest candidates;
+ *   TGL_UNIFORM -> all candidates if c <= k, else Floyd's k-subset drawn with Philox4x32-10,
+ *   key (seed_lo, seed_hi), counter (j, l<<16|s, rk_lo, rk_hi), rk = root key (R#7):
+ *   root_key_base + i at layer 0, parent_key * k_l + j below.  Per-batch and many-batch calls
+ *   therefore give identical bits when root_key_base is the roots' global index.
+ * Device-detected errors (out-of-range root id -> ERANGE, non-finite root time -> EINVAL) give
+ *   that root a count of 0 and set the sticky word read by tgl_check(g, ...).
+ * workspace: >= ws_bytes from tgl_sample_capacity(), device memory, 256-byte aligned, not
+ *   shared by concurrent calls.  Launches: one memset + one sampler kernel per layer (layer 0
+ *   covers all S snapshots of a root in one pass; l >= 1 one launch covering all S chains).
+ */
+TGL_API int tgl_sample(const tgl_tcsr *g, const int32_t *roots, const float *root_ts, int64_t n_roots,
+               int32_t n_layers, const int32_t *fanouts /* host [L] */, tgl_strategy strategy,
+               int32_t n_snapshots, float snapshot_len, uint64_t seed, uint64_t root_key_base,
+               tgl_block *out /* host [L*S] */, void *workspace, size_t ws_bytes, void *stream);
+
+/* ------------------------------------------------------------------ gather (Fig. 2 step 2) */
+
+/* One gather target: out row i = table row ids[i]; row_bytes bytes per row. */
+typedef struct {
+    const void *table; /* device [n_rows * row_bytes] */
+    int64_t n_rows;
+    int64_t row_bytes;
+    void *out;         /* device [n_ids * row_bytes] */
+} tgl_gather_table;
+
+/*
+ * For every table t and every i < n_ids: out_t[i] = table_t[ids[i]] byte for byte (node memory,
+ * mailbox, their timestamps, edge features -- P:L201, L210, Table 3).  id == -1 gives a zero row;
+ * any other id outside [0, n_rows) gives a zero row and sets the sticky ERANGE word.
+ * n_ids = *n_ids_dev (device scalar, clamped to n_ids_cap) when n_ids_dev != NULL, else
+ * n_ids_cap -- so a gather can follow tgl_sample on the stream with no host sync.
+ * One kernel launch for all tables (<= TGL_MAX_GATHER_TABLES).
+ */
+TGL_API int tgl_gather(const int32_t *ids, int64_t n_ids_cap, const int64_t *n_ids_dev,
+               const tgl_gather_table *tables /* host [n_tables] */, int32_t n_tables, void *stream);
+
+/* ------------------------------------------------------------------ errors */
+
+/* Synchronises `stream`, returns the first sticky device error raised since the last check by
+ * tgl_sample on g (or by tgl_gather when g == NULL) and clears it. */
+TGL_API int tgl_check(tgl_tcsr *g, void *stream);
+
+/* ------------------------------------------------------------------ node-sharded mode */
+
+/*
+ * Owner bucketing for the node-sharded T-CSR: node v is owned by shard r with
+ * splits[r] <= v < splits[r+1] (splits: device int64 [world+1], splits[0] = 0, splits[world] = V).
+ * Stable counting sort of the n roots by owner: perm[j] = index of the j-th root in
+ * (owner, original index) order; counts[r] = roots owned by r (device int64 [world]).
+ * The exchange itself (all-to-all-v of requests and replies) is NCCL, issued by the caller.
+ * workspace >= tgl_shard_bucket_workspace() bytes.
+ */
+TGL_API int tgl_shard_bucket_workspace(int64_t n_roots, int32_t world, size_t *bytes /* host */);
+TGL_API int tgl_shard_bucket(const int32_t *roots, int64_t n_roots, const int64_t *splits, int32_t world,
+                     int64_t *perm, int64_t *counts, void *workspace, size_t ws_bytes, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TGL_H_ */

@@ -1,0 +1,249 @@
+"""TGL hot path on B200 (arXiv 2203.14883): T-CSR build, parallel temporal sampler, gather.
+
+Thin Python binding over ``libtgl.so`` (C ABI: ``include/tgl.h``).  PyTorch provides device
+memory and the current CUDA stream; every step of the path runs in the library's sm_100a
+kernels.  There is no CPU fallback: importing this package without the built library raises,
+and every call requires CUDA tensors.
+
+    g = build(src, dst, ts, eid=None, n_nodes=V, add_reverse=True)
+    blocks = sample(g, roots, root_ts, fanouts=[10], strategy="most_recent",  # Alg. 1
+                    n_snapshots=1, snapshot_len=float("inf"), seed=0, root_key_base=0)
+    outs = gather(ids, [memory, mailbox, ...], n_ids_dev=None)                 # Fig. 2 step 2
+"""
+from __future__ import annotations
+
+import ctypes
+import math
+from dataclasses import dataclass
+from typing import List, Optional, Sequence
+
+import torch
+
+from . import _lib
+from ._lib import MOST_RECENT, UNIFORM, TGLError
+
+_L = _lib.load()
+
+__all__ = ["TCSR", "Block", "Sampler", "build", "wrap", "sample", "gather", "check", "shard_bucket",
+           "MOST_RECENT", "UNIFORM", "TGLError", "lib_path"]
+
+lib_path = _lib.LIB_PATH
+
+
+def _ptr(t: Optional[torch.Tensor]):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _stream(stream=None):
+    s = torch.cuda.current_stream() if stream is None else stream
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def _rc(code: int, what: str):
+    if code != _lib.OK:
+        raise TGLError(code, what, _L)
+
+
+def _cuda(t: torch.Tensor, dtype: torch.dtype, name: str) -> torch.Tensor:
+    if not isinstance(t, torch.Tensor) or not t.is_cuda:
+        raise TypeError(f"{name} must be a CUDA tensor (no CPU fallback)")
+    if t.dtype != dtype:
+        raise TypeError(f"{name} must be {dtype}, got {t.dtype}")
+    return t.contiguous()
+
+
+def _strategy(s) -> int:
+    if isinstance(s, str):
+        return {"most_recent": MOST_RECENT, "uniform": UNIFORM}[s]
+    return int(s)
+
+
+class TCSR:
+    """A built T-CSR: indptr int64 [V+1]; nbr int32, ts float32, eid int32 [E_s]."""
+
+    def __init__(self, indptr, nbr, ts, eid, n_nodes, handle):
+        self.indptr, self.nbr, self.ts, self.eid = indptr, nbr, ts, eid
+        self.n_nodes = int(n_nodes)
+        self.n_stored = int(nbr.numel())
+        self._h = handle
+
+    @property
+    def handle(self):
+        return self._h
+
+    def __del__(self):
+        h, self._h = getattr(self, "_h", None), None
+        if h:
+            _L.tgl_tcsr_destroy(h)
+
+
+def build_workspace_bytes(n_edges: int, n_nodes: int, add_reverse: bool) -> int:
+    b = ctypes.c_size_t()
+    _rc(_L.tgl_tcsr_build_workspace(int(n_edges), int(n_nodes), int(add_reverse), ctypes.byref(b)),
+        "tgl_tcsr_build_workspace")
+    return b.value
+
+
+def build(src: torch.Tensor, dst: torch.Tensor, ts: torch.Tensor, eid: Optional[torch.Tensor] = None, *,
+          n_nodes: int, add_reverse: bool, workspace: Optional[torch.Tensor] = None, stream=None) -> TCSR:
+    """tgl_tcsr_build: T-CSR of a chronological stream."""
+    src = _cuda(src, torch.int32, "src")
+    dst = _cuda(dst, torch.int32, "dst")
+    ts = _cuda(ts, torch.float32, "ts")
+    if eid is not None:
+        eid = _cuda(eid, torch.int32, "eid")
+    E = src.numel()
+    Es = E * (2 if add_reverse else 1)
+    dev = src.device
+    indptr = torch.empty(n_nodes + 1, dtype=torch.int64, device=dev)
+    nbr = torch.empty(Es, dtype=torch.int32, device=dev)
+    ts_out = torch.empty(Es, dtype=torch.float32, device=dev)
+    eid_out = torch.empty(Es, dtype=torch.int32, device=dev)
+    wsb = build_workspace_bytes(E, n_nodes, add_reverse)
+    if workspace is None or workspace.numel() < wsb:
+        workspace = torch.empty(max(wsb, 1), dtype=torch.uint8, device=dev)
+    h = ctypes.c_void_p()
+    _rc(_L.tgl_tcsr_build(_ptr(src), _ptr(dst), _ptr(ts), _ptr(eid), E, int(n_nodes), int(add_reverse),
+                          _ptr(indptr), _ptr(nbr), _ptr(ts_out), _ptr(eid_out), _ptr(workspace), wsb,
+                          _stream(stream), ctypes.byref(h)), "tgl_tcsr_build")
+    return TCSR(indptr, nbr, ts_out, eid_out, n_nodes, h)
+
+
+def wrap(indptr: torch.Tensor, nbr: torch.Tensor, ts: torch.Tensor, eid: torch.Tensor) -> TCSR:
+    """tgl_tcsr_wrap: handle over existing T-CSR arrays (e.g. broadcast from another rank)."""
+    indptr = _cuda(indptr, torch.int64, "indptr")
+    nbr = _cuda(nbr, torch.int32, "nbr")
+    ts = _cuda(ts, torch.float32, "ts")
+    eid = _cuda(eid, torch.int32, "eid")
+    h = ctypes.c_void_p()
+    _rc(_L.tgl_tcsr_wrap(_ptr(indptr), _ptr(nbr), _ptr(ts), _ptr(eid), indptr.numel() - 1, nbr.numel(),
+                         ctypes.byref(h)), "tgl_tcsr_wrap")
+    return TCSR(indptr, nbr, ts, eid, indptr.numel() - 1, h)
+
+
+@dataclass
+class Block:
+    """One (layer, snapshot) message-flow block at capacity size; n_roots / nnz live on the device."""
+    offsets: torch.Tensor
+    nbr: torch.Tensor
+    eid: torch.Tensor
+    dt: torch.Tensor
+    ts_edge: Optional[torch.Tensor]
+    n_roots_dev: torch.Tensor
+    nnz_dev: torch.Tensor
+
+    def trimmed(self):
+        """Host-synchronising view: (offsets[:n+1], nbr[:nnz], eid[:nnz], dt[:nnz], ts_edge[:nnz])."""
+        n, nnz = int(self.n_roots_dev.item()), int(self.nnz_dev.item())
+        te = None if self.ts_edge is None else self.ts_edge[:nnz]
+        return self.offsets[: n + 1], self.nbr[:nnz], self.eid[:nnz], self.dt[:nnz], te
+
+
+class Sampler:
+    """Preallocated outputs + workspace for repeated tgl_sample calls of up to max_roots roots."""
+
+    def __init__(self, g: TCSR, max_roots: int, fanouts: Sequence[int], strategy="most_recent",
+                 n_snapshots: int = 1, snapshot_len: float = math.inf, device=None, want_ts_edge_last=False):
+        self.g = g
+        self.fanouts = [int(k) for k in fanouts]
+        self.L, self.S = len(self.fanouts), int(n_snapshots)
+        self.strategy = _strategy(strategy)
+        self.snapshot_len = float(snapshot_len)
+        self.max_roots = int(max_roots)
+        dev = g.nbr.device if device is None else device
+        rc_, ec_, wsb = self.capacity(self.max_roots)
+        self.roots_cap, self.edges_cap = rc_, ec_
+        self.workspace = torch.empty(max(wsb, 1), dtype=torch.uint8, device=dev)
+        self.ws_bytes = wsb
+        scal = torch.zeros(2 * self.L * self.S, dtype=torch.int64, device=dev)
+        self.blocks: List[Block] = []
+        for l in range(self.L):
+            for s in range(self.S):
+                need_ts = l < self.L - 1 or want_ts_edge_last
+                j = l * self.S + s
+                self.blocks.append(Block(
+                    offsets=torch.empty(rc_[l] + 1, dtype=torch.int64, device=dev),
+                    nbr=torch.empty(ec_[l], dtype=torch.int32, device=dev),
+                    eid=torch.empty(ec_[l], dtype=torch.int32, device=dev),
+                    dt=torch.empty(ec_[l], dtype=torch.float32, device=dev),
+                    ts_edge=torch.empty(ec_[l], dtype=torch.float32, device=dev) if need_ts else None,
+                    n_roots_dev=scal[2 * j: 2 * j + 1], nnz_dev=scal[2 * j + 1: 2 * j + 2]))
+        self._c_blocks = (_lib.Block * len(self.blocks))()
+        for j, b in enumerate(self.blocks):
+            l = j // self.S
+            self._c_blocks[j] = _lib.Block(rc_[l], ec_[l], b.offsets.data_ptr(), b.nbr.data_ptr(), b.eid.data_ptr(),
+                                           b.dt.data_ptr(), 0 if b.ts_edge is None else b.ts_edge.data_ptr(),
+                                           b.n_roots_dev.data_ptr(), b.nnz_dev.data_ptr())
+        self._fan = (ctypes.c_int32 * self.L)(*self.fanouts)
+
+    def capacity(self, n_roots: int):
+        rc_ = (ctypes.c_int64 * self.L)()
+        ec_ = (ctypes.c_int64 * self.L)()
+        wsb = ctypes.c_size_t()
+        fan = (ctypes.c_int32 * self.L)(*self.fanouts)
+        _rc(_L.tgl_sample_capacity(int(n_roots), self.L, fan, self.S, self.strategy, self.snapshot_len, rc_, ec_,
+                                   ctypes.byref(wsb)), "tgl_sample_capacity")
+        return list(rc_), list(ec_), wsb.value
+
+    def run(self, roots: torch.Tensor, root_ts: torch.Tensor, *, seed: int = 0, root_key_base: int = 0,
+            n_roots: Optional[int] = None, stream=None) -> List[Block]:
+        """tgl_sample on the current (or given) stream; no host synchronisation."""
+        n = roots.numel() if n_roots is None else int(n_roots)
+        if n > self.max_roots:
+            raise ValueError(f"{n} roots > max_roots {self.max_roots}")
+        if not (roots.is_cuda and roots.dtype == torch.int32 and root_ts.is_cuda and root_ts.dtype == torch.float32):
+            raise TypeError("roots must be CUDA int32 and root_ts CUDA float32 (no CPU fallback)")
+        _rc(_L.tgl_sample(self.g.handle, _ptr(roots), _ptr(root_ts), n, self.L, self._fan, self.strategy, self.S,
+                          self.snapshot_len, int(seed) & 0xFFFFFFFFFFFFFFFF, int(root_key_base) & 0xFFFFFFFFFFFFFFFF,
+                          self._c_blocks, _ptr(self.workspace), self.ws_bytes, _stream(stream)), "tgl_sample")
+        return self.blocks
+
+
+def sample(g: TCSR, roots: torch.Tensor, root_ts: torch.Tensor, *, fanouts: Sequence[int],
+           strategy="most_recent", n_snapshots: int = 1, snapshot_len: float = math.inf, seed: int = 0,
+           root_key_base: int = 0, stream=None) -> List[Block]:
+    """tgl_sample (Alg. 1): returns L*S blocks, block (l, s) at index l*S + s."""
+    roots = _cuda(roots, torch.int32, "roots")
+    root_ts = _cuda(root_ts, torch.float32, "root_ts")
+    s = Sampler(g, max(roots.numel(), 1), fanouts, strategy, n_snapshots, snapshot_len)
+    return s.run(roots, root_ts, seed=seed, root_key_base=root_key_base, n_roots=roots.numel(), stream=stream)
+
+
+def gather(ids: torch.Tensor, tables: Sequence[torch.Tensor], *, n_ids_dev: Optional[torch.Tensor] = None,
+           outs: Optional[Sequence[torch.Tensor]] = None, stream=None) -> List[torch.Tensor]:
+    """tgl_gather: out_t[i] = table_t[ids[i]] (rows of any width); id -1 -> zero row."""
+    ids = _cuda(ids, torch.int32, "ids")
+    n = ids.numel()
+    if len(tables) > _lib.MAX_GATHER_TABLES:
+        raise ValueError("too many tables")
+    res, arr = [], (_lib.GatherTable * max(len(tables), 1))()
+    for j, t in enumerate(tables):
+        if not t.is_cuda or not t.is_contiguous():
+            raise TypeError("gather tables must be contiguous CUDA tensors")
+        rows = t.shape[0]
+        row_bytes = t.element_size() * (t[0].numel() if t.dim() > 1 else 1)
+        o = outs[j] if outs is not None else torch.empty((n,) + tuple(t.shape[1:]), dtype=t.dtype, device=t.device)
+        res.append(o)
+        arr[j] = _lib.GatherTable(t.data_ptr(), rows, row_bytes, o.data_ptr())
+    _rc(_L.tgl_gather(_ptr(ids), n, _ptr(n_ids_dev), arr, len(tables), _stream(stream)), "tgl_gather")
+    return res
+
+
+def check(g: Optional[TCSR] = None, stream=None) -> int:
+    """tgl_check: synchronise and return (and clear) the sticky device error code (0 = none)."""
+    return _L.tgl_check(None if g is None else g.handle, _stream(stream))
+
+
+def shard_bucket(roots: torch.Tensor, splits: torch.Tensor, world: int, stream=None):
+    """tgl_shard_bucket: stable permutation of roots by owner shard + per-shard counts."""
+    roots = _cuda(roots, torch.int32, "roots")
+    splits = _cuda(splits, torch.int64, "splits")
+    n = roots.numel()
+    wsb = ctypes.c_size_t()
+    _rc(_L.tgl_shard_bucket_workspace(n, int(world), ctypes.byref(wsb)), "tgl_shard_bucket_workspace")
+    ws = torch.empty(max(wsb.value, 1), dtype=torch.uint8, device=roots.device)
+    perm = torch.empty(max(n, 1), dtype=torch.int64, device=roots.device)
+    counts = torch.empty(int(world), dtype=torch.int64, device=roots.device)
+    _rc(_L.tgl_shard_bucket(_ptr(roots), n, _ptr(splits), int(world), _ptr(perm), _ptr(counts), _ptr(ws),
+                            wsb.value, _stream(stream)), "tgl_shard_bucket")
+    return perm[:n], counts

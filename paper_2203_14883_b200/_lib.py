@@ -1,0 +1,68 @@
+"""ctypes declarations of libtgl.so (include/tgl.h).  Argument marshalling only.
+
+The shared library is built in-tree (``make`` or ``__graft_entry__.build()``) next to this
+file.  There is no fallback: if it is missing or fails to load, importing the package raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libtgl.so")
+
+OK, EINVAL, ERANGE, EUNSORTED, ECAPACITY, EWORKSPACE, ECUDA, ENCCL, ENOTSUP = 0, -1, -2, -3, -4, -5, -6, -7, -8
+MOST_RECENT, UNIFORM = 0, 1
+MAX_SNAPSHOTS, MAX_FANOUT, MAX_GATHER_TABLES = 16, 1024, 8
+
+P = ctypes.c_void_p
+i32, i64, u64, f32, sz = ctypes.c_int32, ctypes.c_int64, ctypes.c_uint64, ctypes.c_float, ctypes.c_size_t
+
+
+class Block(ctypes.Structure):
+    """tgl_block (include/tgl.h)."""
+    _fields_ = [("cap_roots", i64), ("cap_edges", i64), ("offsets", P), ("nbr", P), ("eid", P), ("dt", P),
+                ("ts_edge", P), ("n_roots_dev", P), ("nnz_dev", P)]
+
+
+class GatherTable(ctypes.Structure):
+    """tgl_gather_table (include/tgl.h)."""
+    _fields_ = [("table", P), ("n_rows", i64), ("row_bytes", i64), ("out", P)]
+
+
+# name -> (restype, argtypes), exactly the declarations of include/tgl.h
+SIGNATURES = {
+    "tgl_abi_version": (ctypes.c_int, []),
+    "tgl_strerror": (ctypes.c_char_p, [ctypes.c_int]),
+    "tgl_tcsr_build_workspace": (ctypes.c_int, [i64, i32, ctypes.c_int, ctypes.POINTER(sz)]),
+    "tgl_tcsr_build": (ctypes.c_int, [P, P, P, P, i64, i32, ctypes.c_int, P, P, P, P, P, sz, P,
+                                      ctypes.POINTER(P)]),
+    "tgl_tcsr_wrap": (ctypes.c_int, [P, P, P, P, i32, i64, ctypes.POINTER(P)]),
+    "tgl_tcsr_destroy": (ctypes.c_int, [P]),
+    "tgl_tcsr_info": (ctypes.c_int, [P, ctypes.POINTER(i32), ctypes.POINTER(i64)]),
+    "tgl_sample_capacity": (ctypes.c_int, [i64, i32, P, i32, ctypes.c_int, f32, P, P, ctypes.POINTER(sz)]),
+    "tgl_sample": (ctypes.c_int, [P, P, P, i64, i32, P, ctypes.c_int, i32, f32, u64, u64, P, P, sz, P]),
+    "tgl_gather": (ctypes.c_int, [P, i64, P, P, i32, P]),
+    "tgl_check": (ctypes.c_int, [P, P]),
+    "tgl_shard_bucket_workspace": (ctypes.c_int, [i64, i32, ctypes.POINTER(sz)]),
+    "tgl_shard_bucket": (ctypes.c_int, [P, i64, P, i32, P, P, P, sz, P]),
+}
+
+
+def load() -> ctypes.CDLL:
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"libtgl.so not built at {LIB_PATH}: run `make` or __graft_entry__.build() "
+                          "(there is no CPU fallback)")
+    lib = ctypes.CDLL(LIB_PATH)
+    for name, (res, args) in SIGNATURES.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    return lib
+
+
+class TGLError(RuntimeError):
+    def __init__(self, code: int, what: str, lib=None):
+        msg = lib.tgl_strerror(code).decode() if lib is not None else str(code)
+        super().__init__(f"{what}: {msg} ({code})")
+        self.code = code

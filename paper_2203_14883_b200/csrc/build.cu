@@ -1,0 +1,403 @@
+// build.cu -- T-CSR construction on B200 (Sec. 3.1 "The T-CSR Data Structure").
+//
+//   K1 validate_hist_kernel   a1 + a2: range / finiteness / chronology checks (device flags) and
+//                             the owner-degree histogram (warp-aggregated atomics).
+//   K2 exclusive_scan         a3: indptr[v] = sum_{u<v} deg[u], indptr[V] = E_s.
+//   K3 radix passes           a4: the stable scatter.  The slot of logical edge j is
+//                             indptr[owner_j] + #{j' < j : owner_j' = owner_j}.  Computed as a
+//                             stable LSD counting sort of (owner, j) by owner, 8 bits per pass:
+//                             each pass is itself histogram -> scan -> stable scatter, with the
+//                             in-tile stable rank from __match_any_sync.  The last pass writes
+//                             the T-CSR arrays directly at the final slot (the sort position IS
+//                             the slot), so lists come out in stream = time order without a
+//                             sort on time, ties by stream order (R#8).
+//
+// Deterministic: no atomic decides an output position.
+#include <algorithm>
+
+#include "common.cuh"
+#include "scan.cuh"
+
+namespace tgl {
+
+constexpr int kRadixThreads = 256;
+constexpr int kRadixWarps = kRadixThreads / 32;
+constexpr int kRadixItems = 16;                          // per thread
+constexpr int kRadixTile = kRadixThreads * kRadixItems;  // 4096 logical edges per tile
+constexpr int kRadixBins = 256;
+
+// ---------------------------------------------------------------------------- K1
+__global__ void __launch_bounds__(256) validate_hist_kernel(const int32_t* __restrict__ src,
+                                                            const int32_t* __restrict__ dst,
+                                                            const float* __restrict__ ts, int64_t n,
+                                                            int32_t n_nodes, int add_reverse,
+                                                            uint32_t* __restrict__ deg, int* __restrict__ err) {
+    int bits = 0;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i - threadIdx.x % 32 < n; i += stride) {
+        const bool live = i < n;
+        int32_t s = 0, d = 0;
+        if (live) {
+            s = src[i];
+            d = dst[i];
+            const float t = ts[i];
+            if (!(t >= 0.0f && t <= 3.402823466e38f)) bits |= kErrInval;  // NaN, inf, negative
+            if (i > 0 && ts[i - 1] > t) bits |= kErrUnsorted;
+            if ((uint32_t)s >= (uint32_t)n_nodes || (uint32_t)d >= (uint32_t)n_nodes) bits |= kErrRange;
+        }
+        const bool ok_s = live && (uint32_t)s < (uint32_t)n_nodes;
+        const bool ok_d = live && add_reverse && (uint32_t)d < (uint32_t)n_nodes;
+        // warp-aggregated histogram: one atomic per distinct owner in the warp
+        {
+            const int key = ok_s ? s : -1;
+            const uint32_t peers = __match_any_sync(kFull, key);
+            if (ok_s && (__ffs(peers) - 1) == (int)(threadIdx.x & 31)) atomicAdd(&deg[s], __popc(peers));
+        }
+        if (add_reverse) {
+            const int key = ok_d ? d : -1;
+            const uint32_t peers = __match_any_sync(kFull, key);
+            if (ok_d && (__ffs(peers) - 1) == (int)(threadIdx.x & 31)) atomicAdd(&deg[d], __popc(peers));
+        }
+    }
+    bits = __reduce_or_sync(kFull, bits);
+    if (bits && (threadIdx.x & 31) == 0) atomicOr(err, bits);
+}
+
+// ---------------------------------------------------------------------------- K3 helpers
+struct Stream {
+    const int32_t* src;
+    const int32_t* dst;
+    const float* ts;
+    const int32_t* eid;  // may be null -> eid = input index
+    int add_reverse;
+};
+
+__device__ __forceinline__ uint32_t owner_of(const Stream& s, uint64_t j) {
+    if (s.add_reverse) {
+        const uint64_t i = j >> 1;
+        return (uint32_t)((j & 1) ? s.dst[i] : s.src[i]);
+    }
+    return (uint32_t)s.src[j];
+}
+
+// Source of a pass: the raw edge stream (key = owner, value = logical index j), a (key, value)
+// buffer pair from the previous pass, or a key buffer whose values are the identity j.
+enum { kSrcStream = 0, kSrcKV = 1, kSrcKeys = 2 };
+// Destination: (key, value) buffers, the T-CSR arrays at the final slot, or an int64 permutation.
+enum { kDstKV = 0, kDstTCSR = 1, kDstPerm = 2 };
+
+// Index of item r of this thread inside the tile: warp-striped, so that the (round, lane)
+// order of a warp is the stream order of its 512 items and warps are in stream order.
+__device__ __forceinline__ uint64_t tile_item(uint64_t tile, int warp, int r, int lane) {
+    return tile * kRadixTile + (uint64_t)warp * (32 * kRadixItems) + (uint64_t)r * 32 + lane;
+}
+
+template <int SRC>
+__global__ void __launch_bounds__(kRadixThreads) radix_upsweep_kernel(Stream s, const uint32_t* __restrict__ keys_in,
+                                                                      uint64_t n, int shift, uint32_t mask,
+                                                                      uint32_t* __restrict__ counts, uint64_t ntiles) {
+    __shared__ uint32_t hist[kRadixWarps][kRadixBins];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int b = threadIdx.x; b < kRadixWarps * kRadixBins; b += kRadixThreads) (&hist[0][0])[b] = 0;
+    __syncthreads();
+    const uint64_t tile = blockIdx.x;
+#pragma unroll 4
+    for (int r = 0; r < kRadixItems; ++r) {
+        const uint64_t j = tile_item(tile, warp, r, lane);
+        if (j < n) {
+            const uint32_t key = SRC == kSrcStream ? owner_of(s, j) : keys_in[j];
+            atomicAdd(&hist[warp][(key >> shift) & mask], 1u);
+        }
+    }
+    __syncthreads();
+    for (int b = threadIdx.x; b < kRadixBins; b += kRadixThreads) {
+        uint32_t c = 0;
+#pragma unroll
+        for (int w = 0; w < kRadixWarps; ++w) c += hist[w][b];
+        counts[(uint64_t)b * ntiles + tile] = c;  // digit-major: scanning it gives global offsets
+    }
+}
+
+// Downsweep: stable scatter of the tile.  offsets = exclusive scan of counts (digit-major).
+template <int SRC, int DST>
+__global__ void __launch_bounds__(kRadixThreads) radix_downsweep_kernel(
+    Stream s, const uint32_t* __restrict__ keys_in, const uint32_t* __restrict__ vals_in, uint64_t n, int shift,
+    uint32_t mask, const uint32_t* __restrict__ offsets, uint64_t ntiles, uint32_t* __restrict__ keys_out,
+    uint32_t* __restrict__ vals_out, int32_t* __restrict__ nbr_out, float* __restrict__ ts_out,
+    int32_t* __restrict__ eid_out, int64_t* __restrict__ perm_out) {
+    __shared__ uint32_t wcnt[kRadixWarps][kRadixBins];
+    __shared__ uint32_t dbase[kRadixBins];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint64_t tile = blockIdx.x;
+    for (int b = threadIdx.x; b < kRadixWarps * kRadixBins; b += kRadixThreads) (&wcnt[0][0])[b] = 0;
+    for (int b = threadIdx.x; b < kRadixBins; b += kRadixThreads) dbase[b] = offsets[(uint64_t)b * ntiles + tile];
+    __syncthreads();
+
+    uint32_t key[kRadixItems], val[kRadixItems], rank[kRadixItems];
+    const uint32_t lt = lanemask_lt();
+#pragma unroll
+    for (int r = 0; r < kRadixItems; ++r) {
+        const uint64_t j = tile_item(tile, warp, r, lane);
+        const bool valid = j < n;
+        key[r] = valid ? (SRC == kSrcStream ? owner_of(s, j) : keys_in[j]) : 0u;
+        val[r] = valid ? (SRC == kSrcKV ? vals_in[j] : (uint32_t)j) : 0u;
+        const uint32_t d = valid ? ((key[r] >> shift) & mask) : (uint32_t)kRadixBins;  // sentinel
+        const uint32_t peers = __match_any_sync(kFull, d);
+        const int leader = __ffs(peers) - 1;
+        uint32_t cnt = 0;
+        if (valid) cnt = wcnt[warp][d];
+        rank[r] = cnt + __popc(peers & lt);
+        __syncwarp();
+        if (valid && lane == leader) wcnt[warp][d] = cnt + __popc(peers);
+        __syncwarp();
+    }
+    __syncthreads();
+    for (int b = threadIdx.x; b < kRadixBins; b += kRadixThreads) {
+        uint32_t run = 0;
+#pragma unroll
+        for (int w = 0; w < kRadixWarps; ++w) {
+            const uint32_t c = wcnt[w][b];
+            wcnt[w][b] = run;
+            run += c;
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < kRadixItems; ++r) {
+        const uint64_t j = tile_item(tile, warp, r, lane);
+        if (j >= n) continue;
+        const uint32_t d = (key[r] >> shift) & mask;
+        const uint64_t pos = (uint64_t)dbase[d] + wcnt[warp][d] + rank[r];
+        if (DST == kDstTCSR) {
+            const uint64_t lj = val[r];
+            const uint64_t i = s.add_reverse ? (lj >> 1) : lj;
+            const bool rev = s.add_reverse && (lj & 1);
+            nbr_out[pos] = rev ? s.src[i] : s.dst[i];
+            ts_out[pos] = s.ts[i];
+            eid_out[pos] = s.eid ? s.eid[i] : (int32_t)i;
+        } else if (DST == kDstPerm) {
+            perm_out[pos] = (int64_t)val[r];
+        } else {
+            keys_out[pos] = key[r];
+            vals_out[pos] = val[r];
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------- host plan
+struct BuildPlan {
+    uint64_t n_logical = 0;
+    int bits = 0, passes = 1;
+    uint64_t ntiles = 0;
+    int nbuf = 0;
+    int* err = nullptr;
+    uint32_t* deg = nullptr;
+    uint64_t* partial = nullptr;
+    uint32_t* counts = nullptr;
+    uint32_t* kbuf[2] = {nullptr, nullptr};
+    uint32_t* vbuf[2] = {nullptr, nullptr};
+    size_t bytes = 0;
+};
+
+static BuildPlan plan_build(int64_t n_edges, int32_t n_nodes, int add_reverse, void* ws) {
+    BuildPlan p;
+    p.n_logical = (uint64_t)n_edges * (add_reverse ? 2 : 1);
+    p.bits = n_nodes <= 1 ? 0 : 32 - __builtin_clz((unsigned)(n_nodes - 1));
+    p.passes = p.bits <= 8 ? 1 : (p.bits + 7) / 8;
+    p.ntiles = (p.n_logical + kRadixTile - 1) / kRadixTile;
+    p.nbuf = p.passes >= 3 ? 2 : (p.passes == 2 ? 1 : 0);
+    Carve c(ws);
+    p.err = c.take<int>(64);
+    p.deg = c.take<uint32_t>((size_t)(n_nodes > 0 ? n_nodes : 1));
+    int64_t scan_n = std::max<int64_t>((int64_t)n_nodes, (int64_t)(kRadixBins * p.ntiles));
+    p.partial = c.take<uint64_t>(scan_workspace_bytes(scan_n) / sizeof(uint64_t));
+    p.counts = c.take<uint32_t>((size_t)kRadixBins * (p.ntiles ? p.ntiles : 1));
+    for (int b = 0; b < p.nbuf; ++b) {
+        p.kbuf[b] = c.take<uint32_t>(p.n_logical);
+        p.vbuf[b] = c.take<uint32_t>(p.n_logical);
+    }
+    p.bytes = c.bytes();
+    return p;
+}
+
+}  // namespace tgl
+
+using namespace tgl;
+
+extern "C" int tgl_tcsr_build_workspace(int64_t n_edges, int32_t n_nodes, int add_reverse, size_t* bytes) {
+    if (!bytes || n_edges < 0 || n_nodes < 0) return TGL_EINVAL;
+    const uint64_t es = (uint64_t)n_edges * (add_reverse ? 2 : 1);
+    if (es >= (1ull << 32)) return TGL_EINVAL;
+    *bytes = plan_build(n_edges, n_nodes, add_reverse ? 1 : 0, nullptr).bytes;
+    return TGL_OK;
+}
+
+extern "C" int tgl_tcsr_build(const int32_t* src, const int32_t* dst, const float* ts, const int32_t* eid,
+                              int64_t n_edges, int32_t n_nodes, int add_reverse, int64_t* indptr, int32_t* nbr,
+                              float* ts_out, int32_t* eid_out, void* workspace, size_t ws_bytes, void* stream,
+                              tgl_tcsr** out) {
+    if (!out || !indptr || n_edges < 0 || n_nodes < 0) return TGL_EINVAL;
+    *out = nullptr;
+    add_reverse = add_reverse ? 1 : 0;
+    const uint64_t es = (uint64_t)n_edges * (add_reverse ? 2 : 1);
+    if (es >= (1ull << 32)) return TGL_EINVAL;
+    if (n_edges > 0 && (!src || !dst || !ts || !nbr || !ts_out || !eid_out)) return TGL_EINVAL;
+    if (!workspace) return TGL_EINVAL;
+    int rc = check_device();
+    if (rc) return rc;
+    BuildPlan p = plan_build(n_edges, n_nodes, add_reverse, workspace);
+    if (ws_bytes < p.bytes) return TGL_EWORKSPACE;
+    cudaStream_t st = (cudaStream_t)stream;
+
+    // K1: validation + degree histogram
+    if (cudaMemsetAsync(p.err, 0, sizeof(int), st) != cudaSuccess) return TGL_ECUDA;
+    if (n_nodes > 0 && cudaMemsetAsync(p.deg, 0, sizeof(uint32_t) * (size_t)n_nodes, st) != cudaSuccess)
+        return TGL_ECUDA;
+    if (n_edges > 0) {
+        int64_t blocks = std::min<int64_t>((n_edges + 255) / 256, 148 * 16);
+        validate_hist_kernel<<<(unsigned)blocks, 256, 0, st>>>(src, dst, ts, n_edges, n_nodes, add_reverse, p.deg,
+                                                                p.err);
+        if (cudaGetLastError() != cudaSuccess) return TGL_ECUDA;
+    }
+    int herr = 0;
+    if (cudaMemcpyAsync(&herr, p.err, sizeof(int), cudaMemcpyDeviceToHost, st) != cudaSuccess) return TGL_ECUDA;
+    if (cudaStreamSynchronize(st) != cudaSuccess) return TGL_ECUDA;
+    if (herr) return err_bits_to_code(herr);
+
+    // K2: indptr = exclusive scan of degrees, indptr[V] = E_s
+    if (cuda_rc(exclusive_scan<uint32_t, int64_t>(p.deg, indptr, n_nodes, indptr + n_nodes, p.partial, st)))
+        return TGL_ECUDA;
+
+    // K3: stable scatter via LSD counting-sort passes over the logical stream
+    if (p.n_logical > 0) {
+        Stream s{src, dst, ts, eid, add_reverse};
+        const uint64_t n = p.n_logical;
+        for (int pass = 0; pass < p.passes; ++pass) {
+            const int shift = 8 * pass;
+            const int nb = std::min(8, std::max(0, p.bits - shift));
+            const uint32_t mask = nb >= 32 ? 0xffffffffu : ((1u << nb) - 1u);
+            const bool first = pass == 0, last = pass == p.passes - 1;
+            const uint32_t* kin = first ? nullptr : p.kbuf[(pass - 1) & 1];
+            const uint32_t* vin = first ? nullptr : p.vbuf[(pass - 1) & 1];
+            uint32_t* kout = last ? nullptr : p.kbuf[pass & 1];
+            uint32_t* vout = last ? nullptr : p.vbuf[pass & 1];
+            const unsigned grid = (unsigned)p.ntiles;
+            if (first)
+                radix_upsweep_kernel<kSrcStream><<<grid, kRadixThreads, 0, st>>>(s, kin, n, shift, mask, p.counts,
+                                                                                  p.ntiles);
+            else
+                radix_upsweep_kernel<kSrcKV><<<grid, kRadixThreads, 0, st>>>(s, kin, n, shift, mask, p.counts,
+                                                                              p.ntiles);
+            if (cuda_rc(exclusive_scan<uint32_t, uint32_t>(p.counts, p.counts, (int64_t)kRadixBins * p.ntiles,
+                                                           (uint32_t*)nullptr, p.partial, st)))
+                return TGL_ECUDA;
+            if (first && last)
+                radix_downsweep_kernel<kSrcStream, kDstTCSR><<<grid, kRadixThreads, 0, st>>>(
+                    s, kin, vin, n, shift, mask, p.counts, p.ntiles, kout, vout, nbr, ts_out, eid_out, nullptr);
+            else if (first)
+                radix_downsweep_kernel<kSrcStream, kDstKV><<<grid, kRadixThreads, 0, st>>>(
+                    s, kin, vin, n, shift, mask, p.counts, p.ntiles, kout, vout, nbr, ts_out, eid_out, nullptr);
+            else if (last)
+                radix_downsweep_kernel<kSrcKV, kDstTCSR><<<grid, kRadixThreads, 0, st>>>(
+                    s, kin, vin, n, shift, mask, p.counts, p.ntiles, kout, vout, nbr, ts_out, eid_out, nullptr);
+            else
+                radix_downsweep_kernel<kSrcKV, kDstKV><<<grid, kRadixThreads, 0, st>>>(
+                    s, kin, vin, n, shift, mask, p.counts, p.ntiles, kout, vout, nbr, ts_out, eid_out, nullptr);
+            if (cudaGetLastError() != cudaSuccess) return TGL_ECUDA;
+        }
+    }
+    return tgl_tcsr_wrap(indptr, nbr, ts_out, eid_out, n_nodes, (int64_t)es, out);
+}
+
+// ---------------------------------------------------------------------------- K8 shard bucketing
+// Node-sharded mode: stable counting sort of the roots by owner shard, the same
+// histogram -> scan -> stable-scatter pass as K3 with digit = owner (world <= 256).
+namespace tgl {
+
+__global__ void __launch_bounds__(256) owner_kernel(const int32_t* __restrict__ roots, int64_t n,
+                                                    const int64_t* __restrict__ splits, int32_t world,
+                                                    uint32_t* __restrict__ owner) {
+    __shared__ int64_t sp[kRadixBins + 1];
+    for (int r = threadIdx.x; r <= world; r += blockDim.x) sp[r] = splits[r];
+    __syncthreads();
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t v = roots[j];
+        // owner = last r with splits[r] <= v (out-of-range ids go to the nearest shard, which
+        // reports them through its own sampler error word)
+        int lo = 0, hi = world;  // search in [0, world)
+        while (hi - lo > 1) {
+            const int mid = (lo + hi) >> 1;
+            if (sp[mid] <= v)
+                lo = mid;
+            else
+                hi = mid;
+        }
+        owner[j] = (uint32_t)lo;
+    }
+}
+
+__global__ void shard_counts_kernel(const uint32_t* __restrict__ offsets, uint64_t ntiles, int32_t world, uint64_t n,
+                                    int64_t* __restrict__ counts) {
+    const int r = threadIdx.x;
+    if (r >= world) return;
+    const uint64_t a = offsets[(uint64_t)r * ntiles];
+    const uint64_t b = r + 1 < world ? offsets[(uint64_t)(r + 1) * ntiles] : n;
+    counts[r] = (int64_t)(b - a);
+}
+
+struct ShardPlan {
+    uint64_t ntiles;
+    uint32_t* owner;
+    uint32_t* counts;
+    uint64_t* partial;
+    size_t bytes;
+};
+
+static ShardPlan plan_shard(int64_t n, void* ws) {
+    ShardPlan p;
+    p.ntiles = ((uint64_t)n + kRadixTile - 1) / kRadixTile;
+    Carve c(ws);
+    p.owner = c.take<uint32_t>((size_t)std::max<int64_t>(n, 1));
+    p.counts = c.take<uint32_t>((size_t)kRadixBins * std::max<uint64_t>(p.ntiles, 1));
+    p.partial = c.take<uint64_t>(scan_workspace_bytes((int64_t)(kRadixBins * p.ntiles)) / sizeof(uint64_t));
+    p.bytes = c.bytes();
+    return p;
+}
+
+}  // namespace tgl
+
+extern "C" int tgl_shard_bucket_workspace(int64_t n_roots, int32_t world, size_t* bytes) {
+    if (!bytes || n_roots < 0 || world < 1 || world > kRadixBins) return TGL_EINVAL;
+    if ((uint64_t)n_roots >= (1ull << 32)) return TGL_EINVAL;
+    *bytes = plan_shard(n_roots, nullptr).bytes;
+    return TGL_OK;
+}
+
+extern "C" int tgl_shard_bucket(const int32_t* roots, int64_t n_roots, const int64_t* splits, int32_t world,
+                                int64_t* perm, int64_t* counts, void* workspace, size_t ws_bytes, void* stream) {
+    if (n_roots < 0 || world < 1 || world > kRadixBins || !splits || !counts || !workspace) return TGL_EINVAL;
+    if (n_roots > 0 && (!roots || !perm)) return TGL_EINVAL;
+    if ((uint64_t)n_roots >= (1ull << 32)) return TGL_EINVAL;
+    int rc = check_device();
+    if (rc) return rc;
+    ShardPlan p = plan_shard(n_roots, workspace);
+    if (ws_bytes < p.bytes) return TGL_EWORKSPACE;
+    cudaStream_t st = (cudaStream_t)stream;
+    if (n_roots == 0) return cuda_rc(cudaMemsetAsync(counts, 0, sizeof(int64_t) * world, st));
+    const int bits = world <= 1 ? 0 : 32 - __builtin_clz((unsigned)(world - 1));
+    const uint32_t mask = (1u << bits) - 1u;
+    const int64_t blocks = std::min<int64_t>((n_roots + 255) / 256, 148 * 8);
+    owner_kernel<<<(unsigned)blocks, 256, 0, st>>>(roots, n_roots, splits, world, p.owner);
+    Stream s{nullptr, nullptr, nullptr, nullptr, 0};
+    const unsigned grid = (unsigned)p.ntiles;
+    radix_upsweep_kernel<kSrcKeys><<<grid, kRadixThreads, 0, st>>>(s, p.owner, (uint64_t)n_roots, 0, mask, p.counts,
+                                                                     p.ntiles);
+    if (cuda_rc(exclusive_scan<uint32_t, uint32_t>(p.counts, p.counts, (int64_t)kRadixBins * p.ntiles,
+                                                   (uint32_t*)nullptr, p.partial, st)))
+        return TGL_ECUDA;
+    radix_downsweep_kernel<kSrcKeys, kDstPerm><<<grid, kRadixThreads, 0, st>>>(
+        s, p.owner, nullptr, (uint64_t)n_roots, 0, mask, p.counts, p.ntiles, nullptr, nullptr, nullptr, nullptr,
+        nullptr, perm);
+    shard_counts_kernel<<<1, kRadixBins, 0, st>>>(p.counts, p.ntiles, world, (uint64_t)n_roots, counts);
+    return cudaGetLastError() == cudaSuccess ? TGL_OK : TGL_ECUDA;
+}

@@ -1,0 +1,91 @@
+// common.cuh -- internal device helpers of libtgl.so (sm_100a).  Not part of the ABI.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/tgl.h"
+
+namespace tgl {
+
+constexpr uint32_t kFull = 0xffffffffu;
+
+// Sticky device error bits (one word per handle / one module-global word for gather).
+// Priority when mapping to a code: EINVAL > ERANGE > EUNSORTED (same order as the oracle's
+// validation, R#20-R#21).
+enum : int { kErrRange = 1, kErrInval = 2, kErrUnsorted = 4 };
+
+inline int err_bits_to_code(int bits) {
+    if (bits & kErrInval) return TGL_EINVAL;
+    if (bits & kErrRange) return TGL_ERANGE;
+    if (bits & kErrUnsorted) return TGL_EUNSORTED;
+    return TGL_OK;
+}
+
+// Philox4x32-10 (Salmon et al. SC'11), R#6.  Two 32x32->64 multiplies per round.
+__device__ __forceinline__ uint4 philox4x32_10(uint4 c, uint32_t k0, uint32_t k1) {
+#pragma unroll
+    for (int r = 0; r < 10; ++r) {
+        if (r) { k0 += 0x9E3779B9u; k1 += 0xBB67AE85u; }
+        const uint32_t hi0 = __umulhi(0xD2511F53u, c.x), lo0 = 0xD2511F53u * c.x;
+        const uint32_t hi1 = __umulhi(0xCD9E8D57u, c.z), lo1 = 0xCD9E8D57u * c.z;
+        c = make_uint4(hi1 ^ c.y ^ k0, lo1, hi0 ^ c.w ^ k1, lo0);
+    }
+    return c;
+}
+
+__device__ __forceinline__ uint32_t lanemask_lt() {
+    uint32_t m;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+    return m;
+}
+
+// Relaxed gpu-scope 64-bit load/store for the decoupled look-back state words.
+__device__ __forceinline__ uint64_t ld_relaxed_u64(const uint64_t* p) {
+    uint64_t v;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_relaxed_u64(uint64_t* p, uint64_t v) {
+    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// Streaming (evict-first) stores for outputs that are not re-read by this kernel.
+template <typename T>
+__device__ __forceinline__ void st_stream(T* p, T v) { __stcs(p, v); }
+
+inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+// Bump allocator over a caller workspace (256-byte aligned carve-outs).
+struct Carve {
+    char* base;
+    size_t off = 0;
+    explicit Carve(void* b) : base(static_cast<char*>(b)) {}
+    template <typename T>
+    T* take(size_t n) {
+        off = align_up(off, 256);
+        T* p = base ? reinterpret_cast<T*>(base + off) : nullptr;
+        off += n * sizeof(T);
+        return p;
+    }
+    size_t bytes() const { return align_up(off, 256); }
+};
+
+// Device-capability gate: the library is compiled for sm_100a only.
+int check_device();
+
+// Map the last CUDA error (launch or API) to TGL_ECUDA.
+inline int cuda_rc(cudaError_t e) { return e == cudaSuccess ? TGL_OK : TGL_ECUDA; }
+
+}  // namespace tgl
+
+struct tgl_tcsr {
+    const int64_t* indptr;
+    const int32_t* nbr;
+    const float* ts;
+    const int32_t* eid;
+    int32_t n_nodes;
+    int64_t n_stored;
+    int* err_dev;  // sticky device error word of this handle (cudaMalloc at creation)
+    int device;
+};
