@@ -24,7 +24,7 @@ from ._lib import MOST_RECENT, UNIFORM, TGLError
 
 _L = _lib.load()
 
-__all__ = ["TCSR", "Block", "Sampler", "build", "wrap", "sample", "gather", "check", "shard_bucket",
+__all__ = ["TCSR", "Block", "Sampler", "build", "wrap", "index_bytes", "sample", "gather", "check", "shard_bucket",
            "MOST_RECENT", "UNIFORM", "TGLError", "lib_path"]
 
 lib_path = _lib.LIB_PATH
@@ -59,10 +59,12 @@ def _strategy(s) -> int:
 
 
 class TCSR:
-    """A built T-CSR: indptr int64 [V+1]; nbr int32, ts float32, eid int32 [E_s]."""
+    """A built T-CSR: indptr int64 [V+1]; nbr int32, ts float32, eid int32 [E_s] (+ ts sector index)."""
 
-    def __init__(self, indptr, nbr, ts, eid, n_nodes, handle):
+    def __init__(self, indptr, nbr, ts, eid, n_nodes, handle, index=None, ts_storage=None):
         self.indptr, self.nbr, self.ts, self.eid = indptr, nbr, ts, eid
+        self.index = index
+        self._ts_storage = ts_storage
         self.n_nodes = int(n_nodes)
         self.n_stored = int(nbr.numel())
         self._h = handle
@@ -84,9 +86,22 @@ def build_workspace_bytes(n_edges: int, n_nodes: int, add_reverse: bool) -> int:
     return b.value
 
 
+def index_bytes(n_stored: int) -> int:
+    b = ctypes.c_size_t()
+    _rc(_L.tgl_tcsr_index_bytes(int(n_stored), ctypes.byref(b)), "tgl_tcsr_index_bytes")
+    return b.value
+
+
+def _ts_buffer(n: int, dev) -> (torch.Tensor, torch.Tensor):
+    """float32 [n] view of a buffer padded to a multiple of 8 floats (sector-group reads)."""
+    storage = torch.empty(max((n + 7) // 8 * 8, 8), dtype=torch.float32, device=dev)
+    return storage[:n], storage
+
+
 def build(src: torch.Tensor, dst: torch.Tensor, ts: torch.Tensor, eid: Optional[torch.Tensor] = None, *,
-          n_nodes: int, add_reverse: bool, workspace: Optional[torch.Tensor] = None, stream=None) -> TCSR:
-    """tgl_tcsr_build: T-CSR of a chronological stream."""
+          n_nodes: int, add_reverse: bool, workspace: Optional[torch.Tensor] = None, with_index: bool = True,
+          stream=None) -> TCSR:
+    """tgl_tcsr_build: T-CSR of a chronological stream + the ts sector index."""
     src = _cuda(src, torch.int32, "src")
     dst = _cuda(dst, torch.int32, "dst")
     ts = _cuda(ts, torch.float32, "ts")
@@ -97,28 +112,37 @@ def build(src: torch.Tensor, dst: torch.Tensor, ts: torch.Tensor, eid: Optional[
     dev = src.device
     indptr = torch.empty(n_nodes + 1, dtype=torch.int64, device=dev)
     nbr = torch.empty(Es, dtype=torch.int32, device=dev)
-    ts_out = torch.empty(Es, dtype=torch.float32, device=dev)
+    ts_out, ts_storage = _ts_buffer(Es, dev)
     eid_out = torch.empty(Es, dtype=torch.int32, device=dev)
+    ib = index_bytes(Es) if with_index else 0
+    index = torch.empty(ib, dtype=torch.uint8, device=dev) if with_index else None
     wsb = build_workspace_bytes(E, n_nodes, add_reverse)
     if workspace is None or workspace.numel() < wsb:
         workspace = torch.empty(max(wsb, 1), dtype=torch.uint8, device=dev)
     h = ctypes.c_void_p()
     _rc(_L.tgl_tcsr_build(_ptr(src), _ptr(dst), _ptr(ts), _ptr(eid), E, int(n_nodes), int(add_reverse),
-                          _ptr(indptr), _ptr(nbr), _ptr(ts_out), _ptr(eid_out), _ptr(workspace), wsb,
-                          _stream(stream), ctypes.byref(h)), "tgl_tcsr_build")
-    return TCSR(indptr, nbr, ts_out, eid_out, n_nodes, h)
+                          _ptr(indptr), _ptr(nbr), _ptr(ts_storage), _ptr(eid_out), _ptr(index), ib,
+                          _ptr(workspace), wsb, _stream(stream), ctypes.byref(h)), "tgl_tcsr_build")
+    return TCSR(indptr, nbr, ts_out, eid_out, n_nodes, h, index, ts_storage)
 
 
-def wrap(indptr: torch.Tensor, nbr: torch.Tensor, ts: torch.Tensor, eid: torch.Tensor) -> TCSR:
+def wrap(indptr: torch.Tensor, nbr: torch.Tensor, ts: torch.Tensor, eid: torch.Tensor, *,
+         with_index: bool = True, stream=None) -> TCSR:
     """tgl_tcsr_wrap: handle over existing T-CSR arrays (e.g. broadcast from another rank)."""
     indptr = _cuda(indptr, torch.int64, "indptr")
     nbr = _cuda(nbr, torch.int32, "nbr")
-    ts = _cuda(ts, torch.float32, "ts")
     eid = _cuda(eid, torch.int32, "eid")
+    n = nbr.numel()
+    ts_view, ts_storage = _ts_buffer(n, nbr.device)
+    ts_view.copy_(_cuda(ts, torch.float32, "ts"))
+    ib = index_bytes(n) if with_index else 0
+    index = torch.empty(ib, dtype=torch.uint8, device=nbr.device) if with_index else None
+    if with_index:
+        _rc(_L.tgl_tcsr_index_build(_ptr(ts_storage), n, _ptr(index), ib, _stream(stream)), "tgl_tcsr_index_build")
     h = ctypes.c_void_p()
-    _rc(_L.tgl_tcsr_wrap(_ptr(indptr), _ptr(nbr), _ptr(ts), _ptr(eid), indptr.numel() - 1, nbr.numel(),
-                         ctypes.byref(h)), "tgl_tcsr_wrap")
-    return TCSR(indptr, nbr, ts, eid, indptr.numel() - 1, h)
+    _rc(_L.tgl_tcsr_wrap(_ptr(indptr), _ptr(nbr), _ptr(ts_storage), _ptr(eid), _ptr(index), ib,
+                         indptr.numel() - 1, n, ctypes.byref(h)), "tgl_tcsr_wrap")
+    return TCSR(indptr, nbr, ts_view, eid, indptr.numel() - 1, h, index, ts_storage)
 
 
 @dataclass

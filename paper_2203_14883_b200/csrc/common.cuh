@@ -88,4 +88,7 @@ struct tgl_tcsr {
     int64_t n_stored;
     int* err_dev;  // sticky device error word of this handle (cudaMalloc at creation)
     int device;
+    const float* index;      // 8-ary sector index over ts (tsindex.cuh), or null
+    int n_levels;
+    uint64_t level_off[12];  // float offset of level l in index
 };

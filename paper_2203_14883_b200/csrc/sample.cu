@@ -1,24 +1,27 @@
 // sample.cu -- the parallel temporal sampler of TGL (Alg. 1) on B200.
 //
-// One kernel launch per (layer, chain).  Layer 0 is a single chain covering all S dynamic
-// snapshots of a root in one pass (the S+1 cuts of a root share its indptr pair and narrow
-// each other's search range); a layer l >= 1 runs one chain per snapshot s whose roots are
-// block (l-1, s)'s outputs (Alg. 1, R#3).
+// Per layer chain (layer 0: one chain covering all S dynamic snapshots of a root, whose S+1 cuts
+// share the indptr pair and narrow each other's range; layer l >= 1: one chain per snapshot s
+// whose roots are block (l-1, s)'s outputs, Alg. 1, R#3) three kernels run on the
+// caller's stream, with no inter-CTA waiting anywhere:
 //
-// A CTA owns a tile of 256 consecutive roots (tile index from an atomic ticket, so tiles start in
-// order and the look-back below always waits on running or finished CTAs):
-//   phase 1  one thread per root: indptr pair (16 B), S+1 cut searches by binary search over
-//            the node's time-sorted list (Sec. 3.1 "Sampling", L260-L262: the stateless
-//            replacement of the per-node pointers pt_0..pt_S), selection:
-//              most_recent -> [max(a, b-k), b)           ("closest to the end pointer")
-//              uniform     -> all of [a, b) if c <= k, else Floyd's k-subset with Philox4x32-10
-//                             draws, sorted ascending (R#5, R#6)
-//   phase 2  block scan of per-root counts + decoupled look-back across tiles (one chained
-//            scan per snapshot) -> deterministic CSR offsets without a second pass (K5)
-//   phase 3  the tile's outputs are copied as one flat range: thread o finds its root by a
-//            binary search over the tile's inclusive counts in shared memory, so loads of
-//            (nbr, eid, ts) and stores of (nbr, eid, dt[, ts_edge, child key, child lo]) are
-//            coalesced and every lane is busy (a9, a10; K6 fused).
+//   K4a window_kernel  one lane per root: indptr pair (16 B), S+1 cut searches (lower_bound) over
+//                      the node's time-sorted list through the 8-ary sector index (tsindex.cuh),
+//                      the stateless replacement of the paper's per-node pointers pt_0..pt_S
+//                      (Sec. 3.1 "Sampling", L260-L262).  Writes per (snapshot, root) the window
+//                      descriptor (first slot, size) and per (snapshot, CTA tile) the number of
+//                      edges the tile will emit:  most_recent -> min(k, c) ("closest to the
+//                      end pointer"); uniform -> min(k, c) (R#5).
+//   K5  tile_scan      one CTA: exclusive scan of the per-tile totals -> tile bases, nnz, n_roots,
+//                      offsets[n] (deterministic CSR offsets, no atomics deciding positions).
+//   K4b copy_kernel    one warp per 32 roots: warp scan of its counts + tile base -> offsets[i];
+//                      uniform: Floyd's k-subset with Philox4x32-10 draws, ascending (R#5, R#6);
+//                      then the tile's outputs are copied as one flat range per snapshot -- lane o
+//                      finds its root by a 5-step search over the warp's inclusive counts -- so
+//                      loads of (nbr, eid, ts) and stores of (nbr, eid, dt[, ts_edge, child key,
+//                      child lo]) are coalesced runs and every lane is busy (a9, a10; K6 fused).
+// The per-root window descriptors (8 B per root and snapshot) live in the caller's workspace and
+// are normally still L2-resident when K4b reads them.
 // dt = t_root (-) t_edge with __fsub_rn; window bounds with __fmul_rn / __fsub_rn (R#12).
 // Everything strictly before the root: ts < U = t.
 #include <algorithm>
@@ -26,14 +29,14 @@
 #include <cstring>
 
 #include "common.cuh"
+#include "tsindex.cuh"
 
 namespace tgl {
 
-constexpr int kSampleThreads = 256;  // roots per tile
+constexpr int kSampleThreads = 256;  // roots per CTA tile (one lane per root)
 constexpr int kSampleWarps = kSampleThreads / 32;
 constexpr int kCopyUnroll = 4;
-constexpr uint64_t kFlagAgg = 1ull << 62, kFlagPrefix = 2ull << 62, kValMask = (1ull << 62) - 1;
-constexpr size_t kPicksSmemLimit = 64 * 1024;
+constexpr int kPicksSmemPerWarp = 8 * 1024;  // bytes of uniform picks kept in shared memory per warp
 
 struct BlockOut {
     int64_t* offsets;
@@ -52,6 +55,8 @@ struct SampleParams {
     const int32_t* nbr;
     const float* ts;
     const int32_t* eid;
+    const float* lvl[kMaxIndexLevels + 1];  // lvl[l] = index level l (1-based)
+    int32_t n_levels;                       // < 0 -> plain binary search
     int32_t n_nodes;
     const int32_t* root_node;
     const float* root_ts;
@@ -63,108 +68,117 @@ struct SampleParams {
     int32_t layer, nsb, snap0, k;
     float snapshot_len;
     uint32_t seed_lo, seed_hi;
-    uint64_t* tile_state;  // [nsb][tiles_cap], zeroed before the launch
-    uint32_t* tile_counter;
-    int64_t tiles_cap;
-    uint32_t* picks_global;  // null -> picks in shared memory
+    uint32_t* win_first;  // [nsb][cap] first slot of the window (uniform: a; most_recent: b - take)
+    uint32_t* win_len;    // [nsb][cap] uniform: window size c; most_recent: take = min(k, c)
+    uint32_t* tile_tot;   // [nsb][tiles_cap] edges emitted per CTA tile
+    uint64_t* tile_base;  // [nsb][tiles_cap] exclusive prefix of tile_tot
+    int64_t roots_cap, tiles_cap;
+    uint32_t* picks_global;  // null -> picks in shared memory; else [tiles_cap*8 warps][nsb*k][32]
     int* err;
     BlockOut out[TGL_MAX_SNAPSHOTS];
 };
 
-// First slot p in [lo, hi) with ts[p] >= x (else hi): the cut of a window (R#2).
-__device__ __forceinline__ uint32_t lower_bound_ts(const float* __restrict__ ts, uint32_t lo, uint32_t hi, float x) {
-    while (lo < hi) {
-        const uint32_t mid = lo + ((hi - lo) >> 1);
-        if (__ldg(ts + mid) < x)
-            lo = mid + 1;
-        else
-            hi = mid;
-    }
-    return lo;
-}
-
-__device__ __forceinline__ uint64_t warp_sum_u64(uint64_t v) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
-    return v;
-}
-
-// Block-wide exclusive scan (uint32 counts, uint64 totals).
-__device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t* total, uint32_t* sm /*[kSampleWarps+1]*/) {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    uint32_t x = v;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t y = __shfl_up_sync(kFull, x, o);
-        if (lane >= o) x += y;
-    }
-    if (lane == 31) sm[warp] = x;
-    __syncthreads();
-    if (warp == 0) {
-        const uint32_t w = lane < kSampleWarps ? sm[lane] : 0;
-        uint32_t wi = w;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t y = __shfl_up_sync(kFull, wi, o);
-            if (lane >= o) wi += y;
-        }
-        if (lane < kSampleWarps) sm[lane] = wi - w;
-        if (lane == kSampleWarps - 1) sm[kSampleWarps] = wi;
-    }
-    __syncthreads();
-    const uint32_t r = sm[warp] + x - v;
-    *total = sm[kSampleWarps];
-    __syncthreads();
-    return r;
-}
-
-template <int STRATEGY>
-__global__ void __launch_bounds__(kSampleThreads) sample_kernel(const __grid_constant__ SampleParams p) {
-    extern __shared__ __align__(16) unsigned char smem[];
-    __shared__ uint32_t s_scan[kSampleWarps + 1];
-    __shared__ uint64_t s_base[TGL_MAX_SNAPSHOTS];
-    __shared__ uint32_t s_tot[TGL_MAX_SNAPSHOTS];
-    __shared__ uint32_t s_tile;
-
-    constexpr int R = kSampleThreads;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int nsb = p.nsb;
-    const int k = p.k;
-
-    uint32_t* incl = reinterpret_cast<uint32_t*>(smem);  // [nsb][R] counts -> inclusive prefix
-    uint32_t* start = incl + nsb * R;                      // [nsb][R] first slot (most_recent) / a (uniform)
-    float* troot = reinterpret_cast<float*>(start + nsb * R);  // [R]
-    float* lo_r = troot + R;                                    // [nsb][R] window lower bound L
-    uint64_t* rkey = reinterpret_cast<uint64_t*>(lo_r + nsb * R);  // [R] (offset is a multiple of 2R floats)
-
-    if (tid == 0) s_tile = atomicAdd(p.tile_counter, 1u);
-    __syncthreads();
-    const uint32_t tile = s_tile;
-
+__device__ __forceinline__ int64_t chain_roots(const SampleParams& p) {
     int64_t n = p.n_roots;
     if (p.n_roots_dev_in) {
         const int64_t m = *p.n_roots_dev_in;
         n = m < n ? m : n;
     }
-    if (n <= 0) {
-        if (tile == 0 && tid < nsb) {
-            p.out[tid].offsets[0] = 0;
-            *p.out[tid].nnz_dev = 0;
-            *p.out[tid].n_roots_dev = 0;
+    return n > 0 ? n : 0;
+}
+
+// ---------------------------------------------------------------------------- cut search
+struct F8 {
+    float4 a, b;
+};
+
+__device__ __forceinline__ F8 ldg8(const float* __restrict__ p) {  // p is 32-byte aligned
+    F8 r;
+    r.a = __ldg(reinterpret_cast<const float4*>(p));
+    r.b = __ldg(reinterpret_cast<const float4*>(p) + 1);
+    return r;
+}
+
+// bit i set iff element i of the group is < x
+__device__ __forceinline__ uint32_t lt_mask(const F8& g, float x) {
+    return (uint32_t)(g.a.x < x) | ((uint32_t)(g.a.y < x) << 1) | ((uint32_t)(g.a.z < x) << 2) |
+           ((uint32_t)(g.a.w < x) << 3) | ((uint32_t)(g.b.x < x) << 4) | ((uint32_t)(g.b.y < x) << 5) |
+           ((uint32_t)(g.b.z < x) << 6) | ((uint32_t)(g.b.w < x) << 7);
+}
+
+// mask of positions [from, to) of group g (positions are global indices, group = 8 entries)
+__device__ __forceinline__ uint32_t range_bits(uint64_t g, uint64_t from, uint64_t to) {
+    const uint64_t g0 = g << 3;
+    const int lo = from > g0 ? (int)(from - g0) : 0;
+    const int hi = to < g0 + 8 ? (int)(to - g0) : 8;
+    if (hi <= lo) return 0u;
+    return ((1u << hi) - 1u) & ~((1u << lo) - 1u);
+}
+
+// number of entries of arr[from, to) that are < x, for to - from <= 16 (spans <= 3 groups)
+__device__ __forceinline__ uint32_t count_lt_small(const float* __restrict__ arr, uint64_t from, uint64_t to,
+                                                   float x) {
+    if (to <= from) return 0;
+    const uint64_t g0 = from >> 3, g1 = (to - 1) >> 3;
+    uint32_t c = __popc(lt_mask(ldg8(arr + (g0 << 3)), x) & range_bits(g0, from, to));
+    if (g1 > g0) c += __popc(lt_mask(ldg8(arr + ((g0 + 1) << 3)), x) & range_bits(g0 + 1, from, to));
+    if (g1 > g0 + 1) c += __popc(lt_mask(ldg8(arr + ((g0 + 2) << 3)), x) & range_bits(g0 + 2, from, to));
+    return c;
+}
+
+// first slot p in [a, b) with ts[p] >= x, else b (R#2).  Index path: one aligned sector per level.
+__device__ __forceinline__ uint32_t lower_bound_ts(const SampleParams& p, uint32_t a, uint32_t b, float x) {
+    if (a >= b) return a;
+    if (p.n_levels < 0) {  // plain binary search (index absent or ts not 32-byte aligned)
+        while (a < b) {
+            const uint32_t mid = a + ((b - a) >> 1);
+            if (__ldg(p.ts + mid) < x)
+                a = mid + 1;
+            else
+                b = mid;
         }
-        return;
+        return a;
     }
-    const int64_t base_i = (int64_t)tile * R;
-    if (base_i >= n) return;  // capacity-sized grid: nobody waits on tiles past the end
-    const int64_t i = base_i + tid;
+    uint64_t A = a, B = b;
+    if (B - A > 16) {
+        int l = 1;
+        while (l < p.n_levels &&
+               ((B + (1ull << (3 * l)) - 1) >> (3 * l)) - ((A + (1ull << (3 * l)) - 1) >> (3 * l)) > 8)
+            ++l;
+        for (; l >= 1; --l) {
+            const int sh = 3 * l;
+            const uint64_t j0 = (A + (1ull << sh) - 1) >> sh, j1 = (B + (1ull << sh) - 1) >> sh;
+            if (j1 <= j0) continue;
+            const uint32_t m = count_lt_small(p.lvl[l], j0, j1, x);  // j1 - j0 <= 8
+            if (m > 0) A = ((j0 + m - 1) << sh) + 1;
+            if (j0 + m < j1) B = (j0 + m) << sh;
+        }
+    }
+    return (uint32_t)(A + count_lt_small(p.ts, A, B, x));
+}
+
+__device__ __forceinline__ uint32_t warp_incl_scan(uint32_t x, int lane) {
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(kFull, x, o);
+        if (lane >= o) x += y;
+    }
+    return x;
+}
+
+// ---------------------------------------------------------------------------- K4a windows
+template <int STRATEGY>
+__global__ void __launch_bounds__(kSampleThreads) window_kernel(const __grid_constant__ SampleParams p) {
+    __shared__ uint32_t s_red[TGL_MAX_SNAPSHOTS][kSampleWarps];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t n = chain_roots(p);
+    const int64_t base_i = (int64_t)blockIdx.x * kSampleThreads;
+    if (base_i >= n) return;  // capacity-sized grid (l >= 1): tiles past the end do nothing
+    const int64_t i = base_i + threadIdx.x;
     const bool valid = i < n;
+    const int nsb = p.nsb;
+    const uint32_t k = (uint32_t)p.k;
 
-    uint32_t* picks = nullptr;
-    if (STRATEGY == TGL_UNIFORM)
-        picks = p.picks_global ? p.picks_global + (size_t)tile * nsb * k * R
-                               : reinterpret_cast<uint32_t*>(rkey + R);
-
-    // ------------------------------------------------------------------ phase 1: cuts + selection
     int32_t v = 0;
     float t = 0.0f;
     bool ok = false;
@@ -178,148 +192,203 @@ __global__ void __launch_bounds__(kSampleThreads) sample_kernel(const __grid_con
         else
             ok = true;
     }
-    troot[tid] = t;
-    uint64_t rk = 0;
-    if (STRATEGY == TGL_UNIFORM) {
-        rk = p.layer == 0 ? p.root_key_base + (uint64_t)i : (valid ? p.root_key[i] : 0ull);
-        rkey[tid] = rk;
-    }
     float lin = -INFINITY;
     if (p.layer > 0 && p.root_lo && ok) lin = p.root_lo[i];
-
     uint32_t lo = 0, hi = 0;
     if (ok) {
         lo = (uint32_t)__ldg(p.indptr + v);
         hi = (uint32_t)__ldg(p.indptr + v + 1);
     }
-    // U of window 0 is the root's own time t (both for layer 0 and for hop roots)
-    uint32_t bcur = ok ? lower_bound_ts(p.ts, lo, hi, t) : lo;
+    // U of window 0 is the root's own time t.  A list that starts at or after t has no candidate
+    // in any window (one sector answers every cut).
+    uint32_t bcur = lo;
+    if (lo < hi && __ldg(p.ts + lo) < t) bcur = lower_bound_ts(p, lo, hi, t);
     for (int b = 0; b < nsb; ++b) {
         // lower bound of window b: layer 0 -> t (-) ((b+1) (x) t_s); l >= 1 -> inherited
         const float x = p.layer == 0 ? __fsub_rn(t, __fmul_rn((float)(b + 1), p.snapshot_len)) : lin;
-        const uint32_t a = (ok && x > -INFINITY) ? lower_bound_ts(p.ts, lo, bcur, x) : lo;
-        const uint32_t c = ok ? bcur - a : 0u;
-        const uint32_t take = c < (uint32_t)k ? c : (uint32_t)k;
-        incl[b * R + tid] = take;
-        lo_r[b * R + tid] = x;
-        if (STRATEGY == TGL_MOST_RECENT) {
-            start[b * R + tid] = bcur - take;
-        } else {
-            start[b * R + tid] = a;
-            uint32_t* pk = picks + (size_t)b * k * R + tid;  // pick q at pk[q * R]
-            if (c <= (uint32_t)k) {
-                for (uint32_t q = 0; q < c; ++q) pk[q * R] = q;
+        uint32_t a = lo;
+        if (x > -INFINITY && bcur > lo)  // empty window when the element before the cut is < x
+            a = __ldg(p.ts + bcur - 1) < x ? bcur : lower_bound_ts(p, lo, bcur - 1, x);
+        const uint32_t c = bcur - a;
+        const uint32_t take = c < k ? c : k;
+        if (valid) {
+            p.win_first[(size_t)b * p.roots_cap + i] = STRATEGY == TGL_MOST_RECENT ? bcur - take : a;
+            p.win_len[(size_t)b * p.roots_cap + i] = STRATEGY == TGL_MOST_RECENT ? take : c;
+        }
+        uint32_t s = take;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(kFull, s, o);
+        if (lane == 0) s_red[b][warp] = s;
+        bcur = a;
+    }
+    __syncthreads();
+    if (threadIdx.x < nsb) {
+        uint32_t s = 0;
+#pragma unroll
+        for (int w = 0; w < kSampleWarps; ++w) s += s_red[threadIdx.x][w];
+        p.tile_tot[(size_t)threadIdx.x * p.tiles_cap + blockIdx.x] = s;
+    }
+}
+
+// ---------------------------------------------------------------------------- K5 tile scan
+__global__ void __launch_bounds__(1024) tile_scan_kernel(const __grid_constant__ SampleParams p) {
+    __shared__ uint64_t sm[33];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t n = chain_roots(p);
+    const int64_t tiles = (n + kSampleThreads - 1) / kSampleThreads;
+    for (int b = 0; b < p.nsb; ++b) {
+        const uint32_t* tot = p.tile_tot + (size_t)b * p.tiles_cap;
+        uint64_t* base = p.tile_base + (size_t)b * p.tiles_cap;
+        uint64_t carry = 0;
+        for (int64_t t0 = 0; t0 < tiles; t0 += 1024) {
+            const int64_t t = t0 + threadIdx.x;
+            const uint64_t v = t < tiles ? tot[t] : 0;
+            uint64_t x = v;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint64_t y = __shfl_up_sync(kFull, x, o);
+                if (lane >= o) x += y;
+            }
+            if (lane == 31) sm[warp] = x;
+            __syncthreads();
+            if (warp == 0) {
+                const uint64_t w = sm[lane];
+                uint64_t wi = w;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const uint64_t y = __shfl_up_sync(kFull, wi, o);
+                    if (lane >= o) wi += y;
+                }
+                sm[lane] = wi - w;
+                if (lane == 31) sm[32] = wi;
+            }
+            __syncthreads();
+            if (t < tiles) base[t] = carry + sm[warp] + x - v;
+            carry += sm[32];
+            __syncthreads();
+        }
+        if (threadIdx.x == 0) {
+            const BlockOut& o = p.out[b];
+            o.offsets[n] = (int64_t)carry;
+            *o.nnz_dev = (int64_t)carry;
+            *o.n_roots_dev = n;
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------- K4b copy
+__host__ __device__ inline int copy_warp_words(int nsb, int k, bool picks_in_smem) {
+    return 2 * nsb * 32 + 32 + 2 * 32 + 2 * nsb + (picks_in_smem ? nsb * k * 32 : 0);
+}
+
+template <int STRATEGY>
+__global__ void __launch_bounds__(kSampleThreads) copy_kernel(const __grid_constant__ SampleParams p) {
+    extern __shared__ __align__(16) uint32_t smem[];
+    __shared__ uint32_t s_wsum[TGL_MAX_SNAPSHOTS][kSampleWarps];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t n = chain_roots(p);
+    const int64_t base_i = (int64_t)blockIdx.x * kSampleThreads;
+    if (base_i >= n) return;
+    const int64_t i = base_i + threadIdx.x;
+    const bool valid = i < n;
+    const int nsb = p.nsb;
+    const int k = p.k;
+    const bool picks_smem = STRATEGY == TGL_UNIFORM && p.picks_global == nullptr;
+    uint32_t* ws = smem + warp * copy_warp_words(nsb, k, picks_smem);
+    uint32_t* inc = ws;                                         // [nsb][32] inclusive counts
+    uint32_t* first = inc + nsb * 32;                           // [nsb][32]
+    float* troot = reinterpret_cast<float*>(first + nsb * 32);  // [32]
+    uint64_t* rkey = reinterpret_cast<uint64_t*>(troot + 32);   // [32] (even word offset)
+    uint64_t* base = rkey + 32;                                 // [nsb]
+    uint32_t* picks = nullptr;
+    if (STRATEGY == TGL_UNIFORM)
+        picks = picks_smem ? reinterpret_cast<uint32_t*>(base + nsb)
+                           : p.picks_global + ((size_t)blockIdx.x * kSampleWarps + warp) * nsb * k * 32;
+
+    const float t = valid ? p.root_ts[i] : 0.0f;
+    troot[lane] = t;
+    uint64_t rk = 0;
+    if (STRATEGY == TGL_UNIFORM) {
+        rk = p.layer == 0 ? p.root_key_base + (uint64_t)i : (valid ? p.root_key[i] : 0ull);
+        rkey[lane] = rk;
+    }
+    // counts, warp-local prefix, window descriptors; uniform picks
+    for (int b = 0; b < nsb; ++b) {
+        uint32_t f = 0, len = 0;
+        if (valid) {
+            f = p.win_first[(size_t)b * p.roots_cap + i];
+            len = p.win_len[(size_t)b * p.roots_cap + i];
+        }
+        const uint32_t take = STRATEGY == TGL_MOST_RECENT ? len : (len < (uint32_t)k ? len : (uint32_t)k);
+        first[b * 32 + lane] = f;
+        const uint32_t x = warp_incl_scan(take, lane);
+        inc[b * 32 + lane] = x;
+        if (lane == 31) s_wsum[b][warp] = x;
+        if (STRATEGY == TGL_UNIFORM) {
+            uint32_t* pk = picks + (size_t)b * k * 32 + lane;  // pick q at pk[q * 32]
+            if (len <= (uint32_t)k) {
+                for (uint32_t q = 0; q < len; ++q) pk[q * 32] = q;
             } else {
                 // Floyd: for m = c-k .. c-1, r uniform in [0, m]; take r unless taken, else m
                 const uint32_t ctr1 = ((uint32_t)p.layer << 16) | (uint32_t)(p.layer == 0 ? b : p.snap0);
                 for (int j = 0; j < k; ++j) {
-                    const uint32_t m = c - (uint32_t)k + (uint32_t)j;
+                    const uint32_t m = len - (uint32_t)k + (uint32_t)j;
                     const uint4 rnd = philox4x32_10(make_uint4((uint32_t)j, ctr1, (uint32_t)rk, (uint32_t)(rk >> 32)),
                                                     p.seed_lo, p.seed_hi);
                     const uint32_t r = __umulhi(rnd.x, m + 1u);
                     bool taken = false;
-                    for (int q = 0; q < j; ++q) taken |= (pk[q * R] == r);
-                    pk[j * R] = taken ? m : r;
+                    for (int q = 0; q < j; ++q) taken |= (pk[q * 32] == r);
+                    pk[j * 32] = taken ? m : r;
                 }
                 for (int j = 1; j < k; ++j) {  // ascending slot order (R#13)
-                    const uint32_t xj = pk[j * R];
+                    const uint32_t xj = pk[j * 32];
                     int q = j - 1;
-                    while (q >= 0 && pk[q * R] > xj) {
-                        pk[(q + 1) * R] = pk[q * R];
+                    while (q >= 0 && pk[q * 32] > xj) {
+                        pk[(q + 1) * 32] = pk[q * 32];
                         --q;
                     }
-                    pk[(q + 1) * R] = xj;
+                    pk[(q + 1) * 32] = xj;
                 }
             }
         }
-        bcur = a;
     }
     __syncthreads();
-
-    // ------------------------------------------------------------------ phase 2: offsets
     for (int b = 0; b < nsb; ++b) {
-        const uint32_t c = incl[b * R + tid];
-        uint32_t tot;
-        const uint32_t ex = block_excl_scan(c, &tot, s_scan);
-        incl[b * R + tid] = ex + c;
-        if (tid == 0) s_tot[b] = tot;
+        uint64_t wb = p.tile_base[(size_t)b * p.tiles_cap + blockIdx.x];
+        for (int w = 0; w < warp; ++w) wb += s_wsum[b][w];
+        if (lane == 0) base[b] = wb;
+        const uint32_t x = inc[b * 32 + lane];
+        const uint32_t ex = lane ? inc[b * 32 + lane - 1] : 0u;
+        if (valid) p.out[b].offsets[i] = (int64_t)(wb + ex);
+        (void)x;
     }
-    __syncthreads();
-    for (int b = warp; b < nsb; b += kSampleWarps) {
-        uint64_t* st = p.tile_state + (size_t)b * p.tiles_cap;
-        const uint64_t agg = s_tot[b];
-        if (lane == 0) st_relaxed_u64(st + tile, (tile == 0 ? kFlagPrefix : kFlagAgg) | agg);
-        uint64_t excl = 0;
-        if (tile > 0) {
-            int64_t pred = (int64_t)tile - 1;
-            while (true) {
-                const int64_t idx = pred - lane;
-                uint64_t w = idx >= 0 ? ld_relaxed_u64(st + idx) : kFlagPrefix;
-                while (__any_sync(kFull, (w >> 62) == 0)) {
-                    if ((w >> 62) == 0) w = ld_relaxed_u64(st + idx);
-                }
-                const uint32_t pm = __ballot_sync(kFull, (w >> 62) == 2);
-                uint64_t val = w & kValMask;
-                if (pm) {
-                    const int first = __ffs(pm) - 1;
-                    if (lane > first) val = 0;
-                    excl += warp_sum_u64(val);
-                    break;
-                }
-                excl += warp_sum_u64(val);
-                pred -= 32;
-            }
-            if (lane == 0) st_relaxed_u64(st + tile, kFlagPrefix | (excl + agg));
-        }
-        if (lane == 0) s_base[b] = excl;
-    }
-    __syncthreads();
+    __syncwarp();
 
-    const bool last_tile = base_i + R >= n;
     for (int b = 0; b < nsb; ++b) {
         const BlockOut& o = p.out[b];
-        const uint32_t inc = incl[b * R + tid];
-        const uint32_t ex = tid ? incl[b * R + tid - 1] : 0u;
-        if (valid) o.offsets[i] = (int64_t)(s_base[b] + ex);
-        if (last_tile && i == n - 1) {
-            const int64_t total = (int64_t)(s_base[b] + inc);
-            o.offsets[n] = total;
-            *o.nnz_dev = total;
-            *o.n_roots_dev = n;
-        }
-    }
-
-    // ------------------------------------------------------------------ phase 3: flat copy
-    for (int b = 0; b < nsb; ++b) {
-        const BlockOut& o = p.out[b];
-        const uint32_t T = s_tot[b];
-        const uint64_t B = s_base[b];
-        const uint32_t* inc = incl + b * R;
-        const uint32_t* stb = start + b * R;
-        for (uint32_t o0 = 0; o0 < T; o0 += R * kCopyUnroll) {
+        const uint32_t* incb = inc + b * 32;
+        const uint32_t T = incb[31];
+        const uint64_t B = base[b];
+        const uint32_t* fb = first + b * 32;
+        for (uint32_t o0 = 0; o0 < T; o0 += 32 * kCopyUnroll) {
             uint32_t pos[kCopyUnroll], rr[kCopyUnroll], qq[kCopyUnroll];
             bool act[kCopyUnroll];
 #pragma unroll
             for (int u = 0; u < kCopyUnroll; ++u) {
-                const uint32_t oi = o0 + (uint32_t)(u * R + tid);
+                const uint32_t oi = o0 + (uint32_t)(u * 32 + lane);
                 act[u] = oi < T;
-                // root of output oi: first r with inc[r] > oi
-                uint32_t lo2 = 0, hi2 = R;
-                while (lo2 < hi2) {
-                    const uint32_t mid = (lo2 + hi2) >> 1;
-                    if (inc[mid] <= oi)
-                        lo2 = mid + 1;
-                    else
-                        hi2 = mid;
-                }
-                const uint32_t r = act[u] ? lo2 : 0u;
-                const uint32_t q = act[u] ? oi - (r ? inc[r - 1] : 0u) : 0u;
+                uint32_t r = 0;  // root of output oi: first r with incb[r] > oi
+#pragma unroll
+                for (int s2 = 16; s2 > 0; s2 >>= 1)
+                    if (incb[r + s2 - 1] <= oi) r += s2;
+                r = act[u] ? r : 0u;
+                const uint32_t q = act[u] ? oi - (r ? incb[r - 1] : 0u) : 0u;
                 rr[u] = r;
                 qq[u] = q;
                 if (STRATEGY == TGL_MOST_RECENT)
-                    pos[u] = stb[r] + q;
+                    pos[u] = fb[r] + q;
                 else
-                    pos[u] = act[u] ? stb[r] + picks[((size_t)b * k + q) * R + r] : 0u;
+                    pos[u] = act[u] ? fb[r] + picks[((size_t)b * k + q) * 32 + r] : 0u;
             }
             int32_t nb[kCopyUnroll], ed[kCopyUnroll];
             float tv[kCopyUnroll];
@@ -334,33 +403,28 @@ __global__ void __launch_bounds__(kSampleThreads) sample_kernel(const __grid_con
 #pragma unroll
             for (int u = 0; u < kCopyUnroll; ++u) {
                 if (!act[u]) continue;
-                const uint64_t oi = B + o0 + (uint32_t)(u * R + tid);
+                const uint64_t oi = B + o0 + (uint32_t)(u * 32 + lane);
+                const float tr = troot[rr[u]];
                 o.nbr[oi] = nb[u];
                 o.eid[oi] = ed[u];
-                o.dt[oi] = __fsub_rn(troot[rr[u]], tv[u]);
+                o.dt[oi] = __fsub_rn(tr, tv[u]);
                 if (o.ts_edge) o.ts_edge[oi] = tv[u];
                 if (o.child_key) o.child_key[oi] = rkey[rr[u]] * (uint64_t)k + qq[u];
-                if (o.child_lo) o.child_lo[oi] = lo_r[b * R + rr[u]];
+                if (o.child_lo)  // children inherit the window's lower bound (R#3)
+                    o.child_lo[oi] = p.layer == 0 ? __fsub_rn(tr, __fmul_rn((float)(b + 1), p.snapshot_len))
+                                                  : p.root_lo[base_i + warp * 32 + rr[u]];
             }
         }
     }
 }
 
-static size_t sample_smem_bytes(int nsb, int k, int strategy, bool picks_in_smem) {
-    const size_t R = kSampleThreads;
-    size_t b = (size_t)nsb * R * 4 * 3 + R * 4;  // incl, start, lo_r, troot
-    b += R * 8;                                  // rkey
-    if (strategy == TGL_UNIFORM && picks_in_smem) b += (size_t)nsb * k * R * 4;
-    return b;
-}
-
-static bool picks_fit_smem(int nsb, int k) { return (size_t)nsb * k * kSampleThreads * 4 <= kPicksSmemLimit; }
+static bool picks_fit_smem(int nsb, int k) { return (size_t)nsb * k * 32 * 4 <= kPicksSmemPerWarp; }
 
 struct Launch {
     int layer, chain, nsb;
     int64_t roots_cap, tiles_cap;
-    uint32_t* counter;
-    uint64_t* state;
+    uint32_t *win_first, *win_len, *tile_tot;
+    uint64_t* tile_base;
     uint32_t* picks;  // global picks or null
 };
 
@@ -369,7 +433,6 @@ struct SamplePlan {
     int64_t roots_cap[64], edges_cap[64];
     Launch launches[1 + 63 * TGL_MAX_SNAPSHOTS];
     int n_launch = 0;
-    size_t memset_bytes = 0;
     uint64_t* child_key[64][TGL_MAX_SNAPSHOTS];
     float* child_lo[64][TGL_MAX_SNAPSHOTS];
     size_t bytes = 0;
@@ -393,38 +456,31 @@ static int plan_sample(int64_t n_roots, int L, const int32_t* fanouts, int S, in
         r = r * k;
     }
     Carve c(ws);
-    // tile counters + look-back state first: one contiguous region, one memset per call
     P.n_launch = 0;
     auto add = [&](int layer, int chain, int nsb) {
         Launch& la = P.launches[P.n_launch++];
         la.layer = layer;
         la.chain = chain;
         la.nsb = nsb;
-        la.roots_cap = P.roots_cap[layer];
-        la.tiles_cap = std::max<int64_t>(1, (la.roots_cap + kSampleThreads - 1) / kSampleThreads);
+        la.roots_cap = std::max<int64_t>(1, P.roots_cap[layer]);
+        la.tiles_cap = (la.roots_cap + kSampleThreads - 1) / kSampleThreads;
+        la.win_first = c.take<uint32_t>((size_t)nsb * la.roots_cap);
+        la.win_len = c.take<uint32_t>((size_t)nsb * la.roots_cap);
+        la.tile_tot = c.take<uint32_t>((size_t)nsb * la.tiles_cap);
+        la.tile_base = c.take<uint64_t>((size_t)nsb * la.tiles_cap);
+        la.picks = nullptr;
+        if (strategy == TGL_UNIFORM && !picks_fit_smem(nsb, fanouts[layer]))
+            la.picks = c.take<uint32_t>((size_t)la.tiles_cap * kSampleThreads * nsb * fanouts[layer]);
     };
     add(0, 0, S);
     for (int l = 1; l < L; ++l)
         for (int s = 0; s < S; ++s) add(l, s, 1);
-    for (int j = 0; j < P.n_launch; ++j) {
-        Launch& la = P.launches[j];
-        la.counter = c.take<uint32_t>(64);
-        la.state = c.take<uint64_t>((size_t)la.nsb * la.tiles_cap);
-    }
-    P.memset_bytes = c.bytes();
     const bool need_lo = L > 1 && std::isfinite(snapshot_len);
     for (int l = 0; l < L - 1; ++l)
         for (int s = 0; s < S; ++s) {
             P.child_key[l][s] = strategy == TGL_UNIFORM ? c.take<uint64_t>((size_t)P.edges_cap[l]) : nullptr;
             P.child_lo[l][s] = need_lo ? c.take<float>((size_t)P.edges_cap[l]) : nullptr;
         }
-    for (int j = 0; j < P.n_launch; ++j) {
-        Launch& la = P.launches[j];
-        const int k = fanouts[la.layer];
-        la.picks = nullptr;
-        if (strategy == TGL_UNIFORM && !picks_fit_smem(la.nsb, k))
-            la.picks = c.take<uint32_t>((size_t)la.tiles_cap * la.nsb * k * kSampleThreads);
-    }
     P.bytes = c.bytes();
     return TGL_OK;
 }
@@ -468,8 +524,7 @@ extern "C" int tgl_sample(const tgl_tcsr* g, const int32_t* roots, const float* 
             if (b.cap_roots < P.roots_cap[l] || b.cap_edges < P.edges_cap[l]) return TGL_ECAPACITY;
         }
     cudaStream_t st = (cudaStream_t)stream;
-    if (cudaMemsetAsync(workspace, 0, P.memset_bytes, st) != cudaSuccess) return TGL_ECUDA;
-
+    const bool indexed = g->index && g->n_levels > 0 && ((uintptr_t)g->ts & 31) == 0;
     for (int j = 0; j < P.n_launch; ++j) {
         const Launch& la = P.launches[j];
         const int l = la.layer, s = la.chain;
@@ -479,14 +534,15 @@ extern "C" int tgl_sample(const tgl_tcsr* g, const int32_t* roots, const float* 
         sp.nbr = g->nbr;
         sp.ts = g->ts;
         sp.eid = g->eid;
+        sp.lvl[0] = g->ts;
+        sp.n_levels = indexed ? g->n_levels : -1;
+        if (indexed)
+            for (int q = 1; q <= g->n_levels; ++q) sp.lvl[q] = g->index + g->level_off[q];
         sp.n_nodes = g->n_nodes;
         if (l == 0) {
             sp.root_node = roots;
             sp.root_ts = root_ts;
-            sp.root_key = nullptr;
-            sp.root_lo = nullptr;
             sp.n_roots = n_roots;
-            sp.n_roots_dev_in = nullptr;
         } else {
             const tgl_block& par = out[(l - 1) * S + s];
             sp.root_node = par.nbr;
@@ -504,8 +560,11 @@ extern "C" int tgl_sample(const tgl_tcsr* g, const int32_t* roots, const float* 
         sp.snapshot_len = snapshot_len;
         sp.seed_lo = (uint32_t)seed;
         sp.seed_hi = (uint32_t)(seed >> 32);
-        sp.tile_state = la.state;
-        sp.tile_counter = la.counter;
+        sp.win_first = la.win_first;
+        sp.win_len = la.win_len;
+        sp.tile_tot = la.tile_tot;
+        sp.tile_base = la.tile_base;
+        sp.roots_cap = la.roots_cap;
         sp.tiles_cap = la.tiles_cap;
         sp.picks_global = la.picks;
         sp.err = g->err_dev;
@@ -526,17 +585,21 @@ extern "C" int tgl_sample(const tgl_tcsr* g, const int32_t* roots, const float* 
         const int64_t grid = l == 0 ? std::max<int64_t>(1, (n_roots + kSampleThreads - 1) / kSampleThreads)
                                     : la.tiles_cap;
         const bool in_smem = la.picks == nullptr;
-        const size_t smem = sample_smem_bytes(la.nsb, sp.k, (int)strategy, in_smem);
+        const size_t smem =
+            (size_t)kSampleWarps * copy_warp_words(la.nsb, sp.k, strategy == TGL_UNIFORM && in_smem) * 4;
         if (strategy == TGL_UNIFORM) {
+            window_kernel<TGL_UNIFORM><<<(unsigned)grid, kSampleThreads, 0, st>>>(sp);
+            tile_scan_kernel<<<1, 1024, 0, st>>>(sp);
             if (smem > 48 * 1024)
-                cudaFuncSetAttribute(sample_kernel<TGL_UNIFORM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)smem);
-            sample_kernel<TGL_UNIFORM><<<(unsigned)grid, kSampleThreads, smem, st>>>(sp);
+                cudaFuncSetAttribute(copy_kernel<TGL_UNIFORM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            copy_kernel<TGL_UNIFORM><<<(unsigned)grid, kSampleThreads, smem, st>>>(sp);
         } else {
+            window_kernel<TGL_MOST_RECENT><<<(unsigned)grid, kSampleThreads, 0, st>>>(sp);
+            tile_scan_kernel<<<1, 1024, 0, st>>>(sp);
             if (smem > 48 * 1024)
-                cudaFuncSetAttribute(sample_kernel<TGL_MOST_RECENT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                cudaFuncSetAttribute(copy_kernel<TGL_MOST_RECENT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)smem);
-            sample_kernel<TGL_MOST_RECENT><<<(unsigned)grid, kSampleThreads, smem, st>>>(sp);
+            copy_kernel<TGL_MOST_RECENT><<<(unsigned)grid, kSampleThreads, smem, st>>>(sp);
         }
         if (cudaGetLastError() != cudaSuccess) return TGL_ECUDA;
     }

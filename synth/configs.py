@@ -278,3 +278,21 @@ def tables(cfg: Workload, device="cpu") -> Dict[str, torch.Tensor]:
         out[name] = hash_f32(idx, cfg.seed, 100 + j).reshape(rows, cols) if cols > 1 else \
             hash_f32(idx, cfg.seed, 100 + j).abs().mul_(float(cfg.t_max)).reshape(rows)
     return out
+
+
+def relevant_substream(src: torch.Tensor, dst: torch.Tensor, ts: torch.Tensor, nodes: torch.Tensor,
+                       n_nodes: int, add_reverse: bool, chunk: int = 1 << 27):
+    """Edges of the stream that can own a logical edge of one of `nodes`, in stream order, with
+    their original indices as eids: (src, dst, ts, eid) numpy arrays.  Input selection for the
+    restricted oracle on billion-edge configs (the oracle then applies its own owner filter)."""
+    keep = torch.zeros(n_nodes, dtype=torch.bool, device=src.device)
+    keep[nodes.long()] = True
+    parts = []
+    for lo in range(0, src.numel(), chunk):
+        hi = min(src.numel(), lo + chunk)
+        s, d = src[lo:hi].long(), dst[lo:hi].long()
+        m = keep[s] | keep[d] if add_reverse else keep[s]
+        idx = torch.nonzero(m).flatten()
+        parts.append((s[idx].int().cpu(), d[idx].int().cpu(), ts[lo:hi][idx].cpu(), (idx + lo).int().cpu()))
+    cat = [torch.cat([p[j] for p in parts]).numpy() if parts else np.zeros(0) for j in range(4)]
+    return cat[0], cat[1], cat[2], cat[3], keep.cpu().numpy().astype(np.uint8)

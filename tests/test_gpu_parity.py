@@ -28,9 +28,10 @@ def cu(a, dtype):
     return torch.as_tensor(np.asarray(a), dtype=dtype).cuda()
 
 
-def gpu_build(tgl, src, dst, ts, eid, n_nodes, add_rev):
+def gpu_build(tgl, src, dst, ts, eid, n_nodes, add_rev, with_index=True):
     return tgl.build(cu(src, torch.int32), cu(dst, torch.int32), cu(ts, torch.float32),
-                     None if eid is None else cu(eid, torch.int32), n_nodes=n_nodes, add_reverse=add_rev)
+                     None if eid is None else cu(eid, torch.int32), n_nodes=n_nodes, add_reverse=add_rev,
+                     with_index=with_index)
 
 
 def assert_tcsr_equal(g, go):
@@ -53,9 +54,10 @@ def assert_blocks_equal(blocks, blocks_o, L, what=""):
             np.testing.assert_array_equal(te.cpu().numpy().view(np.uint32), bo["ts_edge"].view(np.uint32))
 
 
-def both(tgl, src, dst, ts, eid, n_nodes, add_rev, roots, rts, fanouts, strategy, S, t_s, seed, base):
+def both(tgl, src, dst, ts, eid, n_nodes, add_rev, roots, rts, fanouts, strategy, S, t_s, seed, base,
+         with_index=True):
     go = oracle.build(src, dst, ts, eid, n_nodes=n_nodes, add_reverse=add_rev)
-    g = gpu_build(tgl, src, dst, ts, eid, n_nodes, add_rev)
+    g = gpu_build(tgl, src, dst, ts, eid, n_nodes, add_rev, with_index)
     assert_tcsr_equal(g, go)
     bo = oracle.sample(go, roots, rts, fanouts=fanouts, strategy=strategy, n_snapshots=S, snapshot_len=t_s,
                        seed=seed, root_key_base=base)
@@ -83,7 +85,8 @@ def test_random_graphs_bit_exact(tgl):
         t_s = math.inf if S == 1 and case % 4 else float(rng.choice([1.0, 2.5, 7.0]))
         seed = int(rng.integers(0, 2**63))
         base = int(rng.integers(0, 2**40))
-        both(tgl, src, dst, ts, eid, n_nodes, add_rev, roots, rts, fanouts, strategy, S, t_s, seed, base)
+        both(tgl, src, dst, ts, eid, n_nodes, add_rev, roots, rts, fanouts, strategy, S, t_s, seed, base,
+             with_index=case % 7 != 3)
 
 
 @pytest.mark.parametrize("n_nodes", [1, 2, 255, 256, 257, 65536, 65537, 20_000_000])
@@ -114,7 +117,23 @@ def test_multi_tile_ragged_and_hub(tgl):
     rts = (rng.random(len(roots)) * 1.1e5).astype(np.float32)
     for strategy in (0, 1):
         for S, t_s in ((1, math.inf), (3, 5000.0)):
-            both(tgl, src, dst, ts, None, n_nodes, True, roots, rts, [10, 4], strategy, S, t_s, 3, 1000)
+            for with_index in (True, False):
+                both(tgl, src, dst, ts, None, n_nodes, True, roots, rts, [10, 4], strategy, S, t_s, 3, 1000,
+                     with_index=with_index)
+
+
+def test_wrap_rebuilds_index(tgl):
+    """tgl_tcsr_wrap + tgl_tcsr_index_build over arrays of a built T-CSR give identical samples."""
+    src, dst, ts, _ = random_graph(12, 200, 30_000, integer_times=False, t_max=1e4)
+    roots, rts = random_roots(12, 200, 3000, integer_times=False, t_max=1e4)
+    g = gpu_build(tgl, src, dst, ts, None, 200, True)
+    g2 = tgl.wrap(g.indptr.clone(), g.nbr.clone(), g.ts.clone(), g.eid.clone())
+    R, T = cu(roots, torch.int32), cu(rts, torch.float32)
+    a = tgl.sample(g, R, T, fanouts=[10], n_snapshots=3, snapshot_len=500.0)
+    b = tgl.sample(g2, R, T, fanouts=[10], n_snapshots=3, snapshot_len=500.0)
+    for x, y in zip(a, b):
+        for u, w in zip(x.trimmed()[:4], y.trimmed()[:4]):
+            assert torch.equal(u, w)
 
 
 @pytest.mark.parametrize("k,S,strategy", [(64, 1, 1), (65, 1, 1), (1024, 1, 1), (300, 4, 1), (1, 16, 0),
