@@ -90,34 +90,35 @@ TGL_API int tgl_tcsr_build_workspace(int64_t n_edges, int32_t n_nodes, int add_r
  *   nbr[E_s] int32, ts_out[E_s] float32, eid_out[E_s] int32: the logical edges grouped by owner,
  *   each node's list in stream order -- hence time-sorted without a sort -- with ties
  *   broken by stream order (R#8).  Bit-identical to the oracle's counting sort.
- *   ts_out must be 32-byte aligned and its allocation must extend to round_up(E_s, 8) floats: the
- *   sampler reads timestamps in aligned 8-float (one-sector) groups.
- * ts_index (optional, may be NULL): >= tgl_tcsr_index_bytes(E_s) bytes, 256-byte aligned; filled
- *   with the 8-ary sector index over ts_out that the sampler's cut search uses (DESIGN.md
- *   "Cut search").  Without it the sampler falls back to a plain binary search.
+ *   ts_out must be 64-byte aligned and its allocation must extend to round_up(E_s, 16) floats: the
+ *   sampler reads timestamps in aligned 16-float (64-byte, one HBM atom) groups.
+ * aux (optional, may be NULL): >= tgl_tcsr_aux_bytes(E_s) bytes, 256-byte aligned; filled with the
+ *   sampler's acceleration structures over the T-CSR: the 16-ary atom index over ts_out (cut
+ *   search) and an interleaved copy of (nbr, eid) per slot (payload copy) -- DESIGN.md "Data
+ *   layout".  Without it the sampler falls back to binary search and separate nbr / eid reads.
  * workspace: >= tgl_tcsr_build_workspace() bytes of device memory, 256-byte aligned.
  * Synchronous validation: the call blocks on `stream` once to read the device validation word;
  *   on ERANGE / EINVAL / EUNSORTED no handle is returned and outputs are unspecified.
- * On success *out (host) receives a handle that borrows indptr/nbr/ts_out/eid_out/ts_index.
+ * On success *out (host) receives a handle that borrows indptr/nbr/ts_out/eid_out/aux.
  */
 TGL_API int tgl_tcsr_build(const int32_t *src, const int32_t *dst, const float *ts, const int32_t *eid,
                    int64_t n_edges, int32_t n_nodes, int add_reverse,
                    int64_t *indptr, int32_t *nbr, float *ts_out, int32_t *eid_out,
-                   void *ts_index, size_t index_bytes,
+                   void *aux, size_t aux_bytes,
                    void *workspace, size_t ws_bytes, void *stream, tgl_tcsr **out /* host */);
 
-/* Bytes of the optional timestamp sector index for a T-CSR of n_stored edges (host query). */
-TGL_API int tgl_tcsr_index_bytes(int64_t n_stored, size_t *bytes /* host */);
+/* Bytes of the optional sampler aux buffer for a T-CSR of n_stored edges (host query). */
+TGL_API int tgl_tcsr_aux_bytes(int64_t n_stored, size_t *bytes /* host */);
 
-/* (Re)build the sector index over an existing ts array (e.g. one received from another rank). */
-TGL_API int tgl_tcsr_index_build(const float *ts, int64_t n_stored, void *ts_index, size_t index_bytes,
-                         void *stream);
+/* (Re)build the aux buffer over existing T-CSR arrays (e.g. ones received from another rank). */
+TGL_API int tgl_tcsr_aux_build(const float *ts, const int32_t *nbr, const int32_t *eid, int64_t n_stored,
+                       void *aux, size_t aux_bytes, void *stream);
 
 /* Wrap already-built T-CSR arrays (e.g. received from another rank) in a handle.  No
- * validation beyond NULL / size checks.  n_stored = E_s = indptr[n_nodes].  ts_index may be NULL
- * or an index built by tgl_tcsr_build / tgl_tcsr_index_build over the same ts. */
+ * validation beyond NULL / size checks.  n_stored = E_s = indptr[n_nodes].  aux may be NULL or a
+ * buffer filled by tgl_tcsr_build / tgl_tcsr_aux_build over the same arrays. */
 TGL_API int tgl_tcsr_wrap(const int64_t *indptr, const int32_t *nbr, const float *ts, const int32_t *eid,
-                  const void *ts_index, size_t index_bytes,
+                  const void *aux, size_t aux_bytes,
                   int32_t n_nodes, int64_t n_stored, tgl_tcsr **out /* host */);
 
 TGL_API int tgl_tcsr_destroy(tgl_tcsr *g);

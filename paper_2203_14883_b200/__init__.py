@@ -24,7 +24,7 @@ from ._lib import MOST_RECENT, UNIFORM, TGLError
 
 _L = _lib.load()
 
-__all__ = ["TCSR", "Block", "Sampler", "build", "wrap", "index_bytes", "sample", "gather", "check", "shard_bucket",
+__all__ = ["TCSR", "Block", "Sampler", "build", "wrap", "aux_bytes", "sample", "gather", "check", "shard_bucket",
            "MOST_RECENT", "UNIFORM", "TGLError", "lib_path"]
 
 lib_path = _lib.LIB_PATH
@@ -59,7 +59,7 @@ def _strategy(s) -> int:
 
 
 class TCSR:
-    """A built T-CSR: indptr int64 [V+1]; nbr int32, ts float32, eid int32 [E_s] (+ ts sector index)."""
+    """A built T-CSR: indptr int64 [V+1]; nbr int32, ts float32, eid int32 [E_s] (+ sampler aux buffer)."""
 
     def __init__(self, indptr, nbr, ts, eid, n_nodes, handle, index=None, ts_storage=None):
         self.indptr, self.nbr, self.ts, self.eid = indptr, nbr, ts, eid
@@ -75,7 +75,7 @@ class TCSR:
 
     def __del__(self):
         h, self._h = getattr(self, "_h", None), None
-        if h:
+        if h and _L is not None:
             _L.tgl_tcsr_destroy(h)
 
 
@@ -86,22 +86,24 @@ def build_workspace_bytes(n_edges: int, n_nodes: int, add_reverse: bool) -> int:
     return b.value
 
 
-def index_bytes(n_stored: int) -> int:
+def aux_bytes(n_stored: int) -> int:
     b = ctypes.c_size_t()
-    _rc(_L.tgl_tcsr_index_bytes(int(n_stored), ctypes.byref(b)), "tgl_tcsr_index_bytes")
+    _rc(_L.tgl_tcsr_aux_bytes(int(n_stored), ctypes.byref(b)), "tgl_tcsr_aux_bytes")
     return b.value
 
 
 def _ts_buffer(n: int, dev) -> (torch.Tensor, torch.Tensor):
-    """float32 [n] view of a buffer padded to a multiple of 8 floats (sector-group reads)."""
-    storage = torch.empty(max((n + 7) // 8 * 8, 8), dtype=torch.float32, device=dev)
+    """float32 [n] view of a 64-byte aligned buffer padded to a multiple of 16 floats (the sampler
+    reads timestamps in aligned 64-byte groups)."""
+    storage = torch.empty(max((n + 15) // 16 * 16, 16), dtype=torch.float32, device=dev)
+    assert storage.data_ptr() % 64 == 0
     return storage[:n], storage
 
 
 def build(src: torch.Tensor, dst: torch.Tensor, ts: torch.Tensor, eid: Optional[torch.Tensor] = None, *,
           n_nodes: int, add_reverse: bool, workspace: Optional[torch.Tensor] = None, with_index: bool = True,
           stream=None) -> TCSR:
-    """tgl_tcsr_build: T-CSR of a chronological stream + the ts sector index."""
+    """tgl_tcsr_build: T-CSR of a chronological stream + the sampler aux buffer."""
     src = _cuda(src, torch.int32, "src")
     dst = _cuda(dst, torch.int32, "dst")
     ts = _cuda(ts, torch.float32, "ts")
@@ -114,7 +116,7 @@ def build(src: torch.Tensor, dst: torch.Tensor, ts: torch.Tensor, eid: Optional[
     nbr = torch.empty(Es, dtype=torch.int32, device=dev)
     ts_out, ts_storage = _ts_buffer(Es, dev)
     eid_out = torch.empty(Es, dtype=torch.int32, device=dev)
-    ib = index_bytes(Es) if with_index else 0
+    ib = aux_bytes(Es) if with_index else 0
     index = torch.empty(ib, dtype=torch.uint8, device=dev) if with_index else None
     wsb = build_workspace_bytes(E, n_nodes, add_reverse)
     if workspace is None or workspace.numel() < wsb:
@@ -135,10 +137,11 @@ def wrap(indptr: torch.Tensor, nbr: torch.Tensor, ts: torch.Tensor, eid: torch.T
     n = nbr.numel()
     ts_view, ts_storage = _ts_buffer(n, nbr.device)
     ts_view.copy_(_cuda(ts, torch.float32, "ts"))
-    ib = index_bytes(n) if with_index else 0
+    ib = aux_bytes(n) if with_index else 0
     index = torch.empty(ib, dtype=torch.uint8, device=nbr.device) if with_index else None
     if with_index:
-        _rc(_L.tgl_tcsr_index_build(_ptr(ts_storage), n, _ptr(index), ib, _stream(stream)), "tgl_tcsr_index_build")
+        _rc(_L.tgl_tcsr_aux_build(_ptr(ts_storage), _ptr(nbr), _ptr(eid), n, _ptr(index), ib, _stream(stream)),
+            "tgl_tcsr_aux_build")
     h = ctypes.c_void_p()
     _rc(_L.tgl_tcsr_wrap(_ptr(indptr), _ptr(nbr), _ptr(ts_storage), _ptr(eid), _ptr(index), ib,
                          indptr.numel() - 1, n, ctypes.byref(h)), "tgl_tcsr_wrap")

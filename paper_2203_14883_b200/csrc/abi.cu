@@ -43,14 +43,14 @@ extern "C" const char* tgl_strerror(int code) {
 }
 
 extern "C" int tgl_tcsr_wrap(const int64_t* indptr, const int32_t* nbr, const float* ts, const int32_t* eid,
-                             const void* ts_index, size_t index_bytes, int32_t n_nodes, int64_t n_stored,
+                             const void* aux, size_t aux_bytes, int32_t n_nodes, int64_t n_stored,
                              tgl_tcsr** out) {
     if (!out || !indptr || n_nodes < 0 || n_stored < 0) return TGL_EINVAL;
     *out = nullptr;
     if (n_stored > 0 && (!nbr || !ts || !eid)) return TGL_EINVAL;
     if ((uint64_t)n_stored >= (1ull << 32)) return TGL_EINVAL;
-    const IndexLayout lay = index_layout((uint64_t)n_stored);
-    if (ts_index && index_bytes < lay.floats * sizeof(float)) return TGL_EWORKSPACE;
+    const AuxLayout lay = aux_layout((uint64_t)n_stored);
+    if (aux && aux_bytes < lay.bytes) return TGL_EWORKSPACE;
     int rc = check_device();
     if (rc) return rc;
     tgl_tcsr* g = static_cast<tgl_tcsr*>(calloc(1, sizeof(tgl_tcsr)));
@@ -65,9 +65,10 @@ extern "C" int tgl_tcsr_wrap(const int64_t* indptr, const int32_t* nbr, const fl
     g->eid = eid;
     g->n_nodes = n_nodes;
     g->n_stored = n_stored;
-    g->index = static_cast<const float*>(ts_index);
-    g->n_levels = ts_index ? lay.n_levels : 0;
-    for (int l = 0; l <= kMaxIndexLevels && l < 12; ++l) g->level_off[l] = lay.off[l];
+    g->index = static_cast<const float*>(aux);
+    g->n_levels = aux ? lay.index.n_levels : 0;
+    for (int l = 0; l <= kMaxIndexLevels && l < 12; ++l) g->level_off[l] = lay.index.off[l];
+    g->payload = aux ? reinterpret_cast<const int2*>(static_cast<const char*>(aux) + lay.payload_off) : nullptr;
     cudaGetDevice(&g->device);
     *out = g;
     return TGL_OK;

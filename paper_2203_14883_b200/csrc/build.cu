@@ -234,42 +234,47 @@ extern "C" int tgl_tcsr_build_workspace(int64_t n_edges, int32_t n_nodes, int ad
 }
 
 namespace tgl {
-// L_l[j] = ts[j * 8^l] for every level (tsindex.cuh)
-__global__ void index_build_kernel(const float* __restrict__ ts, float* __restrict__ index, IndexLayout lay) {
+// aux buffer (tsindex.cuh): index levels L_l[j] = ts[j * 16^l] and the interleaved payload
+__global__ void aux_build_kernel(const float* __restrict__ ts, const int32_t* __restrict__ nbr,
+                                 const int32_t* __restrict__ eid, uint64_t n, char* __restrict__ aux, AuxLayout lay) {
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-    for (int l = 1; l <= lay.n_levels; ++l) {
-        float* out = index + lay.off[l];
-        const int sh = 3 * l;
-        for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < lay.len[l]; j += stride)
+    float* index = reinterpret_cast<float*>(aux);
+    for (int l = 1; l <= lay.index.n_levels; ++l) {
+        float* out = index + lay.index.off[l];
+        const int sh = kIndexShift * l;
+        for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < lay.index.len[l]; j += stride)
             out[j] = ts[j << sh];
     }
+    int2* pay = reinterpret_cast<int2*>(aux + lay.payload_off);
+    for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += stride)
+        pay[j] = make_int2(nbr[j], eid[j]);
 }
 }  // namespace tgl
 
-extern "C" int tgl_tcsr_index_bytes(int64_t n_stored, size_t* bytes) {
+extern "C" int tgl_tcsr_aux_bytes(int64_t n_stored, size_t* bytes) {
     if (!bytes || n_stored < 0 || (uint64_t)n_stored >= (1ull << 32)) return TGL_EINVAL;
-    *bytes = std::max<size_t>(256, index_layout((uint64_t)n_stored).floats * sizeof(float));
+    *bytes = aux_layout((uint64_t)n_stored).bytes;
     return TGL_OK;
 }
 
-extern "C" int tgl_tcsr_index_build(const float* ts, int64_t n_stored, void* ts_index, size_t index_bytes,
-                                    void* stream) {
-    if (n_stored < 0 || (uint64_t)n_stored >= (1ull << 32) || !ts_index) return TGL_EINVAL;
-    if (n_stored > 0 && !ts) return TGL_EINVAL;
-    IndexLayout lay = index_layout((uint64_t)n_stored);
-    if (index_bytes < lay.floats * sizeof(float)) return TGL_EWORKSPACE;
+extern "C" int tgl_tcsr_aux_build(const float* ts, const int32_t* nbr, const int32_t* eid, int64_t n_stored,
+                                  void* aux, size_t aux_bytes, void* stream) {
+    if (n_stored < 0 || (uint64_t)n_stored >= (1ull << 32) || !aux) return TGL_EINVAL;
+    if (n_stored > 0 && (!ts || !nbr || !eid)) return TGL_EINVAL;
+    const AuxLayout lay = aux_layout((uint64_t)n_stored);
+    if (aux_bytes < lay.bytes) return TGL_EWORKSPACE;
     int rc = check_device();
     if (rc) return rc;
-    if (lay.n_levels == 0) return TGL_OK;
-    const int64_t blocks = std::min<int64_t>((int64_t)((lay.len[1] + 255) / 256), 148 * 8);
-    index_build_kernel<<<(unsigned)std::max<int64_t>(blocks, 1), 256, 0, (cudaStream_t)stream>>>(
-        ts, static_cast<float*>(ts_index), lay);
+    if (n_stored == 0) return TGL_OK;
+    const int64_t blocks = std::min<int64_t>((int64_t)((n_stored + 255) / 256), 148 * 16);
+    aux_build_kernel<<<(unsigned)std::max<int64_t>(blocks, 1), 256, 0, (cudaStream_t)stream>>>(
+        ts, nbr, eid, (uint64_t)n_stored, static_cast<char*>(aux), lay);
     return cudaGetLastError() == cudaSuccess ? TGL_OK : TGL_ECUDA;
 }
 
 extern "C" int tgl_tcsr_build(const int32_t* src, const int32_t* dst, const float* ts, const int32_t* eid,
                               int64_t n_edges, int32_t n_nodes, int add_reverse, int64_t* indptr, int32_t* nbr,
-                              float* ts_out, int32_t* eid_out, void* ts_index, size_t index_bytes, void* workspace,
+                              float* ts_out, int32_t* eid_out, void* aux, size_t aux_bytes, void* workspace,
                               size_t ws_bytes, void* stream, tgl_tcsr** out) {
     if (!out || !indptr || n_edges < 0 || n_nodes < 0) return TGL_EINVAL;
     *out = nullptr;
@@ -341,11 +346,11 @@ extern "C" int tgl_tcsr_build(const int32_t* src, const int32_t* dst, const floa
             if (cudaGetLastError() != cudaSuccess) return TGL_ECUDA;
         }
     }
-    if (ts_index) {
-        rc = tgl_tcsr_index_build(ts_out, (int64_t)es, ts_index, index_bytes, stream);
+    if (aux) {
+        rc = tgl_tcsr_aux_build(ts_out, nbr, eid_out, (int64_t)es, aux, aux_bytes, stream);
         if (rc) return rc;
     }
-    return tgl_tcsr_wrap(indptr, nbr, ts_out, eid_out, ts_index, index_bytes, n_nodes, (int64_t)es, out);
+    return tgl_tcsr_wrap(indptr, nbr, ts_out, eid_out, aux, aux_bytes, n_nodes, (int64_t)es, out);
 }
 
 // ---------------------------------------------------------------------------- K8 shard bucketing

@@ -88,7 +88,8 @@ struct tgl_tcsr {
     int64_t n_stored;
     int* err_dev;  // sticky device error word of this handle (cudaMalloc at creation)
     int device;
-    const float* index;      // 8-ary sector index over ts (tsindex.cuh), or null
+    const float* index;      // 16-ary atom index over ts (tsindex.cuh), or null
     int n_levels;
-    uint64_t level_off[12];  // float offset of level l in index
+    uint64_t level_off[12];  // float offset of level l in index (levels <= 8)
+    const int2* payload;     // interleaved (nbr, eid) per slot, or null
 };

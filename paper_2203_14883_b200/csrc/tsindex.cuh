@@ -1,24 +1,27 @@
-// tsindex.cuh -- the sector index over T-CSR timestamps used by the cut search (internal).
+// tsindex.cuh -- the atom index over T-CSR timestamps used by the cut search (internal).
 //
 // The paper locates candidate windows with per-node pointer arrays pt_0..pt_S advanced once per
 // epoch (Sec. 3.1).  Pointers are mutable shared state that serialises batches
-// (per-node locks); the GPU path is stateless instead: a lower_bound per cut.  To make a
-// lower_bound cost ~one 32-byte sector per level instead of ~log2(deg) scattered probes, the
-// build adds an implicit 8-ary search tree over the global ts array:
+// (per-node locks); the GPU path is stateless instead: a lower_bound per cut.  HBM serves
+// scattered reads in 64-byte atoms (measured with ncu: DRAM bytes = 2 x the requested 32-byte
+// sectors for random sector reads), so the unit of cost is one 64-byte, 16-float group.  To make
+// a lower_bound cost ~one atom per level instead of ~log2(deg) scattered probes, the build adds
+// an implicit 16-ary search tree over the global ts array:
 //
-//     level l (l = 1..n_levels):  L_l[j] = ts[j * 8^l],   j < ceil(E_s / 8^l)
+//     level l (l = 1..n_levels):  L_l[j] = ts[j * 16^l],   j < ceil(E_s / 16^l)
 //
-// Sampling positions are GLOBAL multiples of 8^l, so no per-node offsets are stored; a node's
-// entries at level l are the multiples of 8^l inside [indptr[v], indptr[v+1]), contiguous in L_l.
-// Between two consecutive multiples of 8^l lie exactly 7 multiples of 8^(l-1): one aligned
-// 8-float group (one sector) of L_(l-1).  Size: sum_l E_s / 8^l ~ E_s / 7 floats.
+// Sampling positions are GLOBAL multiples of 16^l, so no per-node offsets are stored; a node's
+// entries at level l are the multiples of 16^l inside [indptr[v], indptr[v+1]), contiguous in
+// L_l.  Between two consecutive multiples of 16^l lie exactly 15 multiples of 16^(l-1): one
+// aligned 16-float group (one atom) of L_(l-1).  Size: sum_l E_s / 16^l ~ E_s / 15 floats.
 #pragma once
 
 #include "common.cuh"
 
 namespace tgl {
 
-constexpr int kMaxIndexLevels = 11;  // 8^11 > 2^32 > E_s
+constexpr int kIndexShift = 4;                     // fan-out 16 = one 64-byte group of floats
+constexpr int kMaxIndexLevels = 8;                 // 16^8 = 2^32 > E_s
 
 struct IndexLayout {
     int n_levels = 0;
@@ -31,7 +34,7 @@ inline IndexLayout index_layout(uint64_t n_stored) {
     IndexLayout L;
     uint64_t o = 0;
     for (int l = 1; l <= kMaxIndexLevels; ++l) {
-        const uint64_t stride = 1ull << (3 * l);
+        const uint64_t stride = 1ull << (kIndexShift * l);
         if (stride >= n_stored) break;  // a level needs >= 2 entries to discriminate
         const uint64_t n = (n_stored + stride - 1) / stride;
         L.off[l] = o;
@@ -41,6 +44,24 @@ inline IndexLayout index_layout(uint64_t n_stored) {
     }
     L.floats = o;
     return L;
+}
+
+// The sampler's auxiliary ("aux") buffer: [ts atom index | (nbr, eid) pairs].  The interleaved
+// payload puts both fields of a slot in one 8-byte word, so copying a run of c sampled slots is
+// one contiguous access (one DRAM row activation) instead of two.
+struct AuxLayout {
+    IndexLayout index;
+    uint64_t payload_off = 0;  // byte offset of the int2 payload array
+    uint64_t bytes = 0;
+};
+
+inline AuxLayout aux_layout(uint64_t n_stored) {
+    AuxLayout A;
+    A.index = index_layout(n_stored);
+    A.payload_off = align_up(A.index.floats * sizeof(float), 256);
+    A.bytes = align_up(A.payload_off + n_stored * 8, 256);
+    if (A.bytes < 256) A.bytes = 256;
+    return A;
 }
 
 }  // namespace tgl

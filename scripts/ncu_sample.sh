@@ -3,7 +3,7 @@
 # usage: bash scripts/ncu_sample.sh <tag> [extra bench args]
 tag=${1:-r1}; shift
 mkdir -p gpurun_out
-ncu --set full --clock-control none --import-source on -k regex:sample_kernel -s 3 -c 1 \
+ncu --set full --clock-control none --import-source on -k regex:"window_kernel|copy_kernel" -s 6 -c 2 \
     -o gpurun_out/prof_${tag} -f python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline "$@" > gpurun_out/ncu_${tag}.log 2>&1
 tail -2 gpurun_out/ncu_${tag}.log
 if [ -n "$LAUNCHES" ]; then

@@ -123,7 +123,7 @@ def test_multi_tile_ragged_and_hub(tgl):
 
 
 def test_wrap_rebuilds_index(tgl):
-    """tgl_tcsr_wrap + tgl_tcsr_index_build over arrays of a built T-CSR give identical samples."""
+    """tgl_tcsr_wrap + tgl_tcsr_aux_build over arrays of a built T-CSR give identical samples."""
     src, dst, ts, _ = random_graph(12, 200, 30_000, integer_times=False, t_max=1e4)
     roots, rts = random_roots(12, 200, 3000, integer_times=False, t_max=1e4)
     g = gpu_build(tgl, src, dst, ts, None, 200, True)
