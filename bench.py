@@ -197,7 +197,7 @@ def run_ours(args):
     chunks = [C.roots(cfg, src, dst, ts, s0, chunk) for s0 in mine]
     sampler = tgl.Sampler(g, chunk, cfg.fanouts, cfg.strategy, cfg.n_snapshots, cfg.snapshot_len)
     L, S = len(cfg.fanouts), cfg.n_snapshots
-    chunk_roots = int(os.environ.get("TGL_CHUNK_ROOTS", 131072))
+    chunk_roots = int(os.environ.get("TGL_CHUNK_ROOTS", 1 << 40))  # library default: one chunk per call
     n_chunks0 = max(1, -(-chunk // chunk_roots))
     launches_per_step = 3 * (n_chunks0 + (L - 1) * S)  # window + tile scan + copy per chunk / chain
     stream = torch.cuda.current_stream()
@@ -443,10 +443,10 @@ def run_reference(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="C5", choices=sorted(C.CONFIGS))
-    ap.add_argument("--batches", type=int, default=256, help="mini-batches per step (epoch mode)")
+    ap.add_argument("--batches", type=int, default=2048, help="mini-batches per step (epoch mode)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--ref-batches", type=int, default=16, help="reference arm: batches per step")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
