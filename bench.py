@@ -130,6 +130,25 @@ def chunk_starts(n_total_roots: int, chunk: int, n_chunks: int, batch: int):
     return out
 
 
+def rank_chunks(n_epoch_roots: int, chunk: int, steps_total: int, world: int, rank: int, batch: int):
+    """Root-sharded data parallelism: the steps_total * world chunks of `chunk` roots are spread
+    evenly over the epoch and chunk c*world + r goes to rank r (batch-aligned, disjoint)."""
+    starts = chunk_starts(n_epoch_roots, chunk, steps_total * world, batch)
+    return [starts[c * world + rank] for c in range(steps_total)]
+
+
+def reduce_report(edges: float, nbytes: float, ms: float, world: int, dev):
+    """Reporting only (outside the timed region): sum of work over ranks, max of device time."""
+    if world == 1:
+        return float(edges), float(nbytes), float(ms)
+    import torch.distributed as dist
+    tot = torch.tensor([edges, nbytes], dtype=torch.float64, device=dev)
+    mx = torch.tensor([ms], dtype=torch.float64, device=dev)
+    dist.all_reduce(tot)
+    dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+    return float(tot[0]), float(tot[1]), float(mx[0])
+
+
 def setup_graph(key: str, cfg: C.Workload, dev):
     t0 = time.time()
     src, dst, ts = C.edges(key, cfg, device=dev)
@@ -191,9 +210,7 @@ def run_ours(args):
     torch.cuda.empty_cache()
 
     # root chunks of this rank: chunk index c*world + rank, spread over the epoch
-    n_chunks = (args.warmup + args.steps) * world
-    starts = chunk_starts(cfg.n_roots_epoch, chunk, n_chunks, B)
-    mine = [starts[c * world + rank] for c in range(args.warmup + args.steps)]
+    mine = rank_chunks(cfg.n_roots_epoch, chunk, args.warmup + args.steps, world, rank, B)
     chunks = [C.roots(cfg, src, dst, ts, s0, chunk) for s0 in mine]
     sampler = tgl.Sampler(g, chunk, cfg.fanouts, cfg.strategy, cfg.n_snapshots, cfg.snapshot_len)
     L, S = len(cfg.fanouts), cfg.n_snapshots
@@ -240,15 +257,7 @@ def run_ours(args):
         bytes_total += algorithmic_bytes(cfg, nr, nz)
     err = tgl.check(g)
 
-    if world > 1:
-        import torch.distributed as dist
-        tot = torch.tensor([edges_total, bytes_total], dtype=torch.float64, device=dev)
-        mx = torch.tensor([total_ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(tot)
-        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
-        edges_all, bytes_all, total_ms_max = float(tot[0]), float(tot[1]), float(mx[0])
-    else:
-        edges_all, bytes_all, total_ms_max = float(edges_total), float(bytes_total), total_ms
+    edges_all, bytes_all, total_ms_max = reduce_report(edges_total, bytes_total, total_ms, world, dev)
 
     value = edges_all / (total_ms_max / 1e3)
     peak, peak_src = measured_peak_hbm()

@@ -123,6 +123,11 @@ TGL_API int tgl_tcsr_wrap(const int64_t *indptr, const int32_t *nbr, const float
 
 TGL_API int tgl_tcsr_destroy(tgl_tcsr *g);
 
+/* Node-sharded handles: the handle's T-CSR holds the lists of global nodes
+ * [node_lo, node_lo + n_nodes); roots passed to tgl_sample are GLOBAL ids, translated in-kernel
+ * (roots outside the range: count 0 + sticky ERANGE).  Neighbour ids stored in the lists stay global. */
+TGL_API int tgl_tcsr_set_node_base(tgl_tcsr *g, int64_t node_lo);
+
 /* Host query of a handle's sizes. */
 TGL_API int tgl_tcsr_info(const tgl_tcsr *g, int32_t *n_nodes /* host */, int64_t *n_stored /* host */);
 
@@ -183,6 +188,17 @@ TGL_API int tgl_sample(const tgl_tcsr *g, const int32_t *roots, const float *roo
                int32_t n_snapshots, float snapshot_len, uint64_t seed, uint64_t root_key_base,
                tgl_block *out /* host [L*S] */, void *workspace, size_t ws_bytes, void *stream);
 
+/*
+ * tgl_sample with EXPLICIT layer-0 root keys (device uint64 [n_roots]) instead of root_key_base + i:
+ * used by the node-sharded mode, where an owner samples roots gathered from many ranks and must
+ * reproduce exactly the keys the replicated mode would have used (R#7).  Same semantics otherwise.
+ */
+TGL_API int tgl_sample_keyed(const tgl_tcsr *g, const int32_t *roots, const float *root_ts,
+                     const uint64_t *root_keys, int64_t n_roots, int32_t n_layers,
+                     const int32_t *fanouts /* host [L] */, tgl_strategy strategy, int32_t n_snapshots,
+                     float snapshot_len, uint64_t seed, tgl_block *out /* host [L*S] */,
+                     void *workspace, size_t ws_bytes, void *stream);
+
 /* ------------------------------------------------------------------ gather (Fig. 2 step 2) */
 
 /* One gather target: out row i = table row ids[i]; row_bytes bytes per row. */
@@ -215,14 +231,29 @@ TGL_API int tgl_check(tgl_tcsr *g, void *stream);
 /*
  * Owner bucketing for the node-sharded T-CSR: node v is owned by shard r with
  * splits[r] <= v < splits[r+1] (splits: device int64 [world+1], splits[0] = 0, splits[world] = V).
- * Stable counting sort of the n roots by owner: perm[j] = index of the j-th root in
- * (owner, original index) order; counts[r] = roots owned by r (device int64 [world]).
+ * Stable counting sort of the n roots by owner: perm[j] = index (int32) of the j-th root in
+ * (owner, original index) order; counts[r] = roots owned by r (device int64 [world]).  n < 2^31.
  * The exchange itself (all-to-all-v of requests and replies) is NCCL, issued by the caller.
  * workspace >= tgl_shard_bucket_workspace() bytes.
  */
 TGL_API int tgl_shard_bucket_workspace(int64_t n_roots, int32_t world, size_t *bytes /* host */);
 TGL_API int tgl_shard_bucket(const int32_t *roots, int64_t n_roots, const int64_t *splits, int32_t world,
-                     int64_t *perm, int64_t *counts, void *workspace, size_t ws_bytes, void *stream);
+                     int32_t *perm, int64_t *counts, void *workspace, size_t ws_bytes, void *stream);
+
+/* counts[i] = offsets[i+1] - offsets[i] (device, int32), e.g. to send a block's per-root counts back. */
+TGL_API int tgl_offsets_to_counts(const int64_t *offsets, int64_t n_roots, int32_t *counts, void *stream);
+
+/*
+ * Un-permute one reply block: counts_in (int32 per root) / nbr_in / eid_in / dt_in are a CSR block
+ * over the roots in BUCKET order (as returned by the owners); the output is the same block in
+ * ORIGINAL root order (root perm[j] gets the edges of bucket position j), i.e. exactly what the
+ * replicated mode writes.  offsets_out [n+1] int64, edge arrays sized like the inputs.
+ */
+TGL_API int tgl_shard_unpermute_workspace(int64_t n_roots, size_t *bytes /* host */);
+TGL_API int tgl_shard_unpermute(const int32_t *perm, int64_t n_roots, const int32_t *counts_in,
+                        const int32_t *nbr_in, const int32_t *eid_in, const float *dt_in,
+                        int64_t *offsets_out, int32_t *nbr_out, int32_t *eid_out, float *dt_out,
+                        void *workspace, size_t ws_bytes, void *stream);
 
 #ifdef __cplusplus
 }

@@ -25,6 +25,7 @@ from ._lib import MOST_RECENT, UNIFORM, TGLError
 _L = _lib.load()
 
 __all__ = ["TCSR", "Block", "Sampler", "build", "wrap", "aux_bytes", "sample", "gather", "check", "shard_bucket",
+           "set_node_base", "shard_unpermute", "offsets_to_counts",
            "MOST_RECENT", "UNIFORM", "TGLError", "lib_path"]
 
 lib_path = _lib.LIB_PATH
@@ -67,6 +68,7 @@ class TCSR:
         self._ts_storage = ts_storage
         self.n_nodes = int(n_nodes)
         self.n_stored = int(nbr.numel())
+        self.node_lo = 0
         self._h = handle
 
     @property
@@ -213,13 +215,22 @@ class Sampler:
         return list(rc_), list(ec_), wsb.value
 
     def run(self, roots: torch.Tensor, root_ts: torch.Tensor, *, seed: int = 0, root_key_base: int = 0,
-            n_roots: Optional[int] = None, stream=None) -> List[Block]:
-        """tgl_sample on the current (or given) stream; no host synchronisation."""
+            root_keys: Optional[torch.Tensor] = None, n_roots: Optional[int] = None, stream=None) -> List[Block]:
+        """tgl_sample (or tgl_sample_keyed when root_keys, int64 bit patterns of uint64 keys, is given)
+        on the current (or given) stream; no host synchronisation."""
         n = roots.numel() if n_roots is None else int(n_roots)
         if n > self.max_roots:
             raise ValueError(f"{n} roots > max_roots {self.max_roots}")
         if not (roots.is_cuda and roots.dtype == torch.int32 and root_ts.is_cuda and root_ts.dtype == torch.float32):
             raise TypeError("roots must be CUDA int32 and root_ts CUDA float32 (no CPU fallback)")
+        if root_keys is not None:
+            if not (root_keys.is_cuda and root_keys.dtype == torch.int64):
+                raise TypeError("root_keys must be a CUDA int64 tensor (uint64 bit patterns)")
+            _rc(_L.tgl_sample_keyed(self.g.handle, _ptr(roots), _ptr(root_ts), _ptr(root_keys), n, self.L, self._fan,
+                                    self.strategy, self.S, self.snapshot_len, int(seed) & 0xFFFFFFFFFFFFFFFF,
+                                    self._c_blocks, _ptr(self.workspace), self.ws_bytes, _stream(stream)),
+                "tgl_sample_keyed")
+            return self.blocks
         _rc(_L.tgl_sample(self.g.handle, _ptr(roots), _ptr(root_ts), n, self.L, self._fan, self.strategy, self.S,
                           self.snapshot_len, int(seed) & 0xFFFFFFFFFFFFFFFF, int(root_key_base) & 0xFFFFFFFFFFFFFFFF,
                           self._c_blocks, _ptr(self.workspace), self.ws_bytes, _stream(stream)), "tgl_sample")
@@ -261,15 +272,51 @@ def check(g: Optional[TCSR] = None, stream=None) -> int:
     return _L.tgl_check(None if g is None else g.handle, _stream(stream))
 
 
+def set_node_base(g: TCSR, node_lo: int) -> None:
+    """tgl_tcsr_set_node_base: g holds the lists of global nodes [node_lo, node_lo + g.n_nodes)."""
+    _rc(_L.tgl_tcsr_set_node_base(g.handle, int(node_lo)), "tgl_tcsr_set_node_base")
+    g.node_lo = int(node_lo)
+
+
+def offsets_to_counts(offsets: torch.Tensor, n: int, out: Optional[torch.Tensor] = None, stream=None):
+    """tgl_offsets_to_counts: per-root counts (int32) of a CSR block."""
+    offsets = _cuda(offsets, torch.int64, "offsets")
+    out = torch.empty(max(n, 0), dtype=torch.int32, device=offsets.device) if out is None else out
+    _rc(_L.tgl_offsets_to_counts(_ptr(offsets), int(n), _ptr(out), _stream(stream)), "tgl_offsets_to_counts")
+    return out
+
+
+def shard_unpermute(perm: torch.Tensor, counts_in: torch.Tensor, nbr_in: torch.Tensor, eid_in: torch.Tensor,
+                    dt_in: torch.Tensor, stream=None):
+    """tgl_shard_unpermute: CSR block in bucket order (per-root counts) -> the same block in original
+    root order (offsets, nbr, eid, dt)."""
+    perm = _cuda(perm, torch.int32, "perm")
+    counts_in = _cuda(counts_in, torch.int32, "counts_in")
+    n = perm.numel()
+    dev = perm.device
+    wsb = ctypes.c_size_t()
+    _rc(_L.tgl_shard_unpermute_workspace(n, ctypes.byref(wsb)), "tgl_shard_unpermute_workspace")
+    ws = torch.empty(max(wsb.value, 1), dtype=torch.uint8, device=dev)
+    nnz = nbr_in.numel()
+    off = torch.empty(n + 1, dtype=torch.int64, device=dev)
+    nbr = torch.empty(nnz, dtype=torch.int32, device=dev)
+    eid = torch.empty(nnz, dtype=torch.int32, device=dev)
+    dt = torch.empty(nnz, dtype=torch.float32, device=dev)
+    _rc(_L.tgl_shard_unpermute(_ptr(perm), n, _ptr(counts_in), _ptr(nbr_in), _ptr(eid_in), _ptr(dt_in), _ptr(off),
+                               _ptr(nbr), _ptr(eid), _ptr(dt), _ptr(ws), wsb.value, _stream(stream)),
+        "tgl_shard_unpermute")
+    return off, nbr, eid, dt
+
+
 def shard_bucket(roots: torch.Tensor, splits: torch.Tensor, world: int, stream=None):
-    """tgl_shard_bucket: stable permutation of roots by owner shard + per-shard counts."""
+    """tgl_shard_bucket: stable permutation (int32) of roots by owner shard + per-shard counts."""
     roots = _cuda(roots, torch.int32, "roots")
     splits = _cuda(splits, torch.int64, "splits")
     n = roots.numel()
     wsb = ctypes.c_size_t()
     _rc(_L.tgl_shard_bucket_workspace(n, int(world), ctypes.byref(wsb)), "tgl_shard_bucket_workspace")
     ws = torch.empty(max(wsb.value, 1), dtype=torch.uint8, device=roots.device)
-    perm = torch.empty(max(n, 1), dtype=torch.int64, device=roots.device)
+    perm = torch.empty(max(n, 1), dtype=torch.int32, device=roots.device)
     counts = torch.empty(int(world), dtype=torch.int64, device=roots.device)
     _rc(_L.tgl_shard_bucket(_ptr(roots), n, _ptr(splits), int(world), _ptr(perm), _ptr(counts), _ptr(ws),
                             wsb.value, _stream(stream)), "tgl_shard_bucket")

@@ -44,6 +44,11 @@ SIGNATURES = {
     "tgl_tcsr_info": (ctypes.c_int, [P, ctypes.POINTER(i32), ctypes.POINTER(i64)]),
     "tgl_sample_capacity": (ctypes.c_int, [i64, i32, P, i32, ctypes.c_int, f32, P, P, ctypes.POINTER(sz)]),
     "tgl_sample": (ctypes.c_int, [P, P, P, i64, i32, P, ctypes.c_int, i32, f32, u64, u64, P, P, sz, P]),
+    "tgl_sample_keyed": (ctypes.c_int, [P, P, P, P, i64, i32, P, ctypes.c_int, i32, f32, u64, P, P, sz, P]),
+    "tgl_tcsr_set_node_base": (ctypes.c_int, [P, i64]),
+    "tgl_shard_unpermute_workspace": (ctypes.c_int, [i64, ctypes.POINTER(sz)]),
+    "tgl_offsets_to_counts": (ctypes.c_int, [P, i64, P, P]),
+    "tgl_shard_unpermute": (ctypes.c_int, [P, i64, P, P, P, P, P, P, P, P, P, sz, P]),
     "tgl_gather": (ctypes.c_int, [P, i64, P, P, i32, P]),
     "tgl_check": (ctypes.c_int, [P, P]),
     "tgl_shard_bucket_workspace": (ctypes.c_int, [i64, i32, ctypes.POINTER(sz)]),

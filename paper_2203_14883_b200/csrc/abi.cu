@@ -74,6 +74,12 @@ extern "C" int tgl_tcsr_wrap(const int64_t* indptr, const int32_t* nbr, const fl
     return TGL_OK;
 }
 
+extern "C" int tgl_tcsr_set_node_base(tgl_tcsr* g, int64_t node_lo) {
+    if (!g || node_lo < 0 || node_lo + g->n_nodes >= (int64_t(1) << 31)) return TGL_EINVAL;
+    g->node_lo = node_lo;
+    return TGL_OK;
+}
+
 extern "C" int tgl_tcsr_destroy(tgl_tcsr* g) {
     if (!g) return TGL_EINVAL;
     if (g->err_dev) cudaFree(g->err_dev);

@@ -125,7 +125,7 @@ __global__ void __launch_bounds__(kRadixThreads) radix_downsweep_kernel(
     Stream s, const uint32_t* __restrict__ keys_in, const uint32_t* __restrict__ vals_in, uint64_t n, int shift,
     uint32_t mask, const uint32_t* __restrict__ offsets, uint64_t ntiles, uint32_t* __restrict__ keys_out,
     uint32_t* __restrict__ vals_out, int32_t* __restrict__ nbr_out, float* __restrict__ ts_out,
-    int32_t* __restrict__ eid_out, int64_t* __restrict__ perm_out) {
+    int32_t* __restrict__ eid_out, int32_t* __restrict__ perm_out) {
     __shared__ uint32_t wcnt[kRadixWarps][kRadixBins];
     __shared__ uint32_t dbase[kRadixBins];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -177,7 +177,7 @@ __global__ void __launch_bounds__(kRadixThreads) radix_downsweep_kernel(
             ts_out[pos] = s.ts[i];
             eid_out[pos] = s.eid ? s.eid[i] : (int32_t)i;
         } else if (DST == kDstPerm) {
-            perm_out[pos] = (int64_t)val[r];
+            perm_out[pos] = (int32_t)val[r];
         } else {
             keys_out[pos] = key[r];
             vals_out[pos] = val[r];
@@ -412,16 +412,16 @@ static ShardPlan plan_shard(int64_t n, void* ws) {
 
 extern "C" int tgl_shard_bucket_workspace(int64_t n_roots, int32_t world, size_t* bytes) {
     if (!bytes || n_roots < 0 || world < 1 || world > kRadixBins) return TGL_EINVAL;
-    if ((uint64_t)n_roots >= (1ull << 32)) return TGL_EINVAL;
+    if ((uint64_t)n_roots >= (1ull << 31)) return TGL_EINVAL;
     *bytes = plan_shard(n_roots, nullptr).bytes;
     return TGL_OK;
 }
 
 extern "C" int tgl_shard_bucket(const int32_t* roots, int64_t n_roots, const int64_t* splits, int32_t world,
-                                int64_t* perm, int64_t* counts, void* workspace, size_t ws_bytes, void* stream) {
+                                int32_t* perm, int64_t* counts, void* workspace, size_t ws_bytes, void* stream) {
     if (n_roots < 0 || world < 1 || world > kRadixBins || !splits || !counts || !workspace) return TGL_EINVAL;
     if (n_roots > 0 && (!roots || !perm)) return TGL_EINVAL;
-    if ((uint64_t)n_roots >= (1ull << 32)) return TGL_EINVAL;
+    if ((uint64_t)n_roots >= (1ull << 31)) return TGL_EINVAL;
     int rc = check_device();
     if (rc) return rc;
     ShardPlan p = plan_shard(n_roots, workspace);

@@ -92,4 +92,5 @@ struct tgl_tcsr {
     int n_levels;
     uint64_t level_off[12];  // float offset of level l in index (levels <= 8)
     const int2* payload;     // interleaved (nbr, eid) per slot, or null
+    int64_t node_lo;         // node-sharded handle: global id of local node 0
 };

@@ -67,9 +67,10 @@ struct SampleParams {
     const float* lvl[kMaxIndexLevels + 1];  // lvl[l] = index level l (1-based)
     int32_t n_levels;                       // < 0 -> plain binary search
     int32_t n_nodes;
+    int64_t node_lo;  // node-sharded handles: global id of local node 0 (0 otherwise)
     const int32_t* root_node;
     const float* root_ts;
-    const uint64_t* root_key;  // l >= 1 (uniform): parent layer's child keys; null at layer 0
+    const uint64_t* root_key;  // explicit root keys (layer 0: caller's, may be null; l >= 1: parent's)
     const float* root_lo;      // l >= 1: inherited lower bounds; null -> -inf
     uint64_t root_key_base;
     int64_t n_roots;                // layer 0: count; l >= 1: capacity
@@ -215,9 +216,10 @@ __global__ void __launch_bounds__(G * kTile) window_kernel(const __grid_constant
     float t = 0.0f;
     bool ok = false;
     if (valid) {
-        v = p.root_node[i];
+        const int64_t vg = (int64_t)p.root_node[i] - p.node_lo;  // shard-local node id
+        v = (int32_t)vg;
         t = p.root_ts[i];
-        if ((uint32_t)v >= (uint32_t)p.n_nodes) {
+        if (vg < 0 || vg >= (int64_t)p.n_nodes) {
             if (Q.q == 0) atomicOr(p.err, kErrRange);
         } else if (!isfinite(t)) {
             if (Q.q == 0) atomicOr(p.err, kErrInval);
@@ -381,7 +383,7 @@ __global__ void __launch_bounds__(kCopyThreads) copy_kernel(const __grid_constan
     troot[lane] = t;
     uint64_t rk = 0;
     if (STRATEGY == TGL_UNIFORM) {
-        rk = p.layer == 0 ? p.root_key_base + (uint64_t)i : (valid ? p.root_key[i] : 0ull);
+        rk = p.root_key ? (valid ? p.root_key[i] : 0ull) : p.root_key_base + (uint64_t)i;
         rkey[lane] = rk;
     }
     // counts, warp-local prefix, window descriptors; uniform picks
@@ -610,10 +612,10 @@ extern "C" int tgl_sample_capacity(int64_t n_roots, int32_t n_layers, const int3
     return TGL_OK;
 }
 
-extern "C" int tgl_sample(const tgl_tcsr* g, const int32_t* roots, const float* root_ts, int64_t n_roots,
-                          int32_t n_layers, const int32_t* fanouts, tgl_strategy strategy, int32_t n_snapshots,
-                          float snapshot_len, uint64_t seed, uint64_t root_key_base, tgl_block* out, void* workspace,
-                          size_t ws_bytes, void* stream) {
+static int sample_impl(const tgl_tcsr* g, const int32_t* roots, const float* root_ts, const uint64_t* root_keys,
+                       int64_t n_roots, int32_t n_layers, const int32_t* fanouts, tgl_strategy strategy,
+                       int32_t n_snapshots, float snapshot_len, uint64_t seed, uint64_t root_key_base, tgl_block* out,
+                       void* workspace, size_t ws_bytes, void* stream) {
     if (!g || !out || !workspace) return TGL_EINVAL;
     if (n_roots > 0 && (!roots || !root_ts)) return TGL_EINVAL;
     static thread_local SamplePlan P;
@@ -648,9 +650,11 @@ extern "C" int tgl_sample(const tgl_tcsr* g, const int32_t* roots, const float* 
         if (indexed)
             for (int q = 1; q <= g->n_levels; ++q) sp.lvl[q] = g->index + g->level_off[q];
         sp.n_nodes = g->n_nodes;
+        sp.node_lo = g->node_lo;
         if (l == 0) {
             sp.root_node = roots;
             sp.root_ts = root_ts;
+            sp.root_key = root_keys;
             sp.n_roots = n_roots;
         } else {
             const tgl_block& par = out[(l - 1) * S + s];
@@ -710,4 +714,21 @@ extern "C" int tgl_sample(const tgl_tcsr* g, const int32_t* roots, const float* 
         }
     }
     return TGL_OK;
+}
+
+extern "C" int tgl_sample(const tgl_tcsr* g, const int32_t* roots, const float* root_ts, int64_t n_roots,
+                          int32_t n_layers, const int32_t* fanouts, tgl_strategy strategy, int32_t n_snapshots,
+                          float snapshot_len, uint64_t seed, uint64_t root_key_base, tgl_block* out, void* workspace,
+                          size_t ws_bytes, void* stream) {
+    return sample_impl(g, roots, root_ts, nullptr, n_roots, n_layers, fanouts, strategy, n_snapshots, snapshot_len,
+                       seed, root_key_base, out, workspace, ws_bytes, stream);
+}
+
+extern "C" int tgl_sample_keyed(const tgl_tcsr* g, const int32_t* roots, const float* root_ts,
+                                const uint64_t* root_keys, int64_t n_roots, int32_t n_layers, const int32_t* fanouts,
+                                tgl_strategy strategy, int32_t n_snapshots, float snapshot_len, uint64_t seed,
+                                tgl_block* out, void* workspace, size_t ws_bytes, void* stream) {
+    if (n_roots > 0 && !root_keys) return TGL_EINVAL;
+    return sample_impl(g, roots, root_ts, root_keys, n_roots, n_layers, fanouts, strategy, n_snapshots, snapshot_len,
+                       seed, 0, out, workspace, ws_bytes, stream);
 }

@@ -1,0 +1,150 @@
+"""Node-sharded sampling: the T-CSR split by node ranges over the ranks.
+
+For graphs larger than one GPU's HBM the T-CSR is split into contiguous node ranges balanced by
+edges; the node v is owned by shard r with splits[r] <= v < splits[r+1].  One sampling call:
+
+  1. K8  tgl_shard_bucket     stable bucketing of the local roots by owner shard (perm, counts)
+  2. K7  tgl_gather           pack the requests (node, t, root key) in bucket order
+  3.     all-to-all-v         requests to their owners (NCCL through torch.distributed)
+  4. K4  tgl_sample_keyed     each owner samples the roots it received, with the roots' GLOBAL keys
+                              (R#7), so the bits equal the replicated mode's
+  5.     all-to-all-v         replies: per-root counts + (nbr, eid, dt) edges, per snapshot block
+  6. K8b tgl_shard_unpermute  back to the original root order: the exact replicated-mode blocks
+
+Steps 1, 2, 4, 6 are the library's kernels; 3 and 5 are the collective (the path's real exchange
+step).  The exchange object is pluggable: `DistExchange` (torch.distributed all_to_all_single:
+NCCL on GPUs, gloo on CPU tests) or a test double.  `ops` is pluggable the same way so the
+exchange protocol can be exercised on CPU with world_size 2 (tests/test_sharded_gloo.py); the
+product default is `CudaOps`, which only calls libtgl.so.  Single layer (the C5 configuration);
+multi-layer node-sharded sampling is NEXT in DESIGN.md.
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+from typing import List, Optional, Sequence
+
+import torch
+
+
+def edge_balanced_splits(indptr: torch.Tensor, world: int) -> torch.Tensor:
+    """splits[r] = first node whose list starts at or after r * E_s / world (int64 [world+1])."""
+    V = indptr.numel() - 1
+    E = int(indptr[-1].item())
+    targets = torch.tensor([E * r // world for r in range(world + 1)], dtype=torch.int64, device=indptr.device)
+    s = torch.searchsorted(indptr[:V].contiguous(), targets, right=False)
+    s[0], s[-1] = 0, V
+    return torch.cummax(s, 0).values
+
+
+class DistExchange:
+    """all-to-all-v over torch.distributed (NCCL or gloo)."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+        self.dist = dist
+        self.group = group
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+
+    def splits(self, send_counts: torch.Tensor) -> torch.Tensor:
+        """Exchange per-peer element counts (int64 [world]) -> counts to receive from each peer."""
+        recv = torch.empty_like(send_counts)
+        self.dist.all_to_all_single(recv, send_counts.contiguous(), group=self.group)
+        return recv
+
+    def exchange(self, t: torch.Tensor, send_splits: Sequence[int], recv_splits: Sequence[int]) -> torch.Tensor:
+        out = torch.empty((int(sum(recv_splits)),) + tuple(t.shape[1:]), dtype=t.dtype, device=t.device)
+        self.dist.all_to_all_single(out, t.contiguous(), list(map(int, recv_splits)), list(map(int, send_splits)),
+                                    group=self.group)
+        return out
+
+
+class CudaOps:
+    """The product ops: libtgl.so kernels only."""
+
+    def __init__(self, shard, fanout: int, strategy, n_snapshots: int, snapshot_len: float, max_roots: int):
+        from . import Sampler
+        import paper_2203_14883_b200 as tgl
+        self.tgl = tgl
+        self.sampler = Sampler(shard, max(max_roots, 1), [fanout], strategy, n_snapshots, snapshot_len)
+
+    def bucket(self, roots, splits, world):
+        return self.tgl.shard_bucket(roots, splits, world)
+
+    def pack(self, perm, roots, root_ts, keys):
+        r, t, k = self.tgl.gather(perm, [roots, root_ts, keys])
+        return r, t, k
+
+    def sample(self, roots, root_ts, keys, seed):
+        """-> per snapshot (counts int32 [n], nbr, eid, dt) over the received roots."""
+        n = roots.numel()
+        blocks = self.sampler.run(roots, root_ts, root_keys=keys, seed=seed, n_roots=n)
+        out = []
+        for b in blocks:
+            nnz = int(b.nnz_dev.item())
+            cnt = self.tgl.offsets_to_counts(b.offsets, n)
+            out.append((cnt, b.nbr[:nnz], b.eid[:nnz], b.dt[:nnz], b.offsets[: n + 1]))
+        return out
+
+    def unpermute(self, perm, counts, nbr, eid, dt):
+        return self.tgl.shard_unpermute(perm, counts, nbr, eid, dt)
+
+
+@dataclass
+class ShardedBlock:
+    offsets: torch.Tensor
+    nbr: torch.Tensor
+    eid: torch.Tensor
+    dt: torch.Tensor
+
+
+class NodeShardedSampler:
+    """One rank's view of the node-sharded sampler (1 layer, S snapshots)."""
+
+    def __init__(self, splits: torch.Tensor, exchange, ops, n_snapshots: int, seed: int):
+        self.splits = splits
+        self.ex = exchange
+        self.ops = ops
+        self.S = int(n_snapshots)
+        self.seed = int(seed)
+
+    def run(self, roots: torch.Tensor, root_ts: torch.Tensor, root_key_base: int) -> List[ShardedBlock]:
+        W = self.ex.world
+        n = roots.numel()
+        dev = roots.device
+        keys = torch.arange(root_key_base, root_key_base + n, dtype=torch.int64, device=dev)
+        perm, counts = self.ops.bucket(roots, self.splits, W)                 # K8
+        send_roots = counts.to(torch.int64)
+        recv_roots = self.ex.splits(send_roots)
+        sr, rr = send_roots.tolist(), recv_roots.tolist()
+        p_nodes, p_ts, p_keys = self.ops.pack(perm, roots, root_ts, keys)     # K7 (bucket order)
+        q_nodes = self.ex.exchange(p_nodes, sr, rr)                          # requests -> owners
+        q_ts = self.ex.exchange(p_ts, sr, rr)
+        q_keys = self.ex.exchange(p_keys, sr, rr)
+        local = self.ops.sample(q_nodes, q_ts, q_keys, self.seed)            # K4 on the local shard
+        seg = [0]
+        for c in rr:
+            seg.append(seg[-1] + int(c))
+        out = []
+        for (cnt, nbr, eid, dt, off) in local:
+            bounds = off[torch.tensor(seg, dtype=torch.int64, device=off.device)].tolist()
+            send_edges = [bounds[p + 1] - bounds[p] for p in range(W)]
+            recv_edges = self.ex.splits(torch.tensor(send_edges, dtype=torch.int64, device=dev)).tolist()
+            r_cnt = self.ex.exchange(cnt, rr, sr)                            # replies -> sources
+            r_nbr = self.ex.exchange(nbr, send_edges, recv_edges)
+            r_eid = self.ex.exchange(eid, send_edges, recv_edges)
+            r_dt = self.ex.exchange(dt, send_edges, recv_edges)
+            o, nb, ed, d = self.ops.unpermute(perm, r_cnt, r_nbr, r_eid, r_dt)  # K8b
+            out.append(ShardedBlock(o, nb, ed, d))
+        return out
+
+
+def slice_shard(g, lo: int, hi: int):
+    """Setup helper: the shard of a full T-CSR for nodes [lo, hi) as its own handle (copies)."""
+    import paper_2203_14883_b200 as tgl
+    a, b = int(g.indptr[lo].item()), int(g.indptr[hi].item())
+    indptr = (g.indptr[lo:hi + 1] - a).contiguous()
+    sh = tgl.wrap(indptr, g.nbr[a:b].clone(), g.ts[a:b].clone(), g.eid[a:b].clone())
+    tgl.set_node_base(sh, lo)
+    return sh

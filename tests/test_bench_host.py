@@ -1,0 +1,65 @@
+"""Host logic of bench.py (no GPU): the algorithmic-bytes model, root-sharded chunk assignment,
+and the max-over-ranks / sum-of-work reporting under torch.distributed (gloo, world_size 2)."""
+import math
+import os
+import subprocess
+import sys
+import textwrap
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import bench  # noqa: E402
+from synth import configs as C  # noqa: E402
+
+
+def test_algorithmic_bytes_model_c5():
+    cfg = C.CONFIGS["C5"]                      # 1 layer, S = 3, t_s = 5: 80 B / root + 24 B / edge
+    assert bench.algorithmic_bytes(cfg, [1], [0]) == 80
+    assert bench.algorithmic_bytes(cfg, [1000], [6300]) == 80 * 1000 + 24 * 6300
+
+
+def test_algorithmic_bytes_model_two_layer():
+    cfg = C.CONFIGS["C2"]                      # L = 2, S = 1, t_s = inf
+    # layer 0: 8 + 16 + 8 + 8 = 40 / root, 28 / edge; layer 1: 8 + 16 + 8 + 8 = 40 / root, 24 / edge
+    assert bench.algorithmic_bytes(cfg, [600, 6000], [6000, 60000]) == 40 * 600 + 28 * 6000 + 40 * 6000 + 24 * 60000
+
+
+@pytest.mark.parametrize("world", [1, 2, 4, 8])
+def test_rank_chunks_disjoint_cover(world):
+    cfg = C.CONFIGS["C5"]
+    chunk, steps = 2048 * cfg.batch, 33
+    per_rank = [bench.rank_chunks(cfg.n_roots_epoch, chunk, steps, world, r, cfg.batch) for r in range(world)]
+    allc = sorted(x for p in per_rank for x in p)
+    assert len(set(allc)) == len(allc) == steps * world               # disjoint
+    assert all(x % cfg.batch == 0 for x in allc)                       # batch aligned
+    assert all(0 <= x <= cfg.n_roots_epoch - chunk for x in allc)
+    gaps = [b - a for a, b in zip(allc, allc[1:])]
+    assert min(gaps) >= chunk                                          # chunks never overlap
+
+
+REPORT = textwrap.dedent(r'''
+    import os, sys
+    sys.path.insert(0, os.environ["REPO"])
+    import torch, torch.distributed as dist
+    import bench
+    dist.init_process_group("gloo")
+    r = dist.get_rank()
+    e, b, ms = bench.reduce_report(100.0 * (r + 1), 10.0, 5.0 + r, 2, torch.device("cpu"))
+    assert (e, b, ms) == (300.0, 20.0, 6.0), (e, b, ms)
+    print("ok", r)
+    dist.destroy_process_group()
+''')
+
+
+def test_reduce_report_gloo_world2(tmp_path):
+    script = tmp_path / "rep.py"
+    script.write_text(REPORT)
+    env = dict(os.environ, REPO=ROOT)
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+                        "--master-addr=127.0.0.1", "--master-port=29655", str(script)],
+                       env=env, capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stderr[-3000:]
+    assert r.stdout.count("ok") == 2
