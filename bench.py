@@ -214,9 +214,7 @@ def run_ours(args):
     chunks = [C.roots(cfg, src, dst, ts, s0, chunk) for s0 in mine]
     sampler = tgl.Sampler(g, chunk, cfg.fanouts, cfg.strategy, cfg.n_snapshots, cfg.snapshot_len)
     L, S = len(cfg.fanouts), cfg.n_snapshots
-    chunk_roots = int(os.environ.get("TGL_CHUNK_ROOTS", 1 << 40))  # library default: one chunk per call
-    n_chunks0 = max(1, -(-chunk // chunk_roots))
-    launches_per_step = 3 * (n_chunks0 + (L - 1) * S)  # window + tile scan + copy per chunk / chain
+    launches_per_step = 3 * (1 + (L - 1) * S)  # window + tile scan + copy per chain
     stream = torch.cuda.current_stream()
 
     for w in range(args.warmup):

@@ -94,8 +94,8 @@ TGL_API int tgl_tcsr_build_workspace(int64_t n_edges, int32_t n_nodes, int add_r
  *   sampler reads timestamps in aligned 16-float (64-byte, one HBM atom) groups.
  * aux (optional, may be NULL): >= tgl_tcsr_aux_bytes(E_s) bytes, 256-byte aligned; filled with the
  *   sampler's acceleration structures over the T-CSR: the 16-ary atom index over ts_out (cut
- *   search) and an interleaved copy of (nbr, eid) per slot (payload copy) -- DESIGN.md "Data
- *   layout".  Without it the sampler falls back to binary search and separate nbr / eid reads.
+ *   search) and a 16-byte record {ts, nbr, eid, 0} per slot, so search and payload copy read the
+ *   same lines -- DESIGN.md "Data layout".  Without it the sampler reads the separate arrays.
  * workspace: >= tgl_tcsr_build_workspace() bytes of device memory, 256-byte aligned.
  * Synchronous validation: the call blocks on `stream` once to read the device validation word;
  *   on ERANGE / EINVAL / EUNSORTED no handle is returned and outputs are unspecified.

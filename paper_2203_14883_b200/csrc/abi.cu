@@ -68,7 +68,7 @@ extern "C" int tgl_tcsr_wrap(const int64_t* indptr, const int32_t* nbr, const fl
     g->index = static_cast<const float*>(aux);
     g->n_levels = aux ? lay.index.n_levels : 0;
     for (int l = 0; l <= kMaxIndexLevels && l < 12; ++l) g->level_off[l] = lay.index.off[l];
-    g->payload = aux ? reinterpret_cast<const int2*>(static_cast<const char*>(aux) + lay.payload_off) : nullptr;
+    g->recs = aux ? static_cast<const void*>(static_cast<const char*>(aux) + lay.rec_off) : nullptr;
     cudaGetDevice(&g->device);
     *out = g;
     return TGL_OK;

@@ -245,9 +245,9 @@ __global__ void aux_build_kernel(const float* __restrict__ ts, const int32_t* __
         for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < lay.index.len[l]; j += stride)
             out[j] = ts[j << sh];
     }
-    int2* pay = reinterpret_cast<int2*>(aux + lay.payload_off);
+    int4* rec = reinterpret_cast<int4*>(aux + lay.rec_off);
     for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += stride)
-        pay[j] = make_int2(nbr[j], eid[j]);
+        rec[j] = make_int4(__float_as_int(ts[j]), nbr[j], eid[j], 0);
 }
 }  // namespace tgl
 

@@ -91,6 +91,6 @@ struct tgl_tcsr {
     const float* index;      // 16-ary atom index over ts (tsindex.cuh), or null
     int n_levels;
     uint64_t level_off[12];  // float offset of level l in index (levels <= 8)
-    const int2* payload;     // interleaved (nbr, eid) per slot, or null
+    const void* recs;        // 16-byte slot records {ts, nbr, eid, 0} (tsindex.cuh), or null
     int64_t node_lo;         // node-sharded handle: global id of local node 0
 };

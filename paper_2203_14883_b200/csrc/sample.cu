@@ -1,32 +1,27 @@
 // sample.cu -- the parallel temporal sampler of TGL (Alg. 1) on B200.
 //
 // Per layer chain (layer 0: one chain covering all S dynamic snapshots of a root, whose S+1 cuts
-// share the indptr pair and narrow each other's range; layer l >= 1: one chain per snapshot s
-// whose roots are block (l-1, s)'s outputs, Alg. 1, R#3) the roots are processed
-// in chunks of C roots (C sized so one chunk's working set stays in the 126 MB L2), and per chunk
-// three kernels run on the caller's stream with no inter-CTA waiting anywhere:
+// share the indptr pair and narrow each other's range; layer l >= 1: one chain per snapshot s whose
+// roots are block (l-1, s)'s outputs, Alg. 1, R#3) three kernels run on the caller's
+// stream, with no inter-CTA waiting anywhere (measured faster on B200 than one fused kernel with a
+// decoupled look-back, whose tiles wait on slow predecessors: profiles/r01):
 //
-//   K4a window_kernel  a QUAD of 4 lanes per root (each lane loads 16 B, so one 64-byte group of 16
-//                      timestamps is ONE coalesced request -- HBM serves ~33 G random requests/s
-//                      whatever their size up to 128 B):
-//                      indptr pair, S+1 cut searches (lower_bound) over the node's time-sorted
-//                      list through the 16-ary atom index (tsindex.cuh) -- the stateless
-//                      replacement of the paper's per-node pointers pt_0..pt_S (Sec. 3.1
-//                      "Sampling", L260-L262).  Writes per (snapshot, root) the window descriptor
-//                      and per (snapshot, 256-root tile) the number of edges the tile emits:
+//   K4a window_kernel  one lane per root: indptr pair, S+1 cut searches (lower_bound) over the
+//                      node's time-sorted ts list -- the stateless replacement of the paper's
+//                      per-node pointers pt_0..pt_S (Sec. 3.1 "Sampling", L260-L262) -- through the
+//                      16-ary index (tsindex.cuh) for long lists.  Writes per (snapshot, root) the
+//                      window descriptor and per (snapshot, 256-root tile) the edge count:
 //                      most_recent -> min(k, c) "closest to the end pointer";
-//                      uniform -> min(k, c) (R#5).  most_recent also prefetches the payload lines
-//                      of the selected window into L2 (fire-and-forget: extra memory-level
-//                      parallelism, and K4b then reads L2).
-//   K5  tile_scan      one CTA: exclusive scan of the per-tile totals (+ the running total of the
-//                      previous chunks) -> tile bases; the last chunk writes nnz, n_roots,
+//                      uniform -> min(k, c) (R#5).
+//   K5  tile_scan      one CTA: exclusive scan of the per-tile totals -> tile bases, nnz, n_roots,
 //                      offsets[n].  Deterministic: no atomic decides a position.
 //   K4b copy_kernel    one warp per 32 roots: warp scan of its counts + tile base -> offsets[i];
 //                      uniform: Floyd's k-subset with Philox4x32-10 draws, ascending (R#5, R#6);
 //                      then the tile's outputs are copied as one flat range per snapshot -- lane o
-//                      finds its root by a 5-step search over the warp's inclusive counts -- so
-//                      loads of (nbr, eid) pairs and ts, and stores of (nbr, eid, dt[, ts_edge,
-//                      child key, child lo]) are coalesced runs and every lane is busy (a9, a10).
+//                      finds its root by a 5-step search over the warp's inclusive counts -- loading
+//                      the selected 16-byte slot record {ts, nbr, eid} (one request per run of
+//                      slots) and storing (nbr, eid, dt[, ts_edge, child key, child lo]) as
+//                      coalesced runs (a9, a10; K6 fused).
 // dt = t_root (-) t_edge with __fsub_rn; window bounds with __fmul_rn / __fsub_rn (R#12).
 // Everything strictly before the root: ts < U = t.
 #include <algorithm>
@@ -39,12 +34,11 @@
 
 namespace tgl {
 
-constexpr int kTile = 256;              // roots per tile (scan granularity)
-constexpr int kCopyThreads = kTile;     // copy kernel: one lane per root in the prologue
-constexpr int kCopyWarps = kCopyThreads / 32;
+constexpr int kTile = 256;  // roots per tile (one lane per root)
+constexpr int kWarps = kTile / 32;
 constexpr int kCopyUnroll = 4;
+constexpr uint32_t kIndexMin = 256;          // lists longer than this descend the 16-ary index
 constexpr int kPicksSmemPerWarp = 8 * 1024;  // bytes of uniform picks kept in shared memory per warp
-constexpr int64_t kDefaultChunk = int64_t(1) << 40;  // no chunking (measured best on B200)
 
 struct BlockOut {
     int64_t* offsets;
@@ -63,9 +57,9 @@ struct SampleParams {
     const int32_t* nbr;
     const float* ts;
     const int32_t* eid;
-    const int2* payload;                    // interleaved (nbr, eid), or null
+    const int4* recs;                       // 16-byte slot records {ts, nbr, eid, 0}, or null
     const float* lvl[kMaxIndexLevels + 1];  // lvl[l] = index level l (1-based)
-    int32_t n_levels;                       // < 0 -> plain binary search
+    int32_t n_levels;                       // 0 -> no index
     int32_t n_nodes;
     int64_t node_lo;  // node-sharded handles: global id of local node 0 (0 otherwise)
     const int32_t* root_node;
@@ -75,20 +69,15 @@ struct SampleParams {
     uint64_t root_key_base;
     int64_t n_roots;                // layer 0: count; l >= 1: capacity
     const int64_t* n_roots_dev_in;  // l >= 1: device count (parent block's nnz)
-    int64_t root_begin;             // first root of this chunk
-    int64_t chunk_cap;              // roots in this chunk (capacity)
-    int32_t first_chunk, last_chunk;
-    int32_t prefetch;  // most_recent: prefetch the selected payload into L2
     int32_t layer, nsb, snap0, k;
     float snapshot_len;
     uint32_t seed_lo, seed_hi;
-    uint32_t* win_first;  // [nsb][chunk_cap] first slot (uniform: a; most_recent: b - take)
-    uint32_t* win_len;    // [nsb][chunk_cap] uniform: window size c; most_recent: take = min(k, c)
+    uint32_t* win_first;  // [nsb][roots_cap] first slot (uniform: a; most_recent: b - take)
+    uint32_t* win_len;    // [nsb][roots_cap] uniform: window size c; most_recent: take = min(k, c)
     uint32_t* tile_tot;   // [nsb][tiles_cap] edges emitted per tile
-    uint64_t* tile_base;  // [nsb][tiles_cap] exclusive prefix of tile_tot (incl. previous chunks)
-    uint64_t* carry;      // [nsb] running total over chunks
-    int64_t tiles_cap;
-    uint32_t* picks_global;  // null -> picks in shared memory; else [tiles_cap*8 warps][nsb*k][32]
+    uint64_t* tile_base;  // [nsb][tiles_cap] exclusive prefix of tile_tot
+    int64_t roots_cap, tiles_cap;
+    uint32_t* picks_global;  // null -> picks in shared memory; else [tiles_cap * 8 warps][nsb*k][32]
     int* err;
     BlockOut out[TGL_MAX_SNAPSHOTS];
 };
@@ -102,75 +91,14 @@ __device__ __forceinline__ int64_t chain_roots(const SampleParams& p) {
     return n > 0 ? n : 0;
 }
 
-__device__ __forceinline__ void prefetch_l2(const void* ptr) { asm volatile("prefetch.global.L2 [%0];" ::"l"(ptr)); }
-
-// ---------------------------------------------------------------------------- cut search (quad)
-// A quad of lanes cooperates on one root: a 64-byte group (16 floats, one HBM atom) is read as
-// four 16-byte lane loads in ONE instruction, i.e. one request.  All four lanes carry the same
-// root state and take the same branches, so quad-masked shuffles / reductions are safe.
-struct Quad {
-    uint32_t mask;  // the G lanes of this root group
-    int q;          // lane index within the group
-    int G;          // lanes per root (1, 2 or 4)
-};
-
-// 16-bit mask: bit i set iff element i of group g of arr is < x.  The G lanes of a root each load
-// 4/G float4s of the 64-byte group (G = 4: one coalesced request; G = 1: four per-lane loads).
-__device__ __forceinline__ uint32_t group_lt(const float* __restrict__ arr, uint64_t g, float x, const Quad& Q) {
-    const float4* base = reinterpret_cast<const float4*>(arr + (g << 4));
-    const int per = 4 / Q.G;
-    uint32_t m = 0;
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-        if (j < per) {
-            const int slot = Q.q * per + j;
-            const float4 f = __ldg(base + slot);
-            m |= ((uint32_t)(f.x < x) | ((uint32_t)(f.y < x) << 1) | ((uint32_t)(f.z < x) << 2) |
-                  ((uint32_t)(f.w < x) << 3))
-                 << (4 * slot);
-        }
-    }
-    return Q.G == 1 ? m : __reduce_or_sync(Q.mask, m);
-}
-
-// mask of positions [from, to) of group g (positions are global indices, group = 16 entries)
-__device__ __forceinline__ uint32_t range_bits(uint64_t g, uint64_t from, uint64_t to) {
-    const uint64_t g0 = g << 4;
-    const int lo = from > g0 ? (int)(from - g0) : 0;
-    const int hi = to < g0 + 16 ? (int)(to - g0) : 16;
-    if (hi <= lo) return 0u;
-    return ((1u << hi) - 1u) & ~((1u << lo) - 1u);
-}
-
-// number of entries of arr[from, to) that are < x, for to - from <= 32 (spans <= 3 groups)
-__device__ __forceinline__ uint32_t count_lt_small(const float* __restrict__ arr, uint64_t from, uint64_t to,
-                                                   float x, const Quad& Q) {
-    if (to <= from) return 0;
-    const uint64_t g0 = from >> 4, g1 = (to - 1) >> 4;
-    uint32_t c = __popc(group_lt(arr, g0, x, Q) & range_bits(g0, from, to));
-    if (g1 > g0) c += __popc(group_lt(arr, g0 + 1, x, Q) & range_bits(g0 + 1, from, to));
-    if (g1 > g0 + 1) c += __popc(group_lt(arr, g0 + 2, x, Q) & range_bits(g0 + 2, from, to));
-    return c;
-}
-
-constexpr uint32_t kSmallList = 32;  // lists up to this length are scanned directly (<= 3 groups)
-
-// first slot p in [a, b) with ts[p] >= x, else b (R#2).  Index path: one 64-byte group per level.
-__device__ __forceinline__ uint32_t lower_bound_ts(const SampleParams& p, uint32_t a, uint32_t b, float x,
-                                                   const Quad& Q) {
+// ---------------------------------------------------------------------------- cut search
+// first slot in [a, b) with ts >= x, else b (R#2).  Long lists first descend the 16-ary index
+// (tsindex.cuh): per level a binary search over <= 16 consecutive index entries (one 64-byte
+// group: one DRAM request + L1 hits); then a binary search over the remaining <= 15 slots.
+__device__ __forceinline__ uint32_t lower_bound_ts(const SampleParams& p, uint32_t a, uint32_t b, float x) {
     if (a >= b) return a;
-    if (p.n_levels < 0) {  // plain binary search (no aux buffer, or ts not 64-byte aligned)
-        while (a < b) {
-            const uint32_t mid = a + ((b - a) >> 1);
-            if (__ldg(p.ts + mid) < x)
-                a = mid + 1;
-            else
-                b = mid;
-        }
-        return a;
-    }
     uint64_t A = a, B = b;
-    if (B - A > kSmallList) {
+    if (p.n_levels > 0 && B - A > kIndexMin) {
         int l = 1;
         while (l < p.n_levels && ((B + (1ull << (kIndexShift * l)) - 1) >> (kIndexShift * l)) -
                                          ((A + (1ull << (kIndexShift * l)) - 1) >> (kIndexShift * l)) >
@@ -180,12 +108,29 @@ __device__ __forceinline__ uint32_t lower_bound_ts(const SampleParams& p, uint32
             const int sh = kIndexShift * l;
             const uint64_t j0 = (A + (1ull << sh) - 1) >> sh, j1 = (B + (1ull << sh) - 1) >> sh;
             if (j1 <= j0) continue;
-            const uint32_t m = count_lt_small(p.lvl[l], j0, j1, x, Q);  // j1 - j0 <= 16
+            const float* L = p.lvl[l];
+            uint64_t lo = j0, hi = j1;  // first index entry >= x
+            while (lo < hi) {
+                const uint64_t mid = (lo + hi) >> 1;
+                if (__ldg(L + mid) < x)
+                    lo = mid + 1;
+                else
+                    hi = mid;
+            }
+            const uint64_t m = lo - j0;  // entries < x
             if (m > 0) A = ((j0 + m - 1) << sh) + 1;
             if (j0 + m < j1) B = (j0 + m) << sh;
         }
     }
-    return (uint32_t)(A + count_lt_small(p.ts, A, B, x, Q));
+    uint32_t lo = (uint32_t)A, hi = (uint32_t)B;
+    while (lo < hi) {
+        const uint32_t mid = lo + ((hi - lo) >> 1);
+        if (__ldg(p.ts + mid) < x)
+            lo = mid + 1;
+        else
+            hi = mid;
+    }
+    return lo;
 }
 
 __device__ __forceinline__ uint32_t warp_incl_scan(uint32_t x, int lane) {
@@ -198,17 +143,15 @@ __device__ __forceinline__ uint32_t warp_incl_scan(uint32_t x, int lane) {
 }
 
 // ---------------------------------------------------------------------------- K4a windows
-template <int STRATEGY, int G>
-__global__ void __launch_bounds__(G * kTile) window_kernel(const __grid_constant__ SampleParams p) {
-    __shared__ uint32_t s_red[TGL_MAX_SNAPSHOTS][G * kTile / 32];
+template <int STRATEGY>
+__global__ void __launch_bounds__(kTile) window_kernel(const __grid_constant__ SampleParams p) {
+    __shared__ uint32_t s_red[TGL_MAX_SNAPSHOTS][kWarps];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const Quad Q{G == 1 ? (1u << lane) : (((1u << G) - 1u) << (lane & ~(G - 1))), lane & (G - 1), G};
     const int64_t n = chain_roots(p);
-    const int64_t tile_begin = p.root_begin + (int64_t)blockIdx.x * kTile;
-    if (tile_begin >= n) return;  // whole CTA: capacity-sized grid, tiles past the end do nothing
-    const int64_t r = (int64_t)blockIdx.x * kTile + (threadIdx.x / G);  // chunk-relative root
-    const int64_t i = p.root_begin + r;
-    const bool valid = i < n && r < p.chunk_cap;
+    const int64_t base_i = (int64_t)blockIdx.x * kTile;
+    if (base_i >= n) return;  // capacity-sized grid (l >= 1): tiles past the end do nothing
+    const int64_t i = base_i + threadIdx.x;
+    const bool valid = i < n;
     const int nsb = p.nsb;
     const uint32_t k = (uint32_t)p.k;
 
@@ -219,57 +162,36 @@ __global__ void __launch_bounds__(G * kTile) window_kernel(const __grid_constant
         const int64_t vg = (int64_t)p.root_node[i] - p.node_lo;  // shard-local node id
         v = (int32_t)vg;
         t = p.root_ts[i];
-        if (vg < 0 || vg >= (int64_t)p.n_nodes) {
-            if (Q.q == 0) atomicOr(p.err, kErrRange);
-        } else if (!isfinite(t)) {
-            if (Q.q == 0) atomicOr(p.err, kErrInval);
-        } else {
+        if (vg < 0 || vg >= (int64_t)p.n_nodes)
+            atomicOr(p.err, kErrRange);
+        else if (!isfinite(t))
+            atomicOr(p.err, kErrInval);
+        else
             ok = true;
-        }
     }
     float lin = -INFINITY;
     if (p.layer > 0 && p.root_lo && ok) lin = p.root_lo[i];
     uint32_t lo = 0, hi = 0;
     if (ok) {
-        if (G == 1) {
-            lo = (uint32_t)__ldg(p.indptr + v);
-            hi = (uint32_t)__ldg(p.indptr + v + 1);
-        } else {  // indptr[v], indptr[v+1] in one request: lanes 0/1 of the group load the two words
-            const uint32_t w = (uint32_t)__ldg(p.indptr + v + (Q.q & 1));
-            lo = __shfl_sync(Q.mask, w, (lane & ~(G - 1)));
-            hi = __shfl_sync(Q.mask, w, (lane & ~(G - 1)) + 1);
-        }
+        lo = (uint32_t)__ldg(p.indptr + v);
+        hi = (uint32_t)__ldg(p.indptr + v + 1);
     }
-    // U of window 0 is the root's own time t.  Short lists are scanned whole (<= 3 groups; every
-    // later cut then hits L1); a long list that starts at or after t has no candidate in any
-    // window (one request answers every cut).
+    // U of window 0 is the root's own time t; a list starting at or after t has no candidate
     uint32_t bcur = lo;
-    if (ok && (hi - lo <= kSmallList || __ldg(p.ts + lo) < t)) bcur = lower_bound_ts(p, lo, hi, t, Q);
+    if (lo < hi && __ldg(p.ts + lo) < t) bcur = lower_bound_ts(p, lo, hi, t);
     for (int b = 0; b < nsb; ++b) {
         // lower bound of window b: layer 0 -> t (-) ((b+1) (x) t_s); l >= 1 -> inherited
         const float x = p.layer == 0 ? __fsub_rn(t, __fmul_rn((float)(b + 1), p.snapshot_len)) : lin;
         uint32_t a = lo;
         if (x > -INFINITY && bcur > lo)  // empty window when the element before the cut is < x
-            a = __ldg(p.ts + bcur - 1) < x ? bcur : lower_bound_ts(p, lo, bcur - 1, x, Q);
+            a = __ldg(p.ts + bcur - 1) < x ? bcur : lower_bound_ts(p, lo, bcur - 1, x);
         const uint32_t c = bcur - a;
         const uint32_t take = c < k ? c : k;
-        if (valid && Q.q == 0) {
-            const uint32_t first = STRATEGY == TGL_MOST_RECENT ? bcur - take : a;
-            p.win_first[(size_t)b * p.chunk_cap + r] = first;
-            p.win_len[(size_t)b * p.chunk_cap + r] = STRATEGY == TGL_MOST_RECENT ? take : c;
-            if (STRATEGY == TGL_MOST_RECENT && take > 0 && p.prefetch) {
-                // warm L2 for K4b: payload run (<= 8 B x k) and its timestamps
-                if (p.payload) {
-                    prefetch_l2(p.payload + first);
-                    prefetch_l2(p.payload + first + take - 1);
-                } else {
-                    prefetch_l2(p.nbr + first);
-                    prefetch_l2(p.eid + first);
-                }
-                prefetch_l2(p.ts + first);
-            }
+        if (valid) {
+            p.win_first[(size_t)b * p.roots_cap + i] = STRATEGY == TGL_MOST_RECENT ? bcur - take : a;
+            p.win_len[(size_t)b * p.roots_cap + i] = STRATEGY == TGL_MOST_RECENT ? take : c;
         }
-        uint32_t s = Q.q == 0 ? take : 0u;
+        uint32_t s = take;
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(kFull, s, o);
         if (lane == 0) s_red[b][warp] = s;
@@ -278,15 +200,15 @@ __global__ void __launch_bounds__(G * kTile) window_kernel(const __grid_constant
     __syncthreads();
     if (threadIdx.x < nsb) {
         uint32_t s = 0;
-#pragma unroll 8
-        for (int w = 0; w < G * kTile / 32; ++w) s += s_red[threadIdx.x][w];
+#pragma unroll
+        for (int w = 0; w < kWarps; ++w) s += s_red[threadIdx.x][w];
         p.tile_tot[(size_t)threadIdx.x * p.tiles_cap + blockIdx.x] = s;
     }
 }
 
 // ---------------------------------------------------------------------------- K5 tile scan
 // One CTA; thread j owns a contiguous run of ceil(tiles / 1024) tiles: local sums, one block scan
-// per snapshot, local re-scan.  ~2 barriers per snapshot.
+// per snapshot, local re-scan.
 __device__ __forceinline__ uint64_t block_excl_scan_1024(uint64_t v, uint64_t* sm /*[33]*/, uint64_t* total) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     uint64_t x = v;
@@ -318,9 +240,7 @@ __device__ __forceinline__ uint64_t block_excl_scan_1024(uint64_t v, uint64_t* s
 __global__ void __launch_bounds__(1024) tile_scan_kernel(const __grid_constant__ SampleParams p) {
     __shared__ uint64_t sm[33];
     const int64_t n = chain_roots(p);
-    int64_t m = n - p.root_begin;
-    m = m < 0 ? 0 : (m < p.chunk_cap ? m : p.chunk_cap);
-    const int64_t tiles = (m + kTile - 1) / kTile;
+    const int64_t tiles = (n + kTile - 1) / kTile;
     const int64_t per = (tiles + 1023) / 1024;
     const int64_t t0 = (int64_t)threadIdx.x * per;
     for (int b = 0; b < p.nsb; ++b) {
@@ -329,22 +249,16 @@ __global__ void __launch_bounds__(1024) tile_scan_kernel(const __grid_constant__
         uint64_t s = 0;
         for (int64_t t = t0; t < t0 + per && t < tiles; ++t) s += tot[t];
         uint64_t total;
-        uint64_t run = block_excl_scan_1024(s, sm, &total) + (p.first_chunk ? 0ull : p.carry[b]);
-        const uint64_t carry_in = p.first_chunk ? 0ull : p.carry[b];
+        uint64_t run = block_excl_scan_1024(s, sm, &total);
         for (int64_t t = t0; t < t0 + per && t < tiles; ++t) {
             base[t] = run;
             run += tot[t];
         }
-        __syncthreads();  // every thread has read carry[b] before it is updated
         if (threadIdx.x == 0) {
-            const uint64_t carry = carry_in + total;
-            p.carry[b] = carry;
-            if (p.last_chunk) {
-                const BlockOut& o = p.out[b];
-                o.offsets[n] = (int64_t)carry;
-                *o.nnz_dev = (int64_t)carry;
-                *o.n_roots_dev = n;
-            }
+            const BlockOut& o = p.out[b];
+            o.offsets[n] = (int64_t)total;
+            *o.nnz_dev = (int64_t)total;
+            *o.n_roots_dev = n;
         }
     }
 }
@@ -355,16 +269,15 @@ __host__ __device__ inline int copy_warp_words(int nsb, int k, bool picks_in_sme
 }
 
 template <int STRATEGY>
-__global__ void __launch_bounds__(kCopyThreads) copy_kernel(const __grid_constant__ SampleParams p) {
+__global__ void __launch_bounds__(kTile) copy_kernel(const __grid_constant__ SampleParams p) {
     extern __shared__ __align__(16) uint32_t smem[];
-    __shared__ uint32_t s_wsum[TGL_MAX_SNAPSHOTS][kCopyWarps];
+    __shared__ uint32_t s_wsum[TGL_MAX_SNAPSHOTS][kWarps];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int64_t n = chain_roots(p);
-    const int64_t tile_begin = p.root_begin + (int64_t)blockIdx.x * kTile;
-    if (tile_begin >= n) return;
-    const int64_t r = (int64_t)blockIdx.x * kTile + threadIdx.x;  // chunk-relative root
-    const int64_t i = p.root_begin + r;
-    const bool valid = i < n && r < p.chunk_cap;
+    const int64_t base_i = (int64_t)blockIdx.x * kTile;
+    if (base_i >= n) return;
+    const int64_t i = base_i + threadIdx.x;
+    const bool valid = i < n;
     const int nsb = p.nsb;
     const int k = p.k;
     const bool picks_smem = STRATEGY == TGL_UNIFORM && p.picks_global == nullptr;
@@ -377,7 +290,7 @@ __global__ void __launch_bounds__(kCopyThreads) copy_kernel(const __grid_constan
     uint32_t* picks = nullptr;
     if (STRATEGY == TGL_UNIFORM)
         picks = picks_smem ? reinterpret_cast<uint32_t*>(base + nsb)
-                           : p.picks_global + ((size_t)blockIdx.x * kCopyWarps + warp) * nsb * k * 32;
+                           : p.picks_global + ((size_t)blockIdx.x * kWarps + warp) * nsb * k * 32;
 
     const float t = valid ? p.root_ts[i] : 0.0f;
     troot[lane] = t;
@@ -390,8 +303,8 @@ __global__ void __launch_bounds__(kCopyThreads) copy_kernel(const __grid_constan
     for (int b = 0; b < nsb; ++b) {
         uint32_t f = 0, len = 0;
         if (valid) {
-            f = p.win_first[(size_t)b * p.chunk_cap + r];
-            len = p.win_len[(size_t)b * p.chunk_cap + r];
+            f = p.win_first[(size_t)b * p.roots_cap + i];
+            len = p.win_len[(size_t)b * p.roots_cap + i];
         }
         const uint32_t take = STRATEGY == TGL_MOST_RECENT ? len : (len < (uint32_t)k ? len : (uint32_t)k);
         first[b * 32 + lane] = f;
@@ -463,25 +376,27 @@ __global__ void __launch_bounds__(kCopyThreads) copy_kernel(const __grid_constan
                 else
                     pos[u] = act[u] ? fb[ro] + picks[((size_t)b * k + q) * 32 + ro] : 0u;
             }
-            int2 ne[kCopyUnroll];
-            float tv[kCopyUnroll];
+            int4 rec[kCopyUnroll];
 #pragma unroll
             for (int u = 0; u < kCopyUnroll; ++u) {
                 if (act[u]) {
-                    ne[u] = p.payload ? __ldg(p.payload + pos[u])
-                                      : make_int2(__ldg(p.nbr + pos[u]), __ldg(p.eid + pos[u]));
-                    tv[u] = __ldg(p.ts + pos[u]);
+                    if (p.recs)
+                        rec[u] = __ldg(p.recs + pos[u]);
+                    else
+                        rec[u] = make_int4(__float_as_int(__ldg(p.ts + pos[u])), __ldg(p.nbr + pos[u]),
+                                           __ldg(p.eid + pos[u]), 0);
                 }
             }
 #pragma unroll
             for (int u = 0; u < kCopyUnroll; ++u) {
                 if (!act[u]) continue;
                 const uint64_t oi = B + o0 + (uint32_t)(u * 32 + lane);
+                const float tv = __int_as_float(rec[u].x);
                 const float tr = troot[rr[u]];
-                o.nbr[oi] = ne[u].x;
-                o.eid[oi] = ne[u].y;
-                o.dt[oi] = __fsub_rn(tr, tv[u]);
-                if (o.ts_edge) o.ts_edge[oi] = tv[u];
+                o.nbr[oi] = rec[u].y;
+                o.eid[oi] = rec[u].z;
+                o.dt[oi] = __fsub_rn(tr, tv);
+                if (o.ts_edge) o.ts_edge[oi] = tv;
                 if (o.child_key) o.child_key[oi] = rkey[rr[u]] * (uint64_t)k + qq[u];
                 if (o.child_lo)  // children inherit the window's lower bound (R#3)
                     o.child_lo[oi] = p.layer == 0 ? __fsub_rn(tr, __fmul_rn((float)(b + 1), p.snapshot_len))
@@ -493,18 +408,11 @@ __global__ void __launch_bounds__(kCopyThreads) copy_kernel(const __grid_constan
 
 static bool picks_fit_smem(int nsb, int k) { return (size_t)nsb * k * 32 * 4 <= kPicksSmemPerWarp; }
 
-// Tuning knobs (environment, read per call; defaults are the measured best on B200).
-static int64_t chunk_roots() {
-    const char* e = getenv("TGL_CHUNK_ROOTS");
-    const int64_t c = e ? atoll(e) : kDefaultChunk;
-    return std::max<int64_t>(kTile, (c + kTile - 1) / kTile * kTile);
-}
-
 struct Launch {
     int layer, chain, nsb;
-    int64_t chunk_cap, tiles_cap, n_chunks;
+    int64_t roots_cap, tiles_cap;
     uint32_t *win_first, *win_len, *tile_tot;
-    uint64_t *tile_base, *carry;
+    uint64_t* tile_base;
     uint32_t* picks;  // global picks or null
 };
 
@@ -542,16 +450,12 @@ static int plan_sample(int64_t n_roots, int L, const int32_t* fanouts, int S, in
         la.layer = layer;
         la.chain = chain;
         la.nsb = nsb;
-        const int64_t cap = std::max<int64_t>(1, P.roots_cap[layer]);
-        // layer 0 (host count known) is processed in L2-sized chunks; l >= 1 in one capacity pass
-        la.chunk_cap = layer == 0 ? std::min<int64_t>(cap, chunk_roots()) : cap;
-        la.n_chunks = layer == 0 ? std::max<int64_t>(1, (P.roots_cap[0] + la.chunk_cap - 1) / la.chunk_cap) : 1;
-        la.tiles_cap = (la.chunk_cap + kTile - 1) / kTile;
-        la.win_first = c.take<uint32_t>((size_t)nsb * la.chunk_cap);
-        la.win_len = c.take<uint32_t>((size_t)nsb * la.chunk_cap);
+        la.roots_cap = std::max<int64_t>(1, P.roots_cap[layer]);
+        la.tiles_cap = (la.roots_cap + kTile - 1) / kTile;
+        la.win_first = c.take<uint32_t>((size_t)nsb * la.roots_cap);
+        la.win_len = c.take<uint32_t>((size_t)nsb * la.roots_cap);
         la.tile_tot = c.take<uint32_t>((size_t)nsb * la.tiles_cap);
         la.tile_base = c.take<uint64_t>((size_t)nsb * la.tiles_cap);
-        la.carry = c.take<uint64_t>((size_t)nsb);
         la.picks = nullptr;
         if (strategy == TGL_UNIFORM && !picks_fit_smem(nsb, fanouts[layer]))
             la.picks = c.take<uint32_t>((size_t)la.tiles_cap * kTile * nsb * fanouts[layer]);
@@ -569,28 +473,13 @@ static int plan_sample(int64_t n_roots, int L, const int32_t* fanouts, int S, in
     return TGL_OK;
 }
 
-static int lanes_per_root() {
-    const char* e = getenv("TGL_LANES_PER_ROOT");
-    const int g = e ? atoi(e) : 1;
-    return (g == 2 || g == 4) ? g : 1;
-}
-
-static bool prefetch_enabled() {
-    const char* e = getenv("TGL_PREFETCH");
-    return e ? atoi(e) != 0 : false;
-}
-
 template <int STRATEGY>
-static int launch_chunk(const SampleParams& sp, int64_t grid, size_t smem, cudaStream_t st) {
-    switch (lanes_per_root()) {
-        case 4: window_kernel<STRATEGY, 4><<<(unsigned)grid, 4 * kTile, 0, st>>>(sp); break;
-        case 2: window_kernel<STRATEGY, 2><<<(unsigned)grid, 2 * kTile, 0, st>>>(sp); break;
-        default: window_kernel<STRATEGY, 1><<<(unsigned)grid, kTile, 0, st>>>(sp); break;
-    }
+static int launch_chain(const SampleParams& sp, int64_t grid, size_t smem, cudaStream_t st) {
+    window_kernel<STRATEGY><<<(unsigned)grid, kTile, 0, st>>>(sp);
     tile_scan_kernel<<<1, 1024, 0, st>>>(sp);
     if (smem > 48 * 1024)
         cudaFuncSetAttribute(copy_kernel<STRATEGY>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    copy_kernel<STRATEGY><<<(unsigned)grid, kCopyThreads, smem, st>>>(sp);
+    copy_kernel<STRATEGY><<<(unsigned)grid, kTile, smem, st>>>(sp);
     return cudaGetLastError() == cudaSuccess ? TGL_OK : TGL_ECUDA;
 }
 
@@ -633,7 +522,9 @@ static int sample_impl(const tgl_tcsr* g, const int32_t* roots, const float* roo
             if (b.cap_roots < P.roots_cap[l] || b.cap_edges < P.edges_cap[l]) return TGL_ECAPACITY;
         }
     cudaStream_t st = (cudaStream_t)stream;
-    const bool indexed = g->index && g->n_levels > 0 && ((uintptr_t)g->ts & 63) == 0 && !getenv("TGL_NO_INDEX");
+    // experiment knobs (tools/sweep.py): TGL_NO_INDEX, TGL_NO_RECS
+    const bool use_recs = g->recs && !getenv("TGL_NO_RECS");
+    const bool use_index = g->index && g->n_levels > 0 && !getenv("TGL_NO_INDEX");
     for (int j = 0; j < P.n_launch; ++j) {
         const Launch& la = P.launches[j];
         const int l = la.layer, s = la.chain;
@@ -643,12 +534,9 @@ static int sample_impl(const tgl_tcsr* g, const int32_t* roots, const float* roo
         sp.nbr = g->nbr;
         sp.ts = g->ts;
         sp.eid = g->eid;
-        sp.payload = getenv("TGL_NO_PAYLOAD") ? nullptr : g->payload;
-        sp.prefetch = prefetch_enabled();
-        sp.lvl[0] = g->ts;
-        sp.n_levels = indexed ? g->n_levels : -1;
-        if (indexed)
-            for (int q = 1; q <= g->n_levels; ++q) sp.lvl[q] = g->index + g->level_off[q];
+        sp.recs = use_recs ? static_cast<const int4*>(g->recs) : nullptr;
+        sp.n_levels = use_index ? g->n_levels : 0;
+        for (int q = 1; q <= sp.n_levels; ++q) sp.lvl[q] = g->index + g->level_off[q];
         sp.n_nodes = g->n_nodes;
         sp.node_lo = g->node_lo;
         if (l == 0) {
@@ -677,8 +565,7 @@ static int sample_impl(const tgl_tcsr* g, const int32_t* roots, const float* roo
         sp.win_len = la.win_len;
         sp.tile_tot = la.tile_tot;
         sp.tile_base = la.tile_base;
-        sp.carry = la.carry;
-        sp.chunk_cap = la.chunk_cap;
+        sp.roots_cap = la.roots_cap;
         sp.tiles_cap = la.tiles_cap;
         sp.picks_global = la.picks;
         sp.err = g->err_dev;
@@ -696,22 +583,12 @@ static int sample_impl(const tgl_tcsr* g, const int32_t* roots, const float* roo
             bo.n_roots_dev = ob.n_roots_dev;
             bo.nnz_dev = ob.nnz_dev;
         }
-        const bool in_smem = la.picks == nullptr;
+        const int64_t grid = l == 0 ? std::max<int64_t>(1, (n_roots + kTile - 1) / kTile) : la.tiles_cap;
         const size_t smem =
-            (size_t)kCopyWarps * copy_warp_words(la.nsb, sp.k, strategy == TGL_UNIFORM && in_smem) * 4;
-        for (int64_t c = 0; c < la.n_chunks; ++c) {
-            sp.root_begin = c * la.chunk_cap;
-            sp.first_chunk = c == 0;
-            sp.last_chunk = c == la.n_chunks - 1;
-            int64_t grid = la.tiles_cap;
-            if (l == 0) {  // exact grid for the known host count
-                const int64_t m = std::min<int64_t>(la.chunk_cap, std::max<int64_t>(0, n_roots - sp.root_begin));
-                grid = std::max<int64_t>(1, (m + kTile - 1) / kTile);
-            }
-            rc = strategy == TGL_UNIFORM ? launch_chunk<TGL_UNIFORM>(sp, grid, smem, st)
-                                         : launch_chunk<TGL_MOST_RECENT>(sp, grid, smem, st);
-            if (rc) return rc;
-        }
+            (size_t)kWarps * copy_warp_words(la.nsb, sp.k, strategy == TGL_UNIFORM && la.picks == nullptr) * 4;
+        rc = strategy == TGL_UNIFORM ? launch_chain<TGL_UNIFORM>(sp, grid, smem, st)
+                                     : launch_chain<TGL_MOST_RECENT>(sp, grid, smem, st);
+        if (rc) return rc;
     }
     return TGL_OK;
 }

@@ -46,20 +46,29 @@ inline IndexLayout index_layout(uint64_t n_stored) {
     return L;
 }
 
-// The sampler's auxiliary ("aux") buffer: [ts atom index | (nbr, eid) pairs].  The interleaved
-// payload puts both fields of a slot in one 8-byte word, so copying a run of c sampled slots is
-// one contiguous access (one DRAM row activation) instead of two.
+// The sampler's auxiliary ("aux") buffer: [ts atom index | slot records].  A slot record is the
+// 16-byte {ts, nbr, eid, 0} of one T-CSR slot, so the cut search and the payload copy of the
+// selected slots read the SAME lines: one DRAM row activation per list instead of one per array
+// (HBM serves ~33 G random requests/s).
+struct SlotRec {
+    float ts;
+    int32_t nbr;
+    int32_t eid;
+    int32_t pad;
+};
+static_assert(sizeof(SlotRec) == 16, "slot record is one 16-byte vector");
+
 struct AuxLayout {
     IndexLayout index;
-    uint64_t payload_off = 0;  // byte offset of the int2 payload array
+    uint64_t rec_off = 0;  // byte offset of the SlotRec array
     uint64_t bytes = 0;
 };
 
 inline AuxLayout aux_layout(uint64_t n_stored) {
     AuxLayout A;
     A.index = index_layout(n_stored);
-    A.payload_off = align_up(A.index.floats * sizeof(float), 256);
-    A.bytes = align_up(A.payload_off + n_stored * 8, 256);
+    A.rec_off = align_up(A.index.floats * sizeof(float), 256);
+    A.bytes = align_up(A.rec_off + n_stored * sizeof(SlotRec), 256);
     if (A.bytes < 256) A.bytes = 256;
     return A;
 }

@@ -35,7 +35,7 @@ torch.cuda.empty_cache()
 
 
 def run(handle, env):
-    for k in ("TGL_CHUNK_ROOTS", "TGL_LANES_PER_ROOT", "TGL_PREFETCH", "TGL_NO_PAYLOAD", "TGL_NO_INDEX"):
+    for k in ("TGL_NO_RECS", "TGL_NO_INDEX"):
         os.environ.pop(k, None)
     os.environ.update({k: str(v) for k, v in env.items()})
     smp = tgl.Sampler(handle, args.roots, cfg.fanouts, cfg.strategy, cfg.n_snapshots, cfg.snapshot_len)
@@ -57,14 +57,14 @@ def run(handle, env):
 
 
 settings = []
-for lanes, idx, pf, pay in itertools.product([1, 2, 4], [1, 0], [0, 1], [0, 1]):
-    env = dict(TGL_LANES_PER_ROOT=lanes, TGL_CHUNK_ROOTS=args.roots, TGL_PREFETCH=pf)
-    if not pay:
-        env["TGL_NO_PAYLOAD"] = 1
+for recs, idx in itertools.product([1, 0], [1, 0]):
+    env = {}
+    if not recs:
+        env["TGL_NO_RECS"] = 1
     if not idx:
         env["TGL_NO_INDEX"] = 1
     settings.append(("aux", env))
-settings.append(("plain", dict(TGL_LANES_PER_ROOT=1, TGL_CHUNK_ROOTS=args.roots, TGL_PREFETCH=0)))
+settings.append(("plain", {}))
 if args.only:
     env = dict(kv.split("=") for kv in args.only.split(","))
     settings = [("plain" if env.pop("handle", "aux") == "plain" else "aux", env)]
