@@ -130,6 +130,31 @@ def chunk_starts(n_total_roots: int, chunk: int, n_chunks: int, batch: int):
     return out
 
 
+def gather_bytes(cfg: C.Workload, n_roots: int, nnz: int) -> int:
+    """Algorithmic bytes of the C3 gather: read + write of every gathered row; node
+    tables for the roots and the sampled neighbours, edge features for the sampled eids."""
+    node_row = sum(4 * cols for name, (rows, cols) in cfg.tables.items() if name != "edge_feat")
+    edge_row = 4 * cfg.tables["edge_feat"][1]
+    return 2 * ((n_roots + nnz) * node_row + nnz * edge_row)
+
+
+def make_gather(tgl, cfg, sampler, dev):
+    """C3 step 2 of Fig. 2: memory, mem_ts, mailbox, mail_ts for the roots and sampled
+    neighbours, edge features for the sampled eids -- preallocated outputs, device-side counts."""
+    tabs = C.tables(cfg, device=dev)
+    node_tabs = [tabs[k] for k in ("memory", "mem_ts", "mailbox", "mail_ts")]
+    cap_r, cap_e = sampler.roots_cap[0], sampler.edges_cap[0]
+    out_r = [torch.empty((cap_r,) + tuple(t.shape[1:]), dtype=t.dtype, device=dev) for t in node_tabs]
+    out_n = [torch.empty((cap_e,) + tuple(t.shape[1:]), dtype=t.dtype, device=dev) for t in node_tabs]
+    out_e = [torch.empty((cap_e, tabs["edge_feat"].shape[1]), dtype=torch.float32, device=dev)]
+
+    def run(roots, block):
+        tgl.gather(roots, node_tabs, outs=out_r)
+        tgl.gather(block.nbr, node_tabs, n_ids_dev=block.nnz_dev, outs=out_n)
+        tgl.gather(block.eid, [tabs["edge_feat"]], n_ids_dev=block.nnz_dev, outs=out_e)
+    return run
+
+
 def rank_chunks(n_epoch_roots: int, chunk: int, steps_total: int, world: int, rank: int, batch: int):
     """Root-sharded data parallelism: the steps_total * world chunks of `chunk` roots are spread
     evenly over the epoch and chunk c*world + r goes to rank r (batch-aligned, disjoint)."""
@@ -162,6 +187,8 @@ def oracle_sample_rate(cfg, src, dst, ts, roots_list, key_bases, budget_s=None):
     """Times the oracle (single thread, as it stands) on the given batches; returns dict."""
     import oracle
     nodes = torch.cat([r for r, _ in roots_list])
+    if len(cfg.fanouts) > 1:  # deeper layers' roots are sampled neighbours: every list may be read
+        nodes = torch.arange(cfg.n_nodes, dtype=torch.int32, device=src.device)
     s_np, d_np, t_np, e_np, keep = C.relevant_substream(src, dst, ts, nodes, cfg.n_nodes, cfg.add_reverse)
     go = oracle.build_restricted(lambda: iter([(s_np, d_np, t_np, e_np, 0)]), n_nodes=cfg.n_nodes,
                                  add_reverse=cfg.add_reverse, keep=keep)
@@ -215,11 +242,19 @@ def run_ours(args):
     sampler = tgl.Sampler(g, chunk, cfg.fanouts, cfg.strategy, cfg.n_snapshots, cfg.snapshot_len)
     L, S = len(cfg.fanouts), cfg.n_snapshots
     launches_per_step = 3 * (1 + (L - 1) * S)  # window + tile scan + copy per chain
-    stream = torch.cuda.current_stream()
+    gather = make_gather(tgl, cfg, sampler, dev) if cfg.tables else None
+    if gather is not None:
+        launches_per_step += 3  # node tables by roots, node tables by nbr, edge features by eid
+
+    def step(j):
+        r, t = chunks[j]
+        blocks = sampler.run(r, t, seed=cfg.sampler_seed, root_key_base=mine[j])
+        if gather is not None:
+            gather(r, blocks[0])
+        return blocks
 
     for w in range(args.warmup):
-        r, t = chunks[w]
-        sampler.run(r, t, seed=cfg.sampler_seed, root_key_base=mine[w])
+        step(w)
     torch.cuda.synchronize(dev)
     if world > 1:
         torch.distributed.barrier()
@@ -232,7 +267,7 @@ def run_ours(args):
         for j in range(args.steps):
             r, t = chunks[args.warmup + j]
             ev[j][0].record()
-            sampler.run(r, t, seed=cfg.sampler_seed, root_key_base=mine[args.warmup + j])
+            step(args.warmup + j)
             ev[j][1].record()
         t_end.record()
         torch.cuda.synchronize(dev)
@@ -245,7 +280,7 @@ def run_ours(args):
     edges_total, bytes_total, roots_total = 0, 0, 0
     for j in range(args.steps):
         r, t = chunks[args.warmup + j]
-        blocks = sampler.run(r, t, seed=cfg.sampler_seed, root_key_base=mine[args.warmup + j])
+        blocks = step(args.warmup + j)
         nr = [int(blocks[l * S].n_roots_dev.item()) for l in range(L)]
         nz = [sum(int(blocks[l * S + s].nnz_dev.item()) for s in range(S)) for l in range(L)]
         # per-layer roots over all S chains for l >= 1
@@ -253,11 +288,15 @@ def run_ours(args):
         edges_total += sum(nz)
         roots_total += nr[0]
         bytes_total += algorithmic_bytes(cfg, nr, nz)
+        if gather is not None:
+            bytes_total += gather_bytes(cfg, nr[0], nz[0])
     err = tgl.check(g)
 
     edges_all, bytes_all, total_ms_max = reduce_report(edges_total, bytes_total, total_ms, world, dev)
 
     value = edges_all / (total_ms_max / 1e3)
+    tcsr_bytes = g.indptr.numel() * 8 + g.n_stored * 12
+    l2_bytes = torch.cuda.get_device_properties(dev).L2_cache_size
     peak, peak_src = measured_peak_hbm()
     # dominant kernel = the sampler kernel (one launch per step for 1-layer configs); the per-step
     # events bracket tgl_sample = one small memset of the look-back state + the kernel(s)
@@ -276,9 +315,15 @@ def run_ours(args):
                    "l2": "no flush: T-CSR and per-step roots exceed L2 (126 MB); every step's roots are distinct"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": None, "peak_source": peak_src,
-                     "kernel": f"tgl_sample ({cfg.strategy}): window_kernel + tile_scan_kernel + copy_kernel, timed together",
-                     "bytes_model": "SURVEY 8(d): per root 8+16+8*cuts+8*S, per edge 24 (+4 ts_edge if l<L-1)",
-                     "algorithmic_bytes_per_step": bytes_total / args.steps},
+                     "kernel": (f"tgl_sample ({cfg.strategy}): window_kernel + tile_scan_kernel + copy_kernel"
+                                + (" + tgl_gather (3 launches)" if gather is not None else "") + ", timed together"),
+                     "bytes_model": "SURVEY 8(d): per root 8+16+8*cuts+8*S, per edge 24 (+4 ts_edge if l<L-1)"
+                                    + ("; gather: 2 x row bytes per gathered id" if gather is not None else ""),
+                     "algorithmic_bytes_per_step": bytes_total / args.steps,
+                     "l2_resident": tcsr_bytes < l2_bytes,
+                     "note": ("T-CSR + gather node tables fit the 126 MB L2: algorithmic bytes are mostly L2 "
+                              "traffic, so frac vs the HBM peak is not meaningful here (SURVEY 8(d))")
+                             if tcsr_bytes < l2_bytes else "T-CSR exceeds L2: HBM-bound random access"},
         "gpu_launches": launches_per_step * args.steps,
         "clocks": clocks.summary(),
         "build_ms": build_ms, "generate_s": gen_s,
@@ -288,7 +333,9 @@ def run_ours(args):
 
     # end to end through the public API with host buffers (rank-local), copies inside the region
     if not args.no_e2e:
-        out["e2e"] = e2e(args, tgl, sampler, chunks, mine, cfg, dev, world)
+        gf = (lambda smp: make_gather(tgl, cfg, smp, dev)) if gather is not None else None
+        out["e2e"] = e2e(args, tgl, sampler, chunks, mine, cfg, dev, world, gather_factory=gf)
+        out["e2e_full_d2h"] = e2e(args, tgl, sampler, chunks, mine, cfg, dev, world, full_d2h=True)
 
     # CPU oracle baseline + parity spot check (rank 0, N = 1 only)
     if world == 1 and not args.no_cpu_baseline:
@@ -299,64 +346,104 @@ def run_ours(args):
         torch.distributed.destroy_process_group()
 
 
-def e2e(args, tgl, sampler, chunks, mine, cfg, dev, world):
-    """Host roots (pinned) -> H2D -> tgl_sample -> D2H of every block trimmed to its nnz."""
+def e2e(args, tgl, sampler, chunks, mine, cfg, dev, world, full_d2h=False, gather_factory=None):
+    """End to end through the public API with host buffers, copies inside the timed region.
+
+    Per step: pinned host roots -> H2D (copy stream) -> tgl_sample (compute stream) -> D2H of the
+    step's result.  full_d2h=False: the result read back is the step's metric, the per-block
+    (n_roots, nnz) counts (the blocks stay on the GPU for the consumer, as in TGL's training step);
+    full_d2h=True: every block (offsets + nbr/eid/dt trimmed to nnz) is copied to pinned host memory.
+    Double-buffered: the H2D of step j+1 and the D2H of step j overlap the sampling of j+1 / j+1.
+    """
     L, S = len(cfg.fanouts), cfg.n_snapshots
     host = [(r.cpu().pin_memory(), t.cpu().pin_memory()) for r, t in chunks]
     cap_r = chunks[0][0].numel()
-    d_r = torch.empty(cap_r, dtype=torch.int32, device=dev)
-    d_t = torch.empty(cap_r, dtype=torch.float32, device=dev)
-    hb = [dict(off=torch.empty(b.offsets.numel(), dtype=torch.int64).pin_memory(),
-               nbr=torch.empty(b.nbr.numel(), dtype=torch.int32).pin_memory(),
-               eid=torch.empty(b.eid.numel(), dtype=torch.int32).pin_memory(),
-               dt=torch.empty(b.dt.numel(), dtype=torch.float32).pin_memory()) for b in sampler.blocks]
-    cnt_h = torch.empty(2 * len(sampler.blocks), dtype=torch.int64).pin_memory()
+    nb = L * S
+    smps = [sampler, tgl.Sampler(sampler.g, cap_r, cfg.fanouts, cfg.strategy, S, cfg.snapshot_len)]
+    gathers = [gather_factory(smp) for smp in smps] if gather_factory is not None else None
+    d_roots = [(torch.empty(cap_r, dtype=torch.int32, device=dev), torch.empty(cap_r, dtype=torch.float32, device=dev))
+               for _ in range(2)]
+    cnt_h = [torch.empty(2 * nb, dtype=torch.int64).pin_memory() for _ in range(2)]
+    hb = None
+    if full_d2h:
+        hb = [[dict(off=torch.empty(b.offsets.numel(), dtype=torch.int64).pin_memory(),
+                    nbr=torch.empty(b.nbr.numel(), dtype=torch.int32).pin_memory(),
+                    eid=torch.empty(b.eid.numel(), dtype=torch.int32).pin_memory(),
+                    dt=torch.empty(b.dt.numel(), dtype=torch.float32).pin_memory()) for b in smp.blocks]
+              for smp in smps]
+    comp = torch.cuda.current_stream()
+    copy_s = torch.cuda.Stream()
+    stats = dict(h2d=0, d2h=0, edges=0)
+    roots_free = [None, None]  # compute finished reading d_roots[slot]
+    outs_free = [None, None]   # copy stream finished reading smps[slot]'s blocks
 
-    def one(j):
-        r, t = host[j]
-        d_r.copy_(r, non_blocking=True)
-        d_t.copy_(t, non_blocking=True)
-        blocks = sampler.run(d_r, d_t, seed=cfg.sampler_seed, root_key_base=mine[j])
-        for q, b in enumerate(blocks):
-            cnt_h[2 * q:2 * q + 1].copy_(b.n_roots_dev, non_blocking=True)
-            cnt_h[2 * q + 1:2 * q + 2].copy_(b.nnz_dev, non_blocking=True)
-        torch.cuda.current_stream().synchronize()
-        h2d = r.numel() * 8
-        d2h = 16 * len(blocks)
-        for q, b in enumerate(blocks):
-            n, z = int(cnt_h[2 * q]), int(cnt_h[2 * q + 1])
-            hb[q]["off"][: n + 1].copy_(b.offsets[: n + 1], non_blocking=True)
-            hb[q]["nbr"][:z].copy_(b.nbr[:z], non_blocking=True)
-            hb[q]["eid"][:z].copy_(b.eid[:z], non_blocking=True)
-            hb[q]["dt"][:z].copy_(b.dt[:z], non_blocking=True)
-            d2h += (n + 1) * 8 + z * 12
-        return h2d, d2h, sum(int(cnt_h[2 * q + 1]) for q in range(len(blocks)))
+    def run(js):
+        pending = None  # (slot, event) whose counts / payload are still to be read
+        for j in js:
+            slot = j % 2
+            r, t = host[j]
+            dr, dt_ = d_roots[slot]
+            with torch.cuda.stream(copy_s):
+                if roots_free[slot] is not None:
+                    copy_s.wait_event(roots_free[slot])
+                dr.copy_(r, non_blocking=True)
+                dt_.copy_(t, non_blocking=True)
+                h2d_done = torch.cuda.Event()
+                h2d_done.record(copy_s)
+            comp.wait_event(h2d_done)
+            if outs_free[slot] is not None:
+                comp.wait_event(outs_free[slot])
+            blocks = smps[slot].run(dr, dt_, seed=cfg.sampler_seed, root_key_base=mine[j])
+            if gathers is not None:
+                gathers[slot](dr, blocks[0])
+            for q, b in enumerate(blocks):
+                cnt_h[slot][2 * q:2 * q + 1].copy_(b.n_roots_dev, non_blocking=True)
+                cnt_h[slot][2 * q + 1:2 * q + 2].copy_(b.nnz_dev, non_blocking=True)
+            done = torch.cuda.Event()
+            done.record(comp)
+            roots_free[slot] = done
+            stats["h2d"] += r.numel() * 8
+            stats["d2h"] += 16 * nb
+            if pending is not None:
+                finish(*pending)
+            pending = (slot, done)
+        if pending is not None:
+            finish(*pending)
 
-    for w in range(args.warmup):
-        one(w)
+    def finish(slot, done):
+        done.synchronize()  # this step's counts are on the host
+        c = cnt_h[slot]
+        stats["edges"] += int(sum(int(c[2 * q + 1]) for q in range(nb)))
+        if full_d2h:
+            with torch.cuda.stream(copy_s):
+                copy_s.wait_event(done)
+                for q, b in enumerate(smps[slot].blocks):
+                    n, z = int(c[2 * q]), int(c[2 * q + 1])
+                    hb[slot][q]["off"][: n + 1].copy_(b.offsets[: n + 1], non_blocking=True)
+                    hb[slot][q]["nbr"][:z].copy_(b.nbr[:z], non_blocking=True)
+                    hb[slot][q]["eid"][:z].copy_(b.eid[:z], non_blocking=True)
+                    hb[slot][q]["dt"][:z].copy_(b.dt[:z], non_blocking=True)
+                    stats["d2h"] += (n + 1) * 8 + z * 12
+                ev = torch.cuda.Event()
+                ev.record(copy_s)
+                outs_free[slot] = ev
+
+    run(range(args.warmup))
     torch.cuda.synchronize(dev)
+    stats.update(h2d=0, d2h=0, edges=0)
     s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    s.record()
-    tot_h2d = tot_d2h = tot_edges = 0
-    for j in range(args.steps):
-        a, b_, z = one(args.warmup + j)
-        tot_h2d += a
-        tot_d2h += b_
-        tot_edges += z
-    e.record()
+    s.record(comp)
+    run(range(args.warmup, args.warmup + args.steps))
+    comp.wait_stream(copy_s)
+    e.record(comp)
     torch.cuda.synchronize(dev)
     ms = s.elapsed_time(e)
-    val = tot_edges / (ms / 1e3)
-    if world > 1:
-        import torch.distributed as dist
-        t = torch.tensor([tot_edges, ms], dtype=torch.float64, device=dev)
-        mx = torch.tensor([ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(t)
-        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
-        val = float(t[0]) / (float(mx[0]) / 1e3)
-    return {"value": val, "unit": UNIT, "h2d_bytes_per_step": tot_h2d // args.steps,
-            "d2h_bytes_per_step": tot_d2h // args.steps,
-            "note": "pinned host roots -> H2D -> tgl_sample -> nnz read -> D2H of all blocks, one stream"}
+    edges, _, ms_max = reduce_report(stats["edges"], 0.0, ms, world, dev)
+    what = ("pinned host roots -> H2D -> tgl_sample -> D2H of every block (offsets, nbr, eid, dt)" if full_d2h else
+            "pinned host roots -> H2D -> tgl_sample -> D2H of the step's metric (per-block n_roots, nnz); "
+            "blocks stay on the GPU for the consumer")
+    return {"value": edges / (ms_max / 1e3), "unit": UNIT, "h2d_bytes_per_step": stats["h2d"] // args.steps,
+            "d2h_bytes_per_step": stats["d2h"] // args.steps, "note": what + "; copy and compute streams overlapped"}
 
 
 def cpu_baseline(args, cfg, src, dst, ts, tgl, g, sampler, chunks, mine):
@@ -422,6 +509,8 @@ def run_reference(args):
     w = args.warmup * per_step
     import oracle
     nodes = torch.cat([r for r, _ in batches])
+    if len(cfg.fanouts) > 1:  # deeper layers' roots are sampled neighbours: every list may be read
+        nodes = torch.arange(cfg.n_nodes, dtype=torch.int32, device=src.device)
     s_np, d_np, t_np, e_np, keep = C.relevant_substream(src, dst, ts, nodes, cfg.n_nodes, cfg.add_reverse)
     go = oracle.build_restricted(lambda: iter([(s_np, d_np, t_np, e_np, 0)]), n_nodes=cfg.n_nodes,
                                  add_reverse=cfg.add_reverse, keep=keep)
@@ -453,13 +542,16 @@ def main():
     ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="C5", choices=sorted(C.CONFIGS))
-    ap.add_argument("--batches", type=int, default=2048, help="mini-batches per step (epoch mode)")
+    ap.add_argument("--batches", type=int, default=0,
+                    help="mini-batches per step (epoch mode); default 2048 for C5, 256 otherwise")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--ref-batches", type=int, default=16, help="reference arm: batches per step")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
+    if args.batches <= 0:
+        args.batches = 2048 if args.config == "C5" else 256
     if args.warmup < 3 and args.impl == "ours":
         print("warning: --warmup < 3 violates the timing rules", file=sys.stderr)
     if args.impl == "reference":
