@@ -133,6 +133,43 @@ __device__ __forceinline__ uint32_t lower_bound_ts(const SampleParams& p, uint32
     return lo;
 }
 
+// Up to 4 cuts searched together over [lo, hi): interleaved binary searches, one independent probe
+// per live cut per step, so a root costs max(log2 d) dependent steps instead of the sum over cuts.
+__device__ __forceinline__ void lower_bound_multi(const SampleParams& p, uint32_t lo, uint32_t hi, int nc,
+                                                  const float (&x)[4], uint32_t (&out)[4]) {
+    uint32_t a[4], b[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        a[j] = lo;
+        b[j] = (j < nc && x[j] > -INFINITY) ? hi : lo;  // -inf cut: every slot is >= x
+    }
+    while (true) {
+        bool live = false;
+        float v[4];
+        uint32_t mid[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            mid[j] = a[j] + ((b[j] - a[j]) >> 1);
+            if (a[j] < b[j]) {
+                v[j] = __ldg(p.ts + mid[j]);
+                live = true;
+            }
+        }
+        if (!live) break;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            if (a[j] < b[j]) {
+                if (v[j] < x[j])
+                    a[j] = mid[j] + 1;
+                else
+                    b[j] = mid[j];
+            }
+        }
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) out[j] = a[j];
+}
+
 __device__ __forceinline__ uint32_t warp_incl_scan(uint32_t x, int lane) {
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -177,25 +214,48 @@ __global__ void __launch_bounds__(kTile) window_kernel(const __grid_constant__ S
         hi = (uint32_t)__ldg(p.indptr + v + 1);
     }
     // U of window 0 is the root's own time t; a list starting at or after t has no candidate
-    uint32_t bcur = lo;
-    if (lo < hi && __ldg(p.ts + lo) < t) bcur = lower_bound_ts(p, lo, hi, t);
-    for (int b = 0; b < nsb; ++b) {
-        // lower bound of window b: layer 0 -> t (-) ((b+1) (x) t_s); l >= 1 -> inherited
-        const float x = p.layer == 0 ? __fsub_rn(t, __fmul_rn((float)(b + 1), p.snapshot_len)) : lin;
-        uint32_t a = lo;
-        if (x > -INFINITY && bcur > lo)  // empty window when the element before the cut is < x
-            a = __ldg(p.ts + bcur - 1) < x ? bcur : lower_bound_ts(p, lo, bcur - 1, x);
-        const uint32_t c = bcur - a;
-        const uint32_t take = c < k ? c : k;
-        if (valid) {
-            p.win_first[(size_t)b * p.roots_cap + i] = STRATEGY == TGL_MOST_RECENT ? bcur - take : a;
-            p.win_len[(size_t)b * p.roots_cap + i] = STRATEGY == TGL_MOST_RECENT ? take : c;
-        }
-        uint32_t s = take;
+    const bool early = lo < hi && __ldg(p.ts + lo) < t;
+    if (nsb <= 3 && p.layer == 0 && isfinite(p.snapshot_len)) {
+        // all S+1 cuts at once: c_0 = t, c_{b+1} = t (-) ((b+1) (x) t_s)
+        float x[4];
+        uint32_t cut[4] = {lo, lo, lo, lo};
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(kFull, s, o);
-        if (lane == 0) s_red[b][warp] = s;
-        bcur = a;
+        for (int j = 0; j < 4; ++j) x[j] = j == 0 ? t : __fsub_rn(t, __fmul_rn((float)j, p.snapshot_len));
+        if (early) lower_bound_multi(p, lo, hi, nsb + 1, x, cut);
+#pragma unroll
+        for (int b = 0; b < 3; ++b) {
+            if (b >= nsb) break;
+            const uint32_t c = cut[b] - cut[b + 1];
+            const uint32_t take = c < k ? c : k;
+            if (valid) {
+                p.win_first[(size_t)b * p.roots_cap + i] = STRATEGY == TGL_MOST_RECENT ? cut[b] - take : cut[b + 1];
+                p.win_len[(size_t)b * p.roots_cap + i] = STRATEGY == TGL_MOST_RECENT ? take : c;
+            }
+            uint32_t s2 = take;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) s2 += __shfl_xor_sync(kFull, s2, o);
+            if (lane == 0) s_red[b][warp] = s2;
+        }
+    } else {
+        uint32_t bcur = early ? lower_bound_ts(p, lo, hi, t) : lo;
+        for (int b = 0; b < nsb; ++b) {
+            // lower bound of window b: layer 0 -> t (-) ((b+1) (x) t_s); l >= 1 -> inherited
+            const float x = p.layer == 0 ? __fsub_rn(t, __fmul_rn((float)(b + 1), p.snapshot_len)) : lin;
+            uint32_t a = lo;
+            if (x > -INFINITY && bcur > lo)  // empty window when the element before the cut is < x
+                a = __ldg(p.ts + bcur - 1) < x ? bcur : lower_bound_ts(p, lo, bcur - 1, x);
+            const uint32_t c = bcur - a;
+            const uint32_t take = c < k ? c : k;
+            if (valid) {
+                p.win_first[(size_t)b * p.roots_cap + i] = STRATEGY == TGL_MOST_RECENT ? bcur - take : a;
+                p.win_len[(size_t)b * p.roots_cap + i] = STRATEGY == TGL_MOST_RECENT ? take : c;
+            }
+            uint32_t s2 = take;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) s2 += __shfl_xor_sync(kFull, s2, o);
+            if (lane == 0) s_red[b][warp] = s2;
+            bcur = a;
+        }
     }
     __syncthreads();
     if (threadIdx.x < nsb) {
