@@ -9,7 +9,7 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libtgl.so")
+LIB_PATH = os.environ.get("TGL_LIB_PATH") or os.path.join(_HERE, "libtgl.so")  # override: experiments only
 
 OK, EINVAL, ERANGE, EUNSORTED, ECAPACITY, EWORKSPACE, ECUDA, ENCCL, ENOTSUP = 0, -1, -2, -3, -4, -5, -6, -7, -8
 MOST_RECENT, UNIFORM = 0, 1

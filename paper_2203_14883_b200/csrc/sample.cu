@@ -36,7 +36,7 @@ namespace tgl {
 
 constexpr int kTile = 256;  // roots per tile (one lane per root)
 constexpr int kWarps = kTile / 32;
-constexpr int kCopyUnroll = 4;
+constexpr int kCopyUnroll = 2;
 constexpr uint32_t kIndexMin = 256;          // lists longer than this descend the 16-ary index
 constexpr int kPicksSmemPerWarp = 8 * 1024;  // bytes of uniform picks kept in shared memory per warp
 
@@ -329,7 +329,7 @@ __host__ __device__ inline int copy_warp_words(int nsb, int k, bool picks_in_sme
 }
 
 template <int STRATEGY>
-__global__ void __launch_bounds__(kTile) copy_kernel(const __grid_constant__ SampleParams p) {
+__global__ void __launch_bounds__(kTile, 6) copy_kernel(const __grid_constant__ SampleParams p) {
     extern __shared__ __align__(16) uint32_t smem[];
     __shared__ uint32_t s_wsum[TGL_MAX_SNAPSHOTS][kWarps];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
