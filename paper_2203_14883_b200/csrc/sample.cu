@@ -13,8 +13,9 @@
 //                      window descriptor and per (snapshot, 256-root tile) the edge count:
 //                      most_recent -> min(k, c) "closest to the end pointer";
 //                      uniform -> min(k, c) (R#5).
-//   K5  tile_scan      one CTA: exclusive scan of the per-tile totals -> tile bases, nnz, n_roots,
-//                      offsets[n].  Deterministic: no atomic decides a position.
+//   (K5) tile bases   the window kernel also adds its tile totals into per-64-tile super totals
+//                      (integer atomics: order-independent, so deterministic); a copy CTA sums
+//                      the super totals and tile totals before it -- no scan kernel, no waiting.
 //   K4b copy_kernel    one warp per 32 roots: warp scan of its counts + tile base -> offsets[i];
 //                      uniform: Floyd's k-subset with Philox4x32-10 draws, ascending (R#5, R#6);
 //                      then the tile's outputs are copied as one flat range per snapshot -- lane o
@@ -37,6 +38,7 @@ namespace tgl {
 constexpr int kTile = 256;  // roots per tile (one lane per root)
 constexpr int kWarps = kTile / 32;
 constexpr int kCopyUnroll = 2;
+constexpr int kSuperShift = 6;  // 64 tiles per super tile (tile bases: super totals + tile totals)
 constexpr uint32_t kIndexMin = 256;          // lists longer than this descend the 16-ary index
 constexpr int kPicksSmemPerWarp = 8 * 1024;  // bytes of uniform picks kept in shared memory per warp
 
@@ -74,8 +76,9 @@ struct SampleParams {
     uint32_t seed_lo, seed_hi;
     uint32_t* win_first;  // [nsb][roots_cap] first slot (uniform: a; most_recent: b - take)
     uint32_t* win_len;    // [nsb][roots_cap] uniform: window size c; most_recent: take = min(k, c)
-    uint32_t* tile_tot;   // [nsb][tiles_cap] edges emitted per tile
-    uint64_t* tile_base;  // [nsb][tiles_cap] exclusive prefix of tile_tot
+    uint32_t* tile_tot;    // [nsb][tiles_cap] edges emitted per 256-root tile
+    uint64_t* super_tot;   // [nsb][supers_cap] per 64 tiles (integer atomics: order-independent), zeroed per call
+    int64_t supers_cap;
     int64_t roots_cap, tiles_cap;
     uint32_t* picks_global;  // null -> picks in shared memory; else [tiles_cap * 8 warps][nsb*k][32]
     int* err;
@@ -263,63 +266,9 @@ __global__ void __launch_bounds__(kTile) window_kernel(const __grid_constant__ S
 #pragma unroll
         for (int w = 0; w < kWarps; ++w) s += s_red[threadIdx.x][w];
         p.tile_tot[(size_t)threadIdx.x * p.tiles_cap + blockIdx.x] = s;
-    }
-}
-
-// ---------------------------------------------------------------------------- K5 tile scan
-// One CTA; thread j owns a contiguous run of ceil(tiles / 1024) tiles: local sums, one block scan
-// per snapshot, local re-scan.
-__device__ __forceinline__ uint64_t block_excl_scan_1024(uint64_t v, uint64_t* sm /*[33]*/, uint64_t* total) {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    uint64_t x = v;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const uint64_t y = __shfl_up_sync(kFull, x, o);
-        if (lane >= o) x += y;
-    }
-    if (lane == 31) sm[warp] = x;
-    __syncthreads();
-    if (warp == 0) {
-        const uint64_t w = sm[lane];
-        uint64_t wi = w;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint64_t y = __shfl_up_sync(kFull, wi, o);
-            if (lane >= o) wi += y;
-        }
-        sm[lane] = wi - w;
-        if (lane == 31) sm[32] = wi;
-    }
-    __syncthreads();
-    const uint64_t r = sm[warp] + x - v;
-    *total = sm[32];
-    __syncthreads();
-    return r;
-}
-
-__global__ void __launch_bounds__(1024) tile_scan_kernel(const __grid_constant__ SampleParams p) {
-    __shared__ uint64_t sm[33];
-    const int64_t n = chain_roots(p);
-    const int64_t tiles = (n + kTile - 1) / kTile;
-    const int64_t per = (tiles + 1023) / 1024;
-    const int64_t t0 = (int64_t)threadIdx.x * per;
-    for (int b = 0; b < p.nsb; ++b) {
-        const uint32_t* tot = p.tile_tot + (size_t)b * p.tiles_cap;
-        uint64_t* base = p.tile_base + (size_t)b * p.tiles_cap;
-        uint64_t s = 0;
-        for (int64_t t = t0; t < t0 + per && t < tiles; ++t) s += tot[t];
-        uint64_t total;
-        uint64_t run = block_excl_scan_1024(s, sm, &total);
-        for (int64_t t = t0; t < t0 + per && t < tiles; ++t) {
-            base[t] = run;
-            run += tot[t];
-        }
-        if (threadIdx.x == 0) {
-            const BlockOut& o = p.out[b];
-            o.offsets[n] = (int64_t)total;
-            *o.nnz_dev = (int64_t)total;
-            *o.n_roots_dev = n;
-        }
+        atomicAdd(reinterpret_cast<unsigned long long*>(p.super_tot + (size_t)threadIdx.x * p.supers_cap +
+                                                        (blockIdx.x >> kSuperShift)),
+                  (unsigned long long)s);
     }
 }
 
@@ -332,9 +281,18 @@ template <int STRATEGY>
 __global__ void __launch_bounds__(kTile, 6) copy_kernel(const __grid_constant__ SampleParams p) {
     extern __shared__ __align__(16) uint32_t smem[];
     __shared__ uint32_t s_wsum[TGL_MAX_SNAPSHOTS][kWarps];
+    __shared__ uint64_t s_tbase[TGL_MAX_SNAPSHOTS];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int64_t n = chain_roots(p);
     const int64_t base_i = (int64_t)blockIdx.x * kTile;
+    if (n == 0) {  // empty chain: the first CTA writes the empty blocks
+        if (blockIdx.x == 0 && threadIdx.x < p.nsb) {
+            p.out[threadIdx.x].offsets[0] = 0;
+            *p.out[threadIdx.x].nnz_dev = 0;
+            *p.out[threadIdx.x].n_roots_dev = 0;
+        }
+        return;
+    }
     if (base_i >= n) return;
     const int64_t i = base_i + threadIdx.x;
     const bool valid = i < n;
@@ -399,10 +357,30 @@ __global__ void __launch_bounds__(kTile, 6) copy_kernel(const __grid_constant__ 
             }
         }
     }
+    // tile base per snapshot: warp b sums the super totals before this tile's super tile and the
+    // tile totals before this tile inside it (all final: the window kernel has completed)
+    for (int b = warp; b < nsb; b += kWarps) {
+        const int64_t t = blockIdx.x, sup = t >> kSuperShift;
+        uint64_t acc = 0;
+        for (int64_t q = lane; q < sup; q += 32) acc += p.super_tot[(size_t)b * p.supers_cap + q];
+        for (int64_t q = (sup << kSuperShift) + lane; q < t; q += 32) acc += p.tile_tot[(size_t)b * p.tiles_cap + q];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(kFull, acc, o);
+        if (lane == 0) s_tbase[b] = acc;
+    }
     __syncthreads();
+    const bool last_tile = base_i + kTile >= n;
     for (int b = 0; b < nsb; ++b) {
-        uint64_t wb = p.tile_base[(size_t)b * p.tiles_cap + blockIdx.x];
+        uint64_t wb = s_tbase[b];
         for (int w = 0; w < warp; ++w) wb += s_wsum[b][w];
+        if (last_tile && threadIdx.x == 0) {  // chain totals: offsets[n], nnz, n_roots
+            uint64_t tot = wb;
+            for (int w = 0; w < kWarps; ++w) tot += s_wsum[b][w];
+            const BlockOut& o = p.out[b];
+            o.offsets[n] = (int64_t)tot;
+            *o.nnz_dev = (int64_t)tot;
+            *o.n_roots_dev = n;
+        }
         if (lane == 0) base[b] = wb;
         const uint32_t ex = lane ? inc[b * 32 + lane - 1] : 0u;
         if (valid) p.out[b].offsets[i] = (int64_t)(wb + ex);
@@ -472,7 +450,8 @@ struct Launch {
     int layer, chain, nsb;
     int64_t roots_cap, tiles_cap;
     uint32_t *win_first, *win_len, *tile_tot;
-    uint64_t* tile_base;
+    uint64_t* super_tot;
+    int64_t supers_cap;
     uint32_t* picks;  // global picks or null
 };
 
@@ -481,6 +460,7 @@ struct SamplePlan {
     int64_t roots_cap[64], edges_cap[64];
     Launch launches[1 + 63 * TGL_MAX_SNAPSHOTS];
     int n_launch = 0;
+    size_t memset_from = 0, memset_bytes = 0;
     uint64_t* child_key[64][TGL_MAX_SNAPSHOTS];
     float* child_lo[64][TGL_MAX_SNAPSHOTS];
     size_t bytes = 0;
@@ -515,7 +495,7 @@ static int plan_sample(int64_t n_roots, int L, const int32_t* fanouts, int S, in
         la.win_first = c.take<uint32_t>((size_t)nsb * la.roots_cap);
         la.win_len = c.take<uint32_t>((size_t)nsb * la.roots_cap);
         la.tile_tot = c.take<uint32_t>((size_t)nsb * la.tiles_cap);
-        la.tile_base = c.take<uint64_t>((size_t)nsb * la.tiles_cap);
+        la.supers_cap = (la.tiles_cap + (1 << kSuperShift) - 1) >> kSuperShift;
         la.picks = nullptr;
         if (strategy == TGL_UNIFORM && !picks_fit_smem(nsb, fanouts[layer]))
             la.picks = c.take<uint32_t>((size_t)la.tiles_cap * kTile * nsb * fanouts[layer]);
@@ -523,6 +503,11 @@ static int plan_sample(int64_t n_roots, int L, const int32_t* fanouts, int S, in
     add(0, 0, S);
     for (int l = 1; l < L; ++l)
         for (int s = 0; s < S; ++s) add(l, s, 1);
+    // super totals of every chain together: one contiguous region, one memset per call
+    P.memset_from = c.bytes();
+    for (int j = 0; j < P.n_launch; ++j)
+        P.launches[j].super_tot = c.take<uint64_t>((size_t)P.launches[j].nsb * P.launches[j].supers_cap);
+    P.memset_bytes = c.bytes() - P.memset_from;
     const bool need_lo = L > 1 && std::isfinite(snapshot_len);
     for (int l = 0; l < L - 1; ++l)
         for (int s = 0; s < S; ++s) {
@@ -536,7 +521,6 @@ static int plan_sample(int64_t n_roots, int L, const int32_t* fanouts, int S, in
 template <int STRATEGY>
 static int launch_chain(const SampleParams& sp, int64_t grid, size_t smem, cudaStream_t st) {
     window_kernel<STRATEGY><<<(unsigned)grid, kTile, 0, st>>>(sp);
-    tile_scan_kernel<<<1, 1024, 0, st>>>(sp);
     if (smem > 48 * 1024)
         cudaFuncSetAttribute(copy_kernel<STRATEGY>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     copy_kernel<STRATEGY><<<(unsigned)grid, kTile, smem, st>>>(sp);
@@ -582,6 +566,8 @@ static int sample_impl(const tgl_tcsr* g, const int32_t* roots, const float* roo
             if (b.cap_roots < P.roots_cap[l] || b.cap_edges < P.edges_cap[l]) return TGL_ECAPACITY;
         }
     cudaStream_t st = (cudaStream_t)stream;
+    if (cudaMemsetAsync(static_cast<char*>(workspace) + P.memset_from, 0, P.memset_bytes, st) != cudaSuccess)
+        return TGL_ECUDA;
     // experiment knobs (tools/sweep.py): TGL_NO_INDEX, TGL_NO_RECS
     const bool use_recs = g->recs && !getenv("TGL_NO_RECS");
     const bool use_index = g->index && g->n_levels > 0 && !getenv("TGL_NO_INDEX");
@@ -624,7 +610,8 @@ static int sample_impl(const tgl_tcsr* g, const int32_t* roots, const float* roo
         sp.win_first = la.win_first;
         sp.win_len = la.win_len;
         sp.tile_tot = la.tile_tot;
-        sp.tile_base = la.tile_base;
+        sp.super_tot = la.super_tot;
+        sp.supers_cap = la.supers_cap;
         sp.roots_cap = la.roots_cap;
         sp.tiles_cap = la.tiles_cap;
         sp.picks_global = la.picks;
