@@ -92,10 +92,11 @@ TGL_API int tgl_tcsr_build_workspace(int64_t n_edges, int32_t n_nodes, int add_r
  *   broken by stream order (R#8).  Bit-identical to the oracle's counting sort.
  *   ts_out must be 64-byte aligned and its allocation must extend to round_up(E_s, 16) floats: the
  *   sampler reads timestamps in aligned 16-float (64-byte, one HBM atom) groups.
- * aux (optional, may be NULL): >= tgl_tcsr_aux_bytes(E_s) bytes, 256-byte aligned; filled with the
- *   sampler's acceleration structures over the T-CSR: the 16-ary atom index over ts_out (cut
- *   search) and a 16-byte record {ts, nbr, eid, 0} per slot, so search and payload copy read the
- *   same lines -- DESIGN.md "Data layout".  Without it the sampler reads the separate arrays.
+ * aux (optional, may be NULL): >= tgl_tcsr_aux_bytes(E_s, V) bytes, 256-byte aligned; filled with
+ *   the sampler's acceleration structures over the T-CSR: the 16-ary index over ts_out (long-list
+ *   cut search), a 16-byte record {ts, nbr, eid, 0} per slot (payload copy: one request per run)
+ *   and a 16-byte record {lo, hi, ts_first, ts_last} per node (list bounds and time span in one
+ *   load) -- DESIGN.md "Data layout".  Without it the sampler reads the separate arrays.
  * workspace: >= tgl_tcsr_build_workspace() bytes of device memory, 256-byte aligned.
  * Synchronous validation: the call blocks on `stream` once to read the device validation word;
  *   on ERANGE / EINVAL / EUNSORTED no handle is returned and outputs are unspecified.
@@ -107,12 +108,12 @@ TGL_API int tgl_tcsr_build(const int32_t *src, const int32_t *dst, const float *
                    void *aux, size_t aux_bytes,
                    void *workspace, size_t ws_bytes, void *stream, tgl_tcsr **out /* host */);
 
-/* Bytes of the optional sampler aux buffer for a T-CSR of n_stored edges (host query). */
-TGL_API int tgl_tcsr_aux_bytes(int64_t n_stored, size_t *bytes /* host */);
+/* Bytes of the optional sampler aux buffer for a T-CSR of n_stored edges over n_nodes nodes. */
+TGL_API int tgl_tcsr_aux_bytes(int64_t n_stored, int32_t n_nodes, size_t *bytes /* host */);
 
 /* (Re)build the aux buffer over existing T-CSR arrays (e.g. ones received from another rank). */
-TGL_API int tgl_tcsr_aux_build(const float *ts, const int32_t *nbr, const int32_t *eid, int64_t n_stored,
-                       void *aux, size_t aux_bytes, void *stream);
+TGL_API int tgl_tcsr_aux_build(const int64_t *indptr, const float *ts, const int32_t *nbr, const int32_t *eid,
+                       int32_t n_nodes, int64_t n_stored, void *aux, size_t aux_bytes, void *stream);
 
 /* Wrap already-built T-CSR arrays (e.g. received from another rank) in a handle.  No
  * validation beyond NULL / size checks.  n_stored = E_s = indptr[n_nodes].  aux may be NULL or a

@@ -88,9 +88,9 @@ def build_workspace_bytes(n_edges: int, n_nodes: int, add_reverse: bool) -> int:
     return b.value
 
 
-def aux_bytes(n_stored: int) -> int:
+def aux_bytes(n_stored: int, n_nodes: int) -> int:
     b = ctypes.c_size_t()
-    _rc(_L.tgl_tcsr_aux_bytes(int(n_stored), ctypes.byref(b)), "tgl_tcsr_aux_bytes")
+    _rc(_L.tgl_tcsr_aux_bytes(int(n_stored), int(n_nodes), ctypes.byref(b)), "tgl_tcsr_aux_bytes")
     return b.value
 
 
@@ -118,7 +118,7 @@ def build(src: torch.Tensor, dst: torch.Tensor, ts: torch.Tensor, eid: Optional[
     nbr = torch.empty(Es, dtype=torch.int32, device=dev)
     ts_out, ts_storage = _ts_buffer(Es, dev)
     eid_out = torch.empty(Es, dtype=torch.int32, device=dev)
-    ib = aux_bytes(Es) if with_index else 0
+    ib = aux_bytes(Es, n_nodes) if with_index else 0
     index = torch.empty(ib, dtype=torch.uint8, device=dev) if with_index else None
     wsb = build_workspace_bytes(E, n_nodes, add_reverse)
     if workspace is None or workspace.numel() < wsb:
@@ -139,11 +139,12 @@ def wrap(indptr: torch.Tensor, nbr: torch.Tensor, ts: torch.Tensor, eid: torch.T
     n = nbr.numel()
     ts_view, ts_storage = _ts_buffer(n, nbr.device)
     ts_view.copy_(_cuda(ts, torch.float32, "ts"))
-    ib = aux_bytes(n) if with_index else 0
+    V = indptr.numel() - 1
+    ib = aux_bytes(n, V) if with_index else 0
     index = torch.empty(ib, dtype=torch.uint8, device=nbr.device) if with_index else None
     if with_index:
-        _rc(_L.tgl_tcsr_aux_build(_ptr(ts_storage), _ptr(nbr), _ptr(eid), n, _ptr(index), ib, _stream(stream)),
-            "tgl_tcsr_aux_build")
+        _rc(_L.tgl_tcsr_aux_build(_ptr(indptr), _ptr(ts_storage), _ptr(nbr), _ptr(eid), V, n, _ptr(index), ib,
+                                  _stream(stream)), "tgl_tcsr_aux_build")
     h = ctypes.c_void_p()
     _rc(_L.tgl_tcsr_wrap(_ptr(indptr), _ptr(nbr), _ptr(ts_storage), _ptr(eid), _ptr(index), ib,
                          indptr.numel() - 1, n, ctypes.byref(h)), "tgl_tcsr_wrap")

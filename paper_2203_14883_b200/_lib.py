@@ -37,8 +37,8 @@ SIGNATURES = {
     "tgl_tcsr_build_workspace": (ctypes.c_int, [i64, i32, ctypes.c_int, ctypes.POINTER(sz)]),
     "tgl_tcsr_build": (ctypes.c_int, [P, P, P, P, i64, i32, ctypes.c_int, P, P, P, P, P, sz, P, sz, P,
                                       ctypes.POINTER(P)]),
-    "tgl_tcsr_aux_bytes": (ctypes.c_int, [i64, ctypes.POINTER(sz)]),
-    "tgl_tcsr_aux_build": (ctypes.c_int, [P, P, P, i64, P, sz, P]),
+    "tgl_tcsr_aux_bytes": (ctypes.c_int, [i64, i32, ctypes.POINTER(sz)]),
+    "tgl_tcsr_aux_build": (ctypes.c_int, [P, P, P, P, i32, i64, P, sz, P]),
     "tgl_tcsr_wrap": (ctypes.c_int, [P, P, P, P, P, sz, i32, i64, ctypes.POINTER(P)]),
     "tgl_tcsr_destroy": (ctypes.c_int, [P]),
     "tgl_tcsr_info": (ctypes.c_int, [P, ctypes.POINTER(i32), ctypes.POINTER(i64)]),

@@ -49,7 +49,7 @@ extern "C" int tgl_tcsr_wrap(const int64_t* indptr, const int32_t* nbr, const fl
     *out = nullptr;
     if (n_stored > 0 && (!nbr || !ts || !eid)) return TGL_EINVAL;
     if ((uint64_t)n_stored >= (1ull << 32)) return TGL_EINVAL;
-    const AuxLayout lay = aux_layout((uint64_t)n_stored);
+    const AuxLayout lay = aux_layout((uint64_t)n_stored, (uint64_t)n_nodes);
     if (aux && aux_bytes < lay.bytes) return TGL_EWORKSPACE;
     int rc = check_device();
     if (rc) return rc;
@@ -69,6 +69,7 @@ extern "C" int tgl_tcsr_wrap(const int64_t* indptr, const int32_t* nbr, const fl
     g->n_levels = aux ? lay.index.n_levels : 0;
     for (int l = 0; l <= kMaxIndexLevels && l < 12; ++l) g->level_off[l] = lay.index.off[l];
     g->recs = aux ? static_cast<const void*>(static_cast<const char*>(aux) + lay.rec_off) : nullptr;
+    g->nodes = aux ? static_cast<const void*>(static_cast<const char*>(aux) + lay.node_off) : nullptr;
     cudaGetDevice(&g->device);
     *out = g;
     return TGL_OK;

@@ -235,8 +235,9 @@ extern "C" int tgl_tcsr_build_workspace(int64_t n_edges, int32_t n_nodes, int ad
 
 namespace tgl {
 // aux buffer (tsindex.cuh): index levels L_l[j] = ts[j * 16^l] and the interleaved payload
-__global__ void aux_build_kernel(const float* __restrict__ ts, const int32_t* __restrict__ nbr,
-                                 const int32_t* __restrict__ eid, uint64_t n, char* __restrict__ aux, AuxLayout lay) {
+__global__ void aux_build_kernel(const int64_t* __restrict__ indptr, const float* __restrict__ ts,
+                                 const int32_t* __restrict__ nbr, const int32_t* __restrict__ eid, uint64_t n,
+                                 uint64_t n_nodes, char* __restrict__ aux, AuxLayout lay) {
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
     float* index = reinterpret_cast<float*>(aux);
     for (int l = 1; l <= lay.index.n_levels; ++l) {
@@ -248,27 +249,32 @@ __global__ void aux_build_kernel(const float* __restrict__ ts, const int32_t* __
     int4* rec = reinterpret_cast<int4*>(aux + lay.rec_off);
     for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += stride)
         rec[j] = make_int4(__float_as_int(ts[j]), nbr[j], eid[j], 0);
+    int4* node = reinterpret_cast<int4*>(aux + lay.node_off);
+    for (uint64_t v = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n_nodes; v += stride) {
+        const uint32_t lo = (uint32_t)indptr[v], hi = (uint32_t)indptr[v + 1];
+        const float f = lo < hi ? ts[lo] : INFINITY, l = lo < hi ? ts[hi - 1] : -INFINITY;
+        node[v] = make_int4((int)lo, (int)hi, __float_as_int(f), __float_as_int(l));
+    }
 }
 }  // namespace tgl
 
-extern "C" int tgl_tcsr_aux_bytes(int64_t n_stored, size_t* bytes) {
-    if (!bytes || n_stored < 0 || (uint64_t)n_stored >= (1ull << 32)) return TGL_EINVAL;
-    *bytes = aux_layout((uint64_t)n_stored).bytes;
+extern "C" int tgl_tcsr_aux_bytes(int64_t n_stored, int32_t n_nodes, size_t* bytes) {
+    if (!bytes || n_stored < 0 || n_nodes < 0 || (uint64_t)n_stored >= (1ull << 32)) return TGL_EINVAL;
+    *bytes = aux_layout((uint64_t)n_stored, (uint64_t)n_nodes).bytes;
     return TGL_OK;
 }
 
-extern "C" int tgl_tcsr_aux_build(const float* ts, const int32_t* nbr, const int32_t* eid, int64_t n_stored,
-                                  void* aux, size_t aux_bytes, void* stream) {
-    if (n_stored < 0 || (uint64_t)n_stored >= (1ull << 32) || !aux) return TGL_EINVAL;
+extern "C" int tgl_tcsr_aux_build(const int64_t* indptr, const float* ts, const int32_t* nbr, const int32_t* eid,
+                                  int32_t n_nodes, int64_t n_stored, void* aux, size_t aux_bytes, void* stream) {
+    if (n_stored < 0 || n_nodes < 0 || (uint64_t)n_stored >= (1ull << 32) || !aux || !indptr) return TGL_EINVAL;
     if (n_stored > 0 && (!ts || !nbr || !eid)) return TGL_EINVAL;
-    const AuxLayout lay = aux_layout((uint64_t)n_stored);
+    const AuxLayout lay = aux_layout((uint64_t)n_stored, (uint64_t)n_nodes);
     if (aux_bytes < lay.bytes) return TGL_EWORKSPACE;
     int rc = check_device();
     if (rc) return rc;
-    if (n_stored == 0) return TGL_OK;
-    const int64_t blocks = std::min<int64_t>((int64_t)((n_stored + 255) / 256), 148 * 16);
+    const int64_t blocks = std::min<int64_t>((int64_t)((std::max<int64_t>(n_stored, n_nodes) + 255) / 256), 148 * 16);
     aux_build_kernel<<<(unsigned)std::max<int64_t>(blocks, 1), 256, 0, (cudaStream_t)stream>>>(
-        ts, nbr, eid, (uint64_t)n_stored, static_cast<char*>(aux), lay);
+        indptr, ts, nbr, eid, (uint64_t)n_stored, (uint64_t)n_nodes, static_cast<char*>(aux), lay);
     return cudaGetLastError() == cudaSuccess ? TGL_OK : TGL_ECUDA;
 }
 
@@ -347,7 +353,7 @@ extern "C" int tgl_tcsr_build(const int32_t* src, const int32_t* dst, const floa
         }
     }
     if (aux) {
-        rc = tgl_tcsr_aux_build(ts_out, nbr, eid_out, (int64_t)es, aux, aux_bytes, stream);
+        rc = tgl_tcsr_aux_build(indptr, ts_out, nbr, eid_out, n_nodes, (int64_t)es, aux, aux_bytes, stream);
         if (rc) return rc;
     }
     return tgl_tcsr_wrap(indptr, nbr, ts_out, eid_out, aux, aux_bytes, n_nodes, (int64_t)es, out);

@@ -60,6 +60,7 @@ struct SampleParams {
     const float* ts;
     const int32_t* eid;
     const int4* recs;                       // 16-byte slot records {ts, nbr, eid, 0}, or null
+    const int4* nodes;                      // 16-byte node records {lo, hi, ts_first, ts_last}, or null
     const float* lvl[kMaxIndexLevels + 1];  // lvl[l] = index level l (1-based)
     int32_t n_levels;                       // 0 -> no index
     int32_t n_nodes;
@@ -138,12 +139,12 @@ __device__ __forceinline__ uint32_t lower_bound_ts(const SampleParams& p, uint32
 
 // Up to 4 cuts searched together over [lo, hi): interleaved binary searches, one independent probe
 // per live cut per step, so a root costs max(log2 d) dependent steps instead of the sum over cuts.
-__device__ __forceinline__ void lower_bound_multi(const SampleParams& p, uint32_t lo, uint32_t hi, int nc,
-                                                  const float (&x)[4], uint32_t (&out)[4]) {
+__device__ __forceinline__ void lower_bound_multi(const SampleParams& p, uint32_t lo, uint32_t hi, float ts_last,
+                                                  int nc, const float (&x)[4], uint32_t (&out)[4]) {
     uint32_t a[4], b[4];
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
-        a[j] = lo;
+        a[j] = ts_last < x[j] ? hi : lo;  // a cut after the list's last edge: every slot is < x
         b[j] = (j < nc && x[j] > -INFINITY) ? hi : lo;  // -inf cut: every slot is >= x
     }
     while (true) {
@@ -212,19 +213,29 @@ __global__ void __launch_bounds__(kTile) window_kernel(const __grid_constant__ S
     float lin = -INFINITY;
     if (p.layer > 0 && p.root_lo && ok) lin = p.root_lo[i];
     uint32_t lo = 0, hi = 0;
+    float ts_first = INFINITY, ts_last = INFINITY;  // INFINITY: unknown / no shortcut
     if (ok) {
-        lo = (uint32_t)__ldg(p.indptr + v);
-        hi = (uint32_t)__ldg(p.indptr + v + 1);
+        if (p.nodes) {  // one 16-byte load: bounds + time span of the list
+            const int4 nr = __ldg(p.nodes + v);
+            lo = (uint32_t)nr.x;
+            hi = (uint32_t)nr.y;
+            ts_first = __int_as_float(nr.z);
+            ts_last = __int_as_float(nr.w);
+        } else {
+            lo = (uint32_t)__ldg(p.indptr + v);
+            hi = (uint32_t)__ldg(p.indptr + v + 1);
+            if (lo < hi) ts_first = __ldg(p.ts + lo);
+        }
     }
     // U of window 0 is the root's own time t; a list starting at or after t has no candidate
-    const bool early = lo < hi && __ldg(p.ts + lo) < t;
+    const bool early = lo < hi && ts_first < t;
     if (nsb <= 3 && p.layer == 0 && isfinite(p.snapshot_len)) {
         // all S+1 cuts at once: c_0 = t, c_{b+1} = t (-) ((b+1) (x) t_s)
         float x[4];
         uint32_t cut[4] = {lo, lo, lo, lo};
 #pragma unroll
         for (int j = 0; j < 4; ++j) x[j] = j == 0 ? t : __fsub_rn(t, __fmul_rn((float)j, p.snapshot_len));
-        if (early) lower_bound_multi(p, lo, hi, nsb + 1, x, cut);
+        if (early) lower_bound_multi(p, lo, hi, p.nodes ? ts_last : INFINITY, nsb + 1, x, cut);
 #pragma unroll
         for (int b = 0; b < 3; ++b) {
             if (b >= nsb) break;
@@ -581,6 +592,7 @@ static int sample_impl(const tgl_tcsr* g, const int32_t* roots, const float* roo
         sp.ts = g->ts;
         sp.eid = g->eid;
         sp.recs = use_recs ? static_cast<const int4*>(g->recs) : nullptr;
+        sp.nodes = use_recs ? static_cast<const int4*>(g->nodes) : nullptr;
         sp.n_levels = use_index ? g->n_levels : 0;
         for (int q = 1; q <= sp.n_levels; ++q) sp.lvl[q] = g->index + g->level_off[q];
         sp.n_nodes = g->n_nodes;

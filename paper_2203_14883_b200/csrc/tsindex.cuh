@@ -58,17 +58,28 @@ struct SlotRec {
 };
 static_assert(sizeof(SlotRec) == 16, "slot record is one 16-byte vector");
 
+// Per-node 16-byte record {lo, hi, ts_first, ts_last}: one load gives the list bounds AND its time
+// span, so a root whose list starts at or after its time (or ends before it) needs no list access,
+// and the others start searching one dependent DRAM step earlier than indptr -> ts[lo].
+struct NodeRec {
+    uint32_t lo, hi;
+    float ts_first, ts_last;  // +inf / -inf for an empty list
+};
+static_assert(sizeof(NodeRec) == 16, "node record is one 16-byte vector");
+
 struct AuxLayout {
     IndexLayout index;
-    uint64_t rec_off = 0;  // byte offset of the SlotRec array
+    uint64_t rec_off = 0;   // byte offset of the SlotRec array
+    uint64_t node_off = 0;  // byte offset of the NodeRec array
     uint64_t bytes = 0;
 };
 
-inline AuxLayout aux_layout(uint64_t n_stored) {
+inline AuxLayout aux_layout(uint64_t n_stored, uint64_t n_nodes) {
     AuxLayout A;
     A.index = index_layout(n_stored);
     A.rec_off = align_up(A.index.floats * sizeof(float), 256);
-    A.bytes = align_up(A.rec_off + n_stored * sizeof(SlotRec), 256);
+    A.node_off = align_up(A.rec_off + n_stored * sizeof(SlotRec), 256);
+    A.bytes = align_up(A.node_off + n_nodes * sizeof(NodeRec), 256);
     if (A.bytes < 256) A.bytes = 256;
     return A;
 }

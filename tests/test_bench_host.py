@@ -9,6 +9,13 @@ import textwrap
 import pytest
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _free_port():
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        return so.getsockname()[1]
 sys.path.insert(0, ROOT)
 
 import bench  # noqa: E402
@@ -59,7 +66,7 @@ def test_reduce_report_gloo_world2(tmp_path):
     script.write_text(REPORT)
     env = dict(os.environ, REPO=ROOT)
     r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
-                        "--master-addr=127.0.0.1", "--master-port=29655", str(script)],
+                        "--master-addr=127.0.0.1", f"--master-port={_free_port()}", str(script)],
                        env=env, capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stderr[-3000:]
     assert r.stdout.count("ok") == 2

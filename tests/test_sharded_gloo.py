@@ -12,6 +12,13 @@ import pytest
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
+
+def _free_port():
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        return so.getsockname()[1]
+
 WORKER = textwrap.dedent(r'''
     import math, os, sys
     sys.path.insert(0, os.environ["REPO"])
@@ -85,7 +92,7 @@ def test_node_sharded_protocol_gloo_world2(tmp_path, S, ts, strat):
     script = tmp_path / "worker.py"
     script.write_text(WORKER)
     env = dict(os.environ, REPO=ROOT, S=str(S), TS=str(ts), STRAT=str(strat), MASTER_ADDR="127.0.0.1")
-    port = 29600 + S * 3 + strat
+    port = _free_port()
     r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
                         "--master-addr=127.0.0.1", f"--master-port={port}", str(script)],
                        env=env, capture_output=True, text=True, timeout=300)
