@@ -241,7 +241,7 @@ def run_ours(args):
     chunks = [C.roots(cfg, src, dst, ts, s0, chunk) for s0 in mine]
     sampler = tgl.Sampler(g, chunk, cfg.fanouts, cfg.strategy, cfg.n_snapshots, cfg.snapshot_len)
     L, S = len(cfg.fanouts), cfg.n_snapshots
-    launches_per_step = 3 * (1 + (L - 1) * S)  # window + tile scan + copy per chain
+    launches_per_step = 2 * (1 + (L - 1) * S)  # window + copy kernel per chain (+1 memset, not ours)
     gather = make_gather(tgl, cfg, sampler, dev) if cfg.tables else None
     if gather is not None:
         launches_per_step += 3  # node tables by roots, node tables by nbr, edge features by eid
@@ -315,7 +315,7 @@ def run_ours(args):
                    "l2": "no flush: T-CSR and per-step roots exceed L2 (126 MB); every step's roots are distinct"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": None, "peak_source": peak_src,
-                     "kernel": (f"tgl_sample ({cfg.strategy}): window_kernel + tile_scan_kernel + copy_kernel"
+                     "kernel": (f"tgl_sample ({cfg.strategy}): window_kernel + copy_kernel"
                                 + (" + tgl_gather (3 launches)" if gather is not None else "") + ", timed together"),
                      "bytes_model": "SURVEY 8(d): per root 8+16+8*cuts+8*S, per edge 24 (+4 ts_edge if l<L-1)"
                                     + ("; gather: 2 x row bytes per gathered id" if gather is not None else ""),

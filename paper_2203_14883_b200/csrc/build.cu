@@ -249,11 +249,20 @@ __global__ void aux_build_kernel(const int64_t* __restrict__ indptr, const float
     int4* rec = reinterpret_cast<int4*>(aux + lay.rec_off);
     for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += stride)
         rec[j] = make_int4(__float_as_int(ts[j]), nbr[j], eid[j], 0);
+    // node records: thread (v, q) writes the q-th 16-byte quarter of node v's record
     int4* node = reinterpret_cast<int4*>(aux + lay.node_off);
-    for (uint64_t v = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n_nodes; v += stride) {
-        const uint32_t lo = (uint32_t)indptr[v], hi = (uint32_t)indptr[v + 1];
-        const float f = lo < hi ? ts[lo] : INFINITY, l = lo < hi ? ts[hi - 1] : -INFINITY;
-        node[v] = make_int4((int)lo, (int)hi, __float_as_int(f), __float_as_int(l));
+    for (uint64_t w = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; w < n_nodes * 4; w += stride) {
+        const uint64_t v = w >> 2;
+        const int q = (int)(w & 3);
+        const uint32_t lo = (uint32_t)indptr[v], hi = (uint32_t)indptr[v + 1], d = hi - lo;
+        int32_t word[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            const int j = 4 * q + e - 2;  // fence index of word e (words 0, 1 of quarter 0: lo, hi)
+            word[e] = j < 0 ? (int32_t)(j == -2 ? lo : hi)
+                            : __float_as_int(d ? ts[fence_pos(lo, d, j)] : INFINITY);
+        }
+        node[w] = make_int4(word[0], word[1], word[2], word[3]);
     }
 }
 }  // namespace tgl

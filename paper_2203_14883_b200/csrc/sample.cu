@@ -60,7 +60,7 @@ struct SampleParams {
     const float* ts;
     const int32_t* eid;
     const int4* recs;                       // 16-byte slot records {ts, nbr, eid, 0}, or null
-    const int4* nodes;                      // 16-byte node records {lo, hi, ts_first, ts_last}, or null
+    const int4* nodes;                      // 64-byte node records {lo, hi, 14 fences} (tsindex.cuh), or null
     const float* lvl[kMaxIndexLevels + 1];  // lvl[l] = index level l (1-based)
     int32_t n_levels;                       // 0 -> no index
     int32_t n_nodes;
@@ -137,16 +137,15 @@ __device__ __forceinline__ uint32_t lower_bound_ts(const SampleParams& p, uint32
     return lo;
 }
 
-// Up to 4 cuts searched together over [lo, hi): interleaved binary searches, one independent probe
-// per live cut per step, so a root costs max(log2 d) dependent steps instead of the sum over cuts.
-__device__ __forceinline__ void lower_bound_multi(const SampleParams& p, uint32_t lo, uint32_t hi, float ts_last,
-                                                  int nc, const float (&x)[4], uint32_t (&out)[4]) {
-    uint32_t a[4], b[4];
+// Up to 4 cuts searched together, cut j in [a[j], b[j]] (a fence gap, or the whole list):
+// interleaved binary searches, one independent probe per live cut per step, so a root costs
+// max(log2 gap) dependent steps instead of the sum over cuts.  Gaps longer than kIndexMin (hub
+// lists) descend the 16-ary index first.
+__device__ __forceinline__ void lower_bound_multi(const SampleParams& p, uint32_t (&a)[4], uint32_t (&b)[4],
+                                                  const float (&x)[4]) {
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-        a[j] = ts_last < x[j] ? hi : lo;  // a cut after the list's last edge: every slot is < x
-        b[j] = (j < nc && x[j] > -INFINITY) ? hi : lo;  // -inf cut: every slot is >= x
-    }
+    for (int j = 0; j < 4; ++j)
+        if (p.n_levels > 0 && b[j] - a[j] > kIndexMin) b[j] = a[j] = lower_bound_ts(p, a[j], b[j], x[j]);
     while (true) {
         bool live = false;
         float v[4];
@@ -170,8 +169,6 @@ __device__ __forceinline__ void lower_bound_multi(const SampleParams& p, uint32_
             }
         }
     }
-#pragma unroll
-    for (int j = 0; j < 4; ++j) out[j] = a[j];
 }
 
 __device__ __forceinline__ uint32_t warp_incl_scan(uint32_t x, int lane) {
@@ -212,30 +209,90 @@ __global__ void __launch_bounds__(kTile) window_kernel(const __grid_constant__ S
     }
     float lin = -INFINITY;
     if (p.layer > 0 && p.root_lo && ok) lin = p.root_lo[i];
-    uint32_t lo = 0, hi = 0;
-    float ts_first = INFINITY, ts_last = INFINITY;  // INFINITY: unknown / no shortcut
-    if (ok) {
-        if (p.nodes) {  // one 16-byte load: bounds + time span of the list
-            const int4 nr = __ldg(p.nodes + v);
-            lo = (uint32_t)nr.x;
-            hi = (uint32_t)nr.y;
-            ts_first = __int_as_float(nr.z);
-            ts_last = __int_as_float(nr.w);
-        } else {
+    // the cut times searched through the fences: all S+1 cuts of a layer-0 root with finite t_s and
+    // S <= 3 (c_0 = t, c_j = t (-) (j (x) t_s)); otherwise U = t and the first window's lower bound
+    const bool multi = nsb <= 3 && p.layer == 0 && isfinite(p.snapshot_len);
+    auto cuts_of = [&](float tr, float lr, float (&x)[4]) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            if (multi)
+                x[j] = j == 0 ? tr : (j <= nsb ? __fsub_rn(tr, __fmul_rn((float)j, p.snapshot_len)) : -INFINITY);
+            else
+                x[j] = j == 0 ? tr : (j == 1 ? (p.layer == 0 ? __fsub_rn(tr, p.snapshot_len) : lr) : -INFINITY);
+        }
+    };
+    float x[4];
+    cuts_of(t, lin, x);
+    uint32_t lo = 0, hi = 0, ga[4], gb[4];  // cut j lies in [ga[j], gb[j]]
+    bool early;                             // some slot is earlier than t: the list must be searched
+    if (p.nodes) {
+        // 4 lanes read one 64-byte node record (one request per record): rounds q = 0..3 cover the
+        // warp's roots q*8 .. q*8+7; per round each quad counts its fences below the root's cut
+        // times and hands lo, hi and the counts to the root's lane
+        int4 ch[4];
+        const int quad = lane >> 2, part = lane & 3;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int src = q * 8 + quad;
+            const int vq = __shfl_sync(kFull, v, src);
+            const bool okq = __shfl_sync(kFull, ok, src);
+            ch[q] = okq ? __ldg(p.nodes + (size_t)vq * 4 + part)
+                        : make_int4(part ? 0x7f800000 : 0, part ? 0x7f800000 : 0, 0x7f800000, 0x7f800000);
+        }
+        uint32_t packed = 0;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int src = q * 8 + quad;
+            float xq[4];
+            cuts_of(__shfl_sync(kFull, t, src), __shfl_sync(kFull, lin, src), xq);
+            const float f[4] = {__int_as_float(ch[q].x), __int_as_float(ch[q].y), __int_as_float(ch[q].z),
+                                __int_as_float(ch[q].w)};
+            uint32_t c = 0;
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                if (part == 0 && e < 2) continue;  // lo, hi
+#pragma unroll
+                for (int j = 0; j < 4; ++j) c += (f[e] < xq[j] ? 1u : 0u) << (8 * j);
+            }
+            c += __shfl_xor_sync(kFull, c, 1);
+            c += __shfl_xor_sync(kFull, c, 2);
+            const int from = 4 * (lane & 7);  // lane q*8 + g takes quad g's result
+            const uint32_t cq = __shfl_sync(kFull, c, from);
+            const uint32_t loq = (uint32_t)__shfl_sync(kFull, ch[q].x, from);
+            const uint32_t hiq = (uint32_t)__shfl_sync(kFull, ch[q].y, from);
+            if ((lane >> 3) == q) {
+                packed = cq;
+                lo = loq;
+                hi = hiq;
+            }
+        }
+        const uint32_t d = hi - lo;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int m = (int)((packed >> (8 * j)) & 0xffu);
+            ga[j] = m ? fence_pos(lo, d, m - 1) + 1 : lo;
+            gb[j] = m < kFences ? fence_pos(lo, d, m) : hi;
+        }
+        early = (packed & 0xffu) != 0;  // f[0] = the first edge time < t
+    } else {
+        if (ok) {
             lo = (uint32_t)__ldg(p.indptr + v);
             hi = (uint32_t)__ldg(p.indptr + v + 1);
-            if (lo < hi) ts_first = __ldg(p.ts + lo);
+        }
+        early = lo < hi && __ldg(p.ts + lo) < t;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            ga[j] = lo;
+            gb[j] = x[j] > -INFINITY ? hi : lo;
         }
     }
-    // U of window 0 is the root's own time t; a list starting at or after t has no candidate
-    const bool early = lo < hi && ts_first < t;
-    if (nsb <= 3 && p.layer == 0 && isfinite(p.snapshot_len)) {
-        // all S+1 cuts at once: c_0 = t, c_{b+1} = t (-) ((b+1) (x) t_s)
-        float x[4];
+    if (multi) {
         uint32_t cut[4] = {lo, lo, lo, lo};
+        if (early) {
+            lower_bound_multi(p, ga, gb, x);
 #pragma unroll
-        for (int j = 0; j < 4; ++j) x[j] = j == 0 ? t : __fsub_rn(t, __fmul_rn((float)j, p.snapshot_len));
-        if (early) lower_bound_multi(p, lo, hi, p.nodes ? ts_last : INFINITY, nsb + 1, x, cut);
+            for (int j = 0; j < 4; ++j) cut[j] = ga[j];
+        }
 #pragma unroll
         for (int b = 0; b < 3; ++b) {
             if (b >= nsb) break;
@@ -251,13 +308,17 @@ __global__ void __launch_bounds__(kTile) window_kernel(const __grid_constant__ S
             if (lane == 0) s_red[b][warp] = s2;
         }
     } else {
-        uint32_t bcur = early ? lower_bound_ts(p, lo, hi, t) : lo;
+        uint32_t bcur = early ? lower_bound_ts(p, ga[0], gb[0], t) : lo;
         for (int b = 0; b < nsb; ++b) {
             // lower bound of window b: layer 0 -> t (-) ((b+1) (x) t_s); l >= 1 -> inherited
-            const float x = p.layer == 0 ? __fsub_rn(t, __fmul_rn((float)(b + 1), p.snapshot_len)) : lin;
+            const float xb = p.layer == 0 ? __fsub_rn(t, __fmul_rn((float)(b + 1), p.snapshot_len)) : lin;
             uint32_t a = lo;
-            if (x > -INFINITY && bcur > lo)  // empty window when the element before the cut is < x
-                a = __ldg(p.ts + bcur - 1) < x ? bcur : lower_bound_ts(p, lo, bcur - 1, x);
+            if (xb > -INFINITY && bcur > lo) {  // empty window when the element before the cut is < x
+                if (b == 0)                      // the first lower bound's fence gap (x[1] = xb)
+                    a = min(lower_bound_ts(p, min(ga[1], bcur), min(gb[1], bcur), xb), bcur);
+                else
+                    a = __ldg(p.ts + bcur - 1) < xb ? bcur : lower_bound_ts(p, lo, bcur - 1, xb);
+            }
             const uint32_t c = bcur - a;
             const uint32_t take = c < k ? c : k;
             if (valid) {

@@ -58,14 +58,22 @@ struct SlotRec {
 };
 static_assert(sizeof(SlotRec) == 16, "slot record is one 16-byte vector");
 
-// Per-node 16-byte record {lo, hi, ts_first, ts_last}: one load gives the list bounds AND its time
-// span, so a root whose list starts at or after its time (or ends before it) needs no list access,
-// and the others start searching one dependent DRAM step earlier than indptr -> ts[lo].
+// Per-node 64-byte record {lo, hi, f[0..13]}: the list bounds and 14 "fences" -- the ts of the
+// slots P_j = lo + floor(j (d-1) / 13), j = 0..13 (f[0] = first, f[13] = last edge time; +inf for
+// an empty list).  One 64-byte read (one DRAM atom, read by 4 cooperating lanes) gives the bounds
+// AND narrows every cut to one gap between consecutive fences: with m = #fences < x, the lower
+// bound lies in [P_(m-1) + 1, P_m] -- for d <= 14 the fences are the whole list (no list access at
+// all), for d <= 53 at most 3 slots remain (one 64-byte group of ts).
+constexpr int kFences = 14;
 struct NodeRec {
     uint32_t lo, hi;
-    float ts_first, ts_last;  // +inf / -inf for an empty list
+    float f[kFences];
 };
-static_assert(sizeof(NodeRec) == 16, "node record is one 16-byte vector");
+static_assert(sizeof(NodeRec) == 64, "node record is one 64-byte DRAM atom");
+
+__host__ __device__ inline uint32_t fence_pos(uint32_t lo, uint32_t d, int j) {
+    return lo + (uint32_t)(((uint64_t)j * (uint64_t)(d - 1)) / (uint64_t)(kFences - 1));
+}
 
 struct AuxLayout {
     IndexLayout index;

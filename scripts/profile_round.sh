@@ -4,7 +4,7 @@ tag=${1:-r01}
 mkdir -p gpurun_out/$tag
 python bench.py > gpurun_out/$tag/bench.json 2> gpurun_out/$tag/bench.err
 ncu --metrics gpu__time_duration.sum --clock-control none \
-    -k regex:'window_kernel|copy_kernel|tile_scan|radix|scan_|validate|aux_build|gather' \
+    -k regex:'window_kernel|copy_kernel|radix|scan_|validate|aux_build|gather' \
     --csv --log-file gpurun_out/$tag/launches.csv \
     python bench.py --steps 5 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/$tag/launches_bench.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:'window_kernel|copy_kernel' -s 6 -c 2 \

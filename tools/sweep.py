@@ -1,8 +1,8 @@
 """Tuning sweep for the sampler on one config (default C5): times tgl_sample per setting.
 
 python tools/sweep.py [--config C5] [--roots 1048576] [--reps 10]
-Settings are the library's environment knobs (TGL_CHUNK_ROOTS, TGL_LANES_PER_ROOT, TGL_PREFETCH,
-TGL_NO_PAYLOAD) plus the no-aux (plain binary search) handle.  Prints one JSON line per setting.
+Settings are the library's experiment knobs (TGL_NO_STAGE, TGL_NO_RECS, TGL_NO_INDEX) plus the
+no-aux (plain binary search) handle.  Prints one JSON line per setting.
 """
 import argparse
 import itertools
@@ -35,7 +35,7 @@ torch.cuda.empty_cache()
 
 
 def run(handle, env):
-    for k in ("TGL_NO_RECS", "TGL_NO_INDEX"):
+    for k in [k for k in os.environ if k.startswith("TGL_") and k != "TGL_LIB_PATH"]:
         os.environ.pop(k, None)
     os.environ.update({k: str(v) for k, v in env.items()})
     smp = tgl.Sampler(handle, args.roots, cfg.fanouts, cfg.strategy, cfg.n_snapshots, cfg.snapshot_len)
@@ -56,15 +56,8 @@ def run(handle, env):
     return ms, edges / args.reps
 
 
-settings = []
-for recs, idx in itertools.product([1, 0], [1, 0]):
-    env = {}
-    if not recs:
-        env["TGL_NO_RECS"] = 1
-    if not idx:
-        env["TGL_NO_INDEX"] = 1
-    settings.append(("aux", env))
-settings.append(("plain", {}))
+settings = [("aux", {}), ("aux", {"TGL_NO_STAGE": 1}), ("aux", {"TGL_NO_RECS": 1}),
+            ("aux", {"TGL_NO_INDEX": 1}), ("plain", {})]
 if args.only:
     env = dict(kv.split("=") for kv in args.only.split(","))
     settings = [("plain" if env.pop("handle", "aux") == "plain" else "aux", env)]
