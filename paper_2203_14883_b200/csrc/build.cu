@@ -246,9 +246,15 @@ __global__ void aux_build_kernel(const int64_t* __restrict__ indptr, const float
         for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < lay.index.len[l]; j += stride)
             out[j] = ts[j << sh];
     }
-    int4* rec = reinterpret_cast<int4*>(aux + lay.rec_off);
-    for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += stride)
-        rec[j] = make_int4(__float_as_int(ts[j]), nbr[j], eid[j], 0);
+    SlotRec* rec = reinterpret_cast<SlotRec*>(aux + lay.rec_off);
+    for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += stride) {
+        SlotRec r;
+        memset(&r, 0, sizeof(r));
+        r.ts = ts[j];
+        r.nbr = nbr[j];
+        r.eid = eid[j];
+        rec[j] = r;
+    }
     // node records: thread (v, q) writes the q-th 16-byte quarter of node v's record
     int4* node = reinterpret_cast<int4*>(aux + lay.node_off);
     for (uint64_t w = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; w < n_nodes * 4; w += stride) {

@@ -35,6 +35,12 @@
 
 namespace tgl {
 
+#ifndef TGL_WINDOW_MINB
+#define TGL_WINDOW_MINB 8
+#endif
+#ifndef TGL_COPY_MINB
+#define TGL_COPY_MINB 6
+#endif
 constexpr int kTile = 256;  // roots per tile (one lane per root)
 constexpr int kWarps = kTile / 32;
 constexpr int kCopyUnroll = 2;
@@ -59,7 +65,7 @@ struct SampleParams {
     const int32_t* nbr;
     const float* ts;
     const int32_t* eid;
-    const int4* recs;                       // 16-byte slot records {ts, nbr, eid, 0}, or null
+    const SlotRec* recs;                    // slot records {ts, nbr, eid[, 0]} (tsindex.cuh), or null
     const int4* nodes;                      // 64-byte node records {lo, hi, 14 fences} (tsindex.cuh), or null
     const float* lvl[kMaxIndexLevels + 1];  // lvl[l] = index level l (1-based)
     int32_t n_levels;                       // 0 -> no index
@@ -182,11 +188,12 @@ __device__ __forceinline__ uint32_t warp_incl_scan(uint32_t x, int lane) {
 
 // ---------------------------------------------------------------------------- K4a windows
 template <int STRATEGY>
-__global__ void __launch_bounds__(kTile) window_kernel(const __grid_constant__ SampleParams p) {
+__global__ void __launch_bounds__(kTile, TGL_WINDOW_MINB) window_kernel(const __grid_constant__ SampleParams p) {
     __shared__ uint32_t s_red[TGL_MAX_SNAPSHOTS][kWarps];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int64_t n = chain_roots(p);
-    const int64_t base_i = (int64_t)blockIdx.x * kTile;
+    const int64_t tile = (int64_t)blockIdx.x;
+    const int64_t base_i = tile * kTile;
     if (base_i >= n) return;  // capacity-sized grid (l >= 1): tiles past the end do nothing
     const int64_t i = base_i + threadIdx.x;
     const bool valid = i < n;
@@ -299,8 +306,10 @@ __global__ void __launch_bounds__(kTile) window_kernel(const __grid_constant__ S
             const uint32_t c = cut[b] - cut[b + 1];
             const uint32_t take = c < k ? c : k;
             if (valid) {
-                p.win_first[(size_t)b * p.roots_cap + i] = STRATEGY == TGL_MOST_RECENT ? cut[b] - take : cut[b + 1];
-                p.win_len[(size_t)b * p.roots_cap + i] = STRATEGY == TGL_MOST_RECENT ? take : c;
+                const uint32_t wf = STRATEGY == TGL_MOST_RECENT ? cut[b] - take : cut[b + 1];
+                const uint32_t wl = STRATEGY == TGL_MOST_RECENT ? take : c;
+                p.win_first[(size_t)b * p.roots_cap + i] = wf;
+                p.win_len[(size_t)b * p.roots_cap + i] = wl;
             }
             uint32_t s2 = take;
 #pragma unroll
@@ -337,9 +346,9 @@ __global__ void __launch_bounds__(kTile) window_kernel(const __grid_constant__ S
         uint32_t s = 0;
 #pragma unroll
         for (int w = 0; w < kWarps; ++w) s += s_red[threadIdx.x][w];
-        p.tile_tot[(size_t)threadIdx.x * p.tiles_cap + blockIdx.x] = s;
+        p.tile_tot[(size_t)threadIdx.x * p.tiles_cap + tile] = s;
         atomicAdd(reinterpret_cast<unsigned long long*>(p.super_tot + (size_t)threadIdx.x * p.supers_cap +
-                                                        (blockIdx.x >> kSuperShift)),
+                                                        (tile >> kSuperShift)),
                   (unsigned long long)s);
     }
 }
@@ -350,15 +359,16 @@ __host__ __device__ inline int copy_warp_words(int nsb, int k, bool picks_in_sme
 }
 
 template <int STRATEGY>
-__global__ void __launch_bounds__(kTile, 6) copy_kernel(const __grid_constant__ SampleParams p) {
+__global__ void __launch_bounds__(kTile, TGL_COPY_MINB) copy_kernel(const __grid_constant__ SampleParams p) {
     extern __shared__ __align__(16) uint32_t smem[];
     __shared__ uint32_t s_wsum[TGL_MAX_SNAPSHOTS][kWarps];
     __shared__ uint64_t s_tbase[TGL_MAX_SNAPSHOTS];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int64_t n = chain_roots(p);
-    const int64_t base_i = (int64_t)blockIdx.x * kTile;
+    const int64_t tile = (int64_t)blockIdx.x;
+    const int64_t base_i = tile * kTile;
     if (n == 0) {  // empty chain: the first CTA writes the empty blocks
-        if (blockIdx.x == 0 && threadIdx.x < p.nsb) {
+        if (tile == 0 && threadIdx.x < p.nsb) {
             p.out[threadIdx.x].offsets[0] = 0;
             *p.out[threadIdx.x].nnz_dev = 0;
             *p.out[threadIdx.x].n_roots_dev = 0;
@@ -380,7 +390,7 @@ __global__ void __launch_bounds__(kTile, 6) copy_kernel(const __grid_constant__ 
     uint32_t* picks = nullptr;
     if (STRATEGY == TGL_UNIFORM)
         picks = picks_smem ? reinterpret_cast<uint32_t*>(base + nsb)
-                           : p.picks_global + ((size_t)blockIdx.x * kWarps + warp) * nsb * k * 32;
+                           : p.picks_global + ((size_t)tile * kWarps + warp) * nsb * k * 32;
 
     const float t = valid ? p.root_ts[i] : 0.0f;
     troot[lane] = t;
@@ -432,7 +442,7 @@ __global__ void __launch_bounds__(kTile, 6) copy_kernel(const __grid_constant__ 
     // tile base per snapshot: warp b sums the super totals before this tile's super tile and the
     // tile totals before this tile inside it (all final: the window kernel has completed)
     for (int b = warp; b < nsb; b += kWarps) {
-        const int64_t t = blockIdx.x, sup = t >> kSuperShift;
+        const int64_t t = tile, sup = t >> kSuperShift;
         uint64_t acc = 0;
         for (int64_t q = lane; q < sup; q += 32) acc += p.super_tot[(size_t)b * p.supers_cap + q];
         for (int64_t q = (sup << kSuperShift) + lane; q < t; q += 32) acc += p.tile_tot[(size_t)b * p.tiles_cap + q];
@@ -490,8 +500,14 @@ __global__ void __launch_bounds__(kTile, 6) copy_kernel(const __grid_constant__ 
 #pragma unroll
             for (int u = 0; u < kCopyUnroll; ++u) {
                 if (act[u]) {
-                    if (p.recs)
-                        rec[u] = __ldg(p.recs + pos[u]);
+                    if (p.recs) {
+#if TGL_REC_WORDS == 4
+                        rec[u] = __ldg(reinterpret_cast<const int4*>(p.recs) + pos[u]);
+#else
+                        const int* w = reinterpret_cast<const int*>(p.recs + pos[u]);
+                        rec[u] = make_int4(__ldg(w), __ldg(w + 1), __ldg(w + 2), 0);
+#endif
+                    }
                     else
                         rec[u] = make_int4(__float_as_int(__ldg(p.ts + pos[u])), __ldg(p.nbr + pos[u]),
                                            __ldg(p.eid + pos[u]), 0);
@@ -652,7 +668,7 @@ static int sample_impl(const tgl_tcsr* g, const int32_t* roots, const float* roo
         sp.nbr = g->nbr;
         sp.ts = g->ts;
         sp.eid = g->eid;
-        sp.recs = use_recs ? static_cast<const int4*>(g->recs) : nullptr;
+        sp.recs = use_recs ? static_cast<const SlotRec*>(g->recs) : nullptr;
         sp.nodes = use_recs ? static_cast<const int4*>(g->nodes) : nullptr;
         sp.n_levels = use_index ? g->n_levels : 0;
         for (int q = 1; q <= sp.n_levels; ++q) sp.lvl[q] = g->index + g->level_off[q];
@@ -703,11 +719,11 @@ static int sample_impl(const tgl_tcsr* g, const int32_t* roots, const float* roo
             bo.n_roots_dev = ob.n_roots_dev;
             bo.nnz_dev = ob.nnz_dev;
         }
-        const int64_t grid = l == 0 ? std::max<int64_t>(1, (n_roots + kTile - 1) / kTile) : la.tiles_cap;
+        const int64_t tiles = l == 0 ? std::max<int64_t>(1, (n_roots + kTile - 1) / kTile) : la.tiles_cap;
         const size_t smem =
             (size_t)kWarps * copy_warp_words(la.nsb, sp.k, strategy == TGL_UNIFORM && la.picks == nullptr) * 4;
-        rc = strategy == TGL_UNIFORM ? launch_chain<TGL_UNIFORM>(sp, grid, smem, st)
-                                     : launch_chain<TGL_MOST_RECENT>(sp, grid, smem, st);
+        rc = strategy == TGL_UNIFORM ? launch_chain<TGL_UNIFORM>(sp, tiles, smem, st)
+                                     : launch_chain<TGL_MOST_RECENT>(sp, tiles, smem, st);
         if (rc) return rc;
     }
     return TGL_OK;

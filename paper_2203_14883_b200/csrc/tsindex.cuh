@@ -50,13 +50,19 @@ inline IndexLayout index_layout(uint64_t n_stored) {
 // 16-byte {ts, nbr, eid, 0} of one T-CSR slot, so the cut search and the payload copy of the
 // selected slots read the SAME lines: one DRAM row activation per list instead of one per array
 // (HBM serves ~33 G random requests/s).
+#ifndef TGL_REC_WORDS
+#define TGL_REC_WORDS 4
+#endif
+constexpr int kRecWords = TGL_REC_WORDS;  // 4: {ts, nbr, eid, 0} (one 16-byte vector); 3: packed
 struct SlotRec {
     float ts;
     int32_t nbr;
     int32_t eid;
+#if TGL_REC_WORDS == 4
     int32_t pad;
+#endif
 };
-static_assert(sizeof(SlotRec) == 16, "slot record is one 16-byte vector");
+static_assert(sizeof(SlotRec) == 4 * kRecWords, "slot record size");
 
 // Per-node 64-byte record {lo, hi, f[0..13]}: the list bounds and 14 "fences" -- the ts of the
 // slots P_j = lo + floor(j (d-1) / 13), j = 0..13 (f[0] = first, f[13] = last edge time; +inf for

@@ -21,6 +21,7 @@ ap.add_argument("--config", default="C5")
 ap.add_argument("--roots", type=int, default=1 << 20)
 ap.add_argument("--reps", type=int, default=10)
 ap.add_argument("--only", default="", help="comma list k=v of one setting to run (e.g. for ncu)")
+ap.add_argument("--settings", default="", help="JSON list of env dicts (aux handle) to run instead")
 args = ap.parse_args()
 cfg = C.CONFIGS[args.config]
 src, dst, ts = C.edges(args.config, cfg, device="cuda")
@@ -58,6 +59,8 @@ def run(handle, env):
 
 settings = [("aux", {}), ("aux", {"TGL_NO_STAGE": 1}), ("aux", {"TGL_NO_RECS": 1}),
             ("aux", {"TGL_NO_INDEX": 1}), ("plain", {})]
+if args.settings:
+    settings = [("aux", e) for e in json.loads(args.settings)]
 if args.only:
     env = dict(kv.split("=") for kv in args.only.split(","))
     settings = [("plain" if env.pop("handle", "aux") == "plain" else "aux", env)]
