@@ -162,6 +162,27 @@ def rank_chunks(n_epoch_roots: int, chunk: int, steps_total: int, world: int, ra
     return [starts[c * world + rank] for c in range(steps_total)]
 
 
+def measured_traffic(key: str, roots_per_step: float):
+    """DRAM bytes per step of the sampler kernels from the committed ncu --set full capture
+    (tools/ncu_traffic.py: dram__bytes_read.sum + dram__bytes_write.sum per root of the captured
+    launches, x this step's roots).  TGL_TRAFFIC_JSON overrides the newest profiles/r*/traffic.json."""
+    import glob
+    path = os.environ.get("TGL_TRAFFIC_JSON")
+    if not path:
+        cands = sorted(glob.glob(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r*",
+                                              "traffic.json")))
+        path = cands[-1] if cands else None
+    if not path or not os.path.exists(path):
+        return None, None
+    d = json.load(open(path)).get(key)
+    if not d:
+        return None, None
+    src = (f"{os.path.relpath(path, os.path.dirname(os.path.abspath(__file__)))}: ncu --set full "
+           f"({d['capture']}, {d['roots']:,} roots per launch), DRAM read + write of "
+           f"{' + '.join(sorted(d['kernels']))} = {d['bytes_per_root']:.1f} B per root x roots per step")
+    return d["bytes_per_root"] * roots_per_step, src
+
+
 def reduce_report(edges: float, nbytes: float, ms: float, world: int, dev):
     """Reporting only (outside the timed region): sum of work over ranks, max of device time."""
     if world == 1:
@@ -180,6 +201,100 @@ def setup_graph(key: str, cfg: C.Workload, dev):
     torch.cuda.synchronize(dev)
     gen_s = time.time() - t0
     return src, dst, ts, gen_s
+
+
+# ----------------------------------------------------------------------------- node-sharded mode
+def run_node_sharded(args):
+    """SURVEY 8(e) node-sharded T-CSR: each rank keeps the edge-balanced node range [splits[r],
+    splits[r+1]) (sliced from a full build, which is then freed) and samples its own root chunks
+    through the exchange protocol of paper_2203_14883_b200.sharded: owner bucketing (K8), NCCL
+    all-to-all-v of requests, tgl_sample_keyed on the shard with the roots' global keys (so the
+    bits equal the replicated mode), all-to-all-v of replies, un-permute (K8b).  1 layer (C5)."""
+    import paper_2203_14883_b200 as tgl
+    from paper_2203_14883_b200 import sharded as sh
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    import torch.distributed as dist
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    key = args.config
+    cfg = C.CONFIGS[key]
+    if len(cfg.fanouts) != 1:
+        raise SystemExit("node-sharded mode: single-layer configs only (C1, C3, C5)")
+    B = cfg.batch
+    chunk = args.batches * B
+    src, dst, ts, gen_s = setup_graph(key, cfg, dev)
+    g = tgl.build(src, dst, ts, n_nodes=cfg.n_nodes, add_reverse=cfg.add_reverse, with_index=False)
+    splits = sh.edge_balanced_splits(g.indptr, world)
+    lo, hi = int(splits[rank]), int(splits[rank + 1])
+    shard = sh.slice_shard(g, lo, hi)
+    del g
+    torch.cuda.empty_cache()
+    n_distinct = max(1, min(args.warmup + args.steps, args.distinct))
+    mine = rank_chunks(cfg.n_roots_epoch, chunk, n_distinct, world, rank, B)
+    chunks = [C.roots(cfg, src, dst, ts, s0, chunk) for s0 in mine]
+    del src, dst, ts
+    torch.cuda.empty_cache()
+    ops = sh.CudaOps(shard, cfg.fanouts[0], cfg.strategy, cfg.n_snapshots, cfg.snapshot_len, world * chunk)
+    ex = sh.DistExchange() if world > 1 else _SelfExchange()
+    smp = sh.NodeShardedSampler(splits.to(dev), ex, ops, cfg.n_snapshots, cfg.sampler_seed)
+
+    def step(j):
+        r, t = chunks[j % n_distinct]
+        return smp.run(r, t, mine[j % n_distinct])
+
+    for w in range(args.warmup):
+        step(w)
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    clocks = ClockSampler(local)
+    edges = 0
+    with clocks:
+        e0.record()
+        for j in range(args.steps):
+            blocks = step(args.warmup + j)
+            edges += sum(int(b.offsets[-1].item()) for b in blocks)
+        e1.record()
+        torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    ms = e0.elapsed_time(e1)
+    tot = torch.tensor([float(edges)], dtype=torch.float64, device=dev)
+    mx = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(tot)
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+    out = {"metric": METRIC, "value": float(tot[0]) / (float(mx[0]) / 1e3), "unit": UNIT, "n_gpus": world,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": float(mx[0]) / args.steps,
+           "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+           "config": {"workload": f"{key} {cfg.name}", "batch_roots": B, "batches_per_step": args.batches,
+                      "roots_per_step_per_gpu": chunk,
+                      "parallelism": f"node-sharded T-CSR over {world} rank(s), edge-balanced node ranges; "
+                                     "requests/replies by all-to-all-v (NCCL)",
+                      "shard_nodes": hi - lo, "shard_edges": int(shard.n_stored),
+                      "l2": "no flush: shard and per-step roots exceed L2"},
+           "clocks": clocks.summary(), "generate_s": gen_s,
+           "note": "the timed step includes the host-synchronising count exchanges of the protocol"}
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+class _SelfExchange:
+    """world = 1: the all-to-all-v of one rank is the identity."""
+    world, rank = 1, 0
+
+    def splits(self, send_counts):
+        return send_counts.clone()
+
+    def exchange(self, t, send_splits, recv_splits):
+        return t
 
 
 # ----------------------------------------------------------------------------- oracle (CPU) side
@@ -205,7 +320,26 @@ def oracle_sample_rate(cfg, src, dst, ts, roots_list, key_bases, budget_s=None):
         outs.append(blocks)
         if budget_s is not None and secs > budget_s:
             break
-    return {"edges": nnz, "roots": n_roots, "seconds": secs, "outs": outs, "batches": len(outs)}
+    res = {"edges": nnz, "roots": n_roots, "seconds": secs, "outs": outs, "batches": len(outs)}
+    # "oracle x N threads": the same batches over all host cores.  The sampler is
+    # stateless per root and ctypes releases the GIL in the C call, so threads give identical bits.
+    from concurrent.futures import ThreadPoolExecutor
+    n_thr = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
+    todo = list(zip(host, key_bases))[:len(outs)]
+
+    def one(item):
+        (r, t), base = item
+        return oracle.sample(go, r, t, fanouts=cfg.fanouts, strategy=strat, n_snapshots=cfg.n_snapshots,
+                             snapshot_len=cfg.snapshot_len, seed=cfg.sampler_seed, root_key_base=base)
+    t0 = time.perf_counter()
+    with ThreadPoolExecutor(n_thr) as ex:
+        par = list(ex.map(one, todo))
+    psecs = time.perf_counter() - t0
+    same = all(np.array_equal(a["nbr"], b["nbr"]) and np.array_equal(a["dt"].view(np.uint32), b["dt"].view(np.uint32))
+               for xs, ys in zip(par, outs) for a, b in zip(xs, ys))
+    res["threads"] = {"value": nnz / psecs, "unit": UNIT, "cores": n_thr, "seconds": psecs,
+                      "identical_to_single_thread": bool(same)}
+    return res
 
 
 # ----------------------------------------------------------------------------- our arm
@@ -237,8 +371,12 @@ def run_ours(args):
     torch.cuda.empty_cache()
 
     # root chunks of this rank: chunk index c*world + rank, spread over the epoch
-    mine = rank_chunks(cfg.n_roots_epoch, chunk, args.warmup + args.steps, world, rank, B)
+    # (at most --distinct different chunks, cycled: a chunk's footprint is GBs, far beyond L2)
+    n_distinct = max(1, min(args.warmup + args.steps, args.distinct))
+    mine = rank_chunks(cfg.n_roots_epoch, chunk, n_distinct, world, rank, B)
     chunks = [C.roots(cfg, src, dst, ts, s0, chunk) for s0 in mine]
+    mine = [mine[j % n_distinct] for j in range(args.warmup + args.steps)]
+    chunks = [chunks[j % n_distinct] for j in range(args.warmup + args.steps)]
     sampler = tgl.Sampler(g, chunk, cfg.fanouts, cfg.strategy, cfg.n_snapshots, cfg.snapshot_len)
     L, S = len(cfg.fanouts), cfg.n_snapshots
     launches_per_step = 2 * (1 + (L - 1) * S)  # window + copy kernel per chain (+1 memset, not ours)
@@ -301,6 +439,7 @@ def run_ours(args):
     # dominant kernel = the sampler kernel (one launch per step for 1-layer configs); the per-step
     # events bracket tgl_sample = one small memset of the look-back state + the kernel(s)
     kern_ms = float(np.mean(step_ms))
+    traffic, traffic_src = measured_traffic(key, roots_total / args.steps) if gather is None else (None, None)
     achieved = (bytes_total / args.steps) / (kern_ms / 1e3) / 1e9
     out = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -312,9 +451,10 @@ def run_ours(args):
                                f"{'' if not math.isfinite(cfg.snapshot_len) else f' of {cfg.snapshot_len:g}'}",
                    "batch_roots": B, "batches_per_step": M, "roots_per_step_per_gpu": chunk,
                    "parallelism": f"root-sharded dp{world}, replicated T-CSR",
-                   "l2": "no flush: T-CSR and per-step roots exceed L2 (126 MB); every step's roots are distinct"},
+                   "l2": ("no flush: T-CSR and per-step roots exceed L2 (126 MB); "
+                          f"{n_distinct} distinct root chunks cycled over the steps")},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": None, "peak_source": peak_src,
+                     "traffic": traffic, "traffic_source": traffic_src, "peak_source": peak_src,
                      "kernel": (f"tgl_sample ({cfg.strategy}): window_kernel + copy_kernel"
                                 + (" + tgl_gather (3 launches)" if gather is not None else "") + ", timed together"),
                      "bytes_model": "SURVEY 8(d): per root 8+16+8*cuts+8*S, per edge 24 (+4 ts_edge if l<L-1)"
@@ -331,6 +471,11 @@ def run_ours(args):
         "device_error": int(err),
     }
 
+    # per-batch mode (SURVEY 8(d) mode 1): one tgl_sample call per batch, replayed as a CUDA graph
+    if not args.no_per_batch:
+        mid = n_distinct // 2  # a chunk from the middle of the epoch (early batches have short histories)
+        out["per_batch"] = per_batch(args, tgl, g, cfg, chunks[mid], mine[mid], dev, world)
+
     # end to end through the public API with host buffers (rank-local), copies inside the region
     if not args.no_e2e:
         gf = (lambda smp: make_gather(tgl, cfg, smp, dev)) if gather is not None else None
@@ -346,6 +491,55 @@ def run_ours(args):
         torch.distributed.destroy_process_group()
 
 
+def per_batch(args, tgl, g, cfg, chunk, key0, dev, world, n_graph=64, reps=10):
+    """Latency mode: n_graph consecutive batches, one tgl_sample call each (batch b's roots, key base
+    = its global root index), captured once as a CUDA graph and replayed; device time per batch =
+    replay time / n_graph (CUDA events, max over ranks).  Edges counted from an eager re-run."""
+    B = cfg.batch
+    r, t = chunk
+    n_graph = max(1, min(n_graph, r.numel() // B))
+    smp = tgl.Sampler(g, B, cfg.fanouts, cfg.strategy, cfg.n_snapshots, cfg.snapshot_len)
+    L, S = len(cfg.fanouts), cfg.n_snapshots
+
+    def calls():
+        for j in range(n_graph):
+            smp.run(r[j * B:(j + 1) * B], t[j * B:(j + 1) * B], seed=cfg.sampler_seed, root_key_base=key0 + j * B)
+
+    edges = 0
+    for j in range(n_graph):  # eager pass: warm-up + the work count
+        blocks = smp.run(r[j * B:(j + 1) * B], t[j * B:(j + 1) * B], seed=cfg.sampler_seed,
+                         root_key_base=key0 + j * B)
+        edges += sum(int(blocks[q].nnz_dev.item()) for q in range(L * S))
+    side = torch.cuda.Stream()
+    side.wait_stream(torch.cuda.current_stream())
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(side):
+        calls()  # warm-up on the capture stream
+        torch.cuda.synchronize(dev)
+        with torch.cuda.graph(graph, stream=side):
+            calls()
+    torch.cuda.synchronize(dev)
+    for _ in range(3):
+        graph.replay()
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        torch.distributed.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        graph.replay()
+    e1.record()
+    torch.cuda.synchronize(dev)
+    ms = e0.elapsed_time(e1)
+    edges_all, _, ms_max = reduce_report(edges * reps, 0.0, ms, world, dev)
+    launches = 2 * (1 + (L - 1) * S)
+    return {"batch_roots": B, "batches_per_graph": n_graph, "replays": reps, "graph": True,
+            "latency_us_per_batch": ms_max * 1e3 / (reps * n_graph),
+            "value": edges_all / (ms_max / 1e3), "unit": UNIT, "gpu_launches_per_batch": launches,
+            "note": "per-batch calls (batch-sized grids, under one wave) replayed as a CUDA graph: "
+                    "launch-latency bound; the headline value is epoch mode"}
+
+
 def e2e(args, tgl, sampler, chunks, mine, cfg, dev, world, full_d2h=False, gather_factory=None):
     """End to end through the public API with host buffers, copies inside the timed region.
 
@@ -356,7 +550,11 @@ def e2e(args, tgl, sampler, chunks, mine, cfg, dev, world, full_d2h=False, gathe
     Double-buffered: the H2D of step j+1 and the D2H of step j overlap the sampling of j+1 / j+1.
     """
     L, S = len(cfg.fanouts), cfg.n_snapshots
-    host = [(r.cpu().pin_memory(), t.cpu().pin_memory()) for r, t in chunks]
+    pinned = {}  # one pinned copy per distinct chunk (the step list cycles over them)
+    for r, t in chunks:
+        if id(r) not in pinned:
+            pinned[id(r)] = (r.cpu().pin_memory(), t.cpu().pin_memory())
+    host = [pinned[id(r)] for r, _ in chunks]
     cap_r = chunks[0][0].numel()
     nb = L * S
     smps = [sampler, tgl.Sampler(sampler.g, cap_r, cfg.fanouts, cfg.strategy, S, cfg.snapshot_len)]
@@ -480,7 +678,7 @@ def cpu_baseline(args, cfg, src, dst, ts, tgl, g, sampler, chunks, mine):
              "sample": f"{res['batches']} consecutive batches x {B} roots ({res['roots']:,} roots, "
                        f"{res['edges']:,} sampled edges) from timed step 0, single-threaded C oracle "
                        f"(-O2 -ffp-contract=off) on a T-CSR restricted to the sampled nodes",
-             "seconds": res["seconds"]},
+             "seconds": res["seconds"], "oracle_x_threads": res["threads"]},
             {"checked_roots": checked, "bit_exact": bool(ok), "against": "oracle/ (CPU), same batches"})
 
 
@@ -539,7 +737,7 @@ def run_reference(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="C5", choices=sorted(C.CONFIGS))
     ap.add_argument("--batches", type=int, default=0,
@@ -547,7 +745,11 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--ref-batches", type=int, default=16, help="reference arm: batches per step")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--distinct", type=int, default=32, help="distinct root chunks (cycled over the steps)")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-per-batch", action="store_true")
+    ap.add_argument("--sharding", default="root", choices=["root", "node"],
+                    help="root: replicated T-CSR, roots sharded (default); node: node-sharded T-CSR (SURVEY 8(e))")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     if args.batches <= 0:
@@ -557,7 +759,7 @@ def main():
     if args.impl == "reference":
         run_reference(args)
     else:
-        run_ours(args)
+        run_node_sharded(args) if args.sharding == "node" else run_ours(args)
 
 
 if __name__ == "__main__":

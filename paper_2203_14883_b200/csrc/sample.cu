@@ -6,13 +6,14 @@
 // stream, with no inter-CTA waiting anywhere (measured faster on B200 than one fused kernel with a
 // decoupled look-back, whose tiles wait on slow predecessors: profiles/r01):
 //
-//   K4a window_kernel  one lane per root: indptr pair, S+1 cut searches (lower_bound) over the
-//                      node's time-sorted ts list -- the stateless replacement of the paper's
-//                      per-node pointers pt_0..pt_S (Sec. 3.1 "Sampling", L260-L262) -- through the
-//                      16-ary index (tsindex.cuh) for long lists.  Writes per (snapshot, root) the
-//                      window descriptor and per (snapshot, 256-root tile) the edge count:
-//                      most_recent -> min(k, c) "closest to the end pointer";
-//                      uniform -> min(k, c) (R#5).
+//   K4a window_kernel  one lane per root: node record (bounds + 14 fence timestamps, read by 4
+//                      cooperating lanes), S+1 cut searches (lower_bound) inside their fence gaps
+//                      of the node's time-sorted ts list -- the stateless replacement of the
+//                      paper's per-node pointers pt_0..pt_S (Sec. 3.1 "Sampling", L260-L262) --
+//                      through the 16-ary index (tsindex.cuh) for long gaps.  Writes per root the
+//                      S+1 cuts and per (snapshot, 256-root tile) the edge count min(k, c):
+//                      most_recent -> the min(k, c) "closest to the end pointer";
+//                      uniform -> a uniform min(k, c)-subset (R#5).
 //   (K5) tile bases   the window kernel also adds its tile totals into per-64-tile super totals
 //                      (integer atomics: order-independent, so deterministic); a copy CTA sums
 //                      the super totals and tile totals before it -- no scan kernel, no waiting.
@@ -43,7 +44,10 @@ namespace tgl {
 #endif
 constexpr int kTile = 256;  // roots per tile (one lane per root)
 constexpr int kWarps = kTile / 32;
-constexpr int kCopyUnroll = 2;
+#ifndef TGL_COPY_UNROLL
+#define TGL_COPY_UNROLL 2
+#endif
+constexpr int kCopyUnroll = TGL_COPY_UNROLL;  // outputs in flight per lane in the flat copy
 constexpr int kSuperShift = 6;  // 64 tiles per super tile (tile bases: super totals + tile totals)
 constexpr uint32_t kIndexMin = 256;          // lists longer than this descend the 16-ary index
 constexpr int kPicksSmemPerWarp = 8 * 1024;  // bytes of uniform picks kept in shared memory per warp
@@ -81,8 +85,7 @@ struct SampleParams {
     int32_t layer, nsb, snap0, k;
     float snapshot_len;
     uint32_t seed_lo, seed_hi;
-    uint32_t* win_first;  // [nsb][roots_cap] first slot (uniform: a; most_recent: b - take)
-    uint32_t* win_len;    // [nsb][roots_cap] uniform: window size c; most_recent: take = min(k, c)
+    uint32_t* cuts;  // [nsb+1][roots_cap] c_0 >= c_1 >= .. >= c_nsb: window b = slots [c_(b+1), c_b)
     uint32_t* tile_tot;    // [nsb][tiles_cap] edges emitted per 256-root tile
     uint64_t* super_tot;   // [nsb][supers_cap] per 64 tiles (integer atomics: order-independent), zeroed per call
     int64_t supers_cap;
@@ -306,10 +309,8 @@ __global__ void __launch_bounds__(kTile, TGL_WINDOW_MINB) window_kernel(const __
             const uint32_t c = cut[b] - cut[b + 1];
             const uint32_t take = c < k ? c : k;
             if (valid) {
-                const uint32_t wf = STRATEGY == TGL_MOST_RECENT ? cut[b] - take : cut[b + 1];
-                const uint32_t wl = STRATEGY == TGL_MOST_RECENT ? take : c;
-                p.win_first[(size_t)b * p.roots_cap + i] = wf;
-                p.win_len[(size_t)b * p.roots_cap + i] = wl;
+                if (b == 0) p.cuts[i] = cut[0];
+                p.cuts[(size_t)(b + 1) * p.roots_cap + i] = cut[b + 1];
             }
             uint32_t s2 = take;
 #pragma unroll
@@ -331,8 +332,8 @@ __global__ void __launch_bounds__(kTile, TGL_WINDOW_MINB) window_kernel(const __
             const uint32_t c = bcur - a;
             const uint32_t take = c < k ? c : k;
             if (valid) {
-                p.win_first[(size_t)b * p.roots_cap + i] = STRATEGY == TGL_MOST_RECENT ? bcur - take : a;
-                p.win_len[(size_t)b * p.roots_cap + i] = STRATEGY == TGL_MOST_RECENT ? take : c;
+                if (b == 0) p.cuts[i] = bcur;
+                p.cuts[(size_t)(b + 1) * p.roots_cap + i] = a;
             }
             uint32_t s2 = take;
 #pragma unroll
@@ -400,14 +401,14 @@ __global__ void __launch_bounds__(kTile, TGL_COPY_MINB) copy_kernel(const __grid
         rkey[lane] = rk;
     }
     // counts, warp-local prefix, window descriptors; uniform picks
+    uint32_t cb = valid ? p.cuts[i] : 0u;  // c_b
     for (int b = 0; b < nsb; ++b) {
-        uint32_t f = 0, len = 0;
-        if (valid) {
-            f = p.win_first[(size_t)b * p.roots_cap + i];
-            len = p.win_len[(size_t)b * p.roots_cap + i];
-        }
-        const uint32_t take = STRATEGY == TGL_MOST_RECENT ? len : (len < (uint32_t)k ? len : (uint32_t)k);
-        first[b * 32 + lane] = f;
+        const uint32_t cn = valid ? p.cuts[(size_t)(b + 1) * p.roots_cap + i] : 0u;  // c_(b+1)
+        const uint32_t len = cb - cn;                                                 // window size c
+        const uint32_t take = len < (uint32_t)k ? len : (uint32_t)k;
+        // most_recent: the take slots closest to the end pointer; uniform: picks from c_(b+1)
+        first[b * 32 + lane] = STRATEGY == TGL_MOST_RECENT ? cb - take : cn;
+        cb = cn;
         const uint32_t x = warp_incl_scan(take, lane);
         inc[b * 32 + lane] = x;
         if (lane == 31) s_wsum[b][warp] = x;
@@ -470,64 +471,73 @@ __global__ void __launch_bounds__(kTile, TGL_COPY_MINB) copy_kernel(const __grid
     __syncwarp();
 
     const int64_t warp_root0 = i - lane;  // global index of this warp's first root
-    for (int b = 0; b < nsb; ++b) {
-        const BlockOut& o = p.out[b];
-        const uint32_t* incb = inc + b * 32;
-        const uint32_t T = incb[31];
-        const uint64_t B = base[b];
-        const uint32_t* fb = first + b * 32;
-        for (uint32_t o0 = 0; o0 < T; o0 += 32 * kCopyUnroll) {
-            uint32_t pos[kCopyUnroll], rr[kCopyUnroll], qq[kCopyUnroll];
-            bool act[kCopyUnroll];
+    // flat copy over all snapshot blocks of the warp: output o -> block b (running over the warp's
+    // block totals) -> root r (5-step search of the block's inclusive counts) -> slot
+    uint32_t total = 0;
+    for (int b = 0; b < nsb; ++b) total += inc[b * 32 + 31];
+    for (uint32_t o0 = 0; o0 < total; o0 += 32 * kCopyUnroll) {
+        uint32_t pos[kCopyUnroll], rr[kCopyUnroll], qq[kCopyUnroll], rem[kCopyUnroll];
+        int bb[kCopyUnroll];
+        bool act[kCopyUnroll];
 #pragma unroll
-            for (int u = 0; u < kCopyUnroll; ++u) {
-                const uint32_t oi = o0 + (uint32_t)(u * 32 + lane);
-                act[u] = oi < T;
-                uint32_t ro = 0;  // root of output oi: first r with incb[r] > oi
-#pragma unroll
-                for (int s2 = 16; s2 > 0; s2 >>= 1)
-                    if (incb[ro + s2 - 1] <= oi) ro += s2;
-                ro = act[u] ? ro : 0u;
-                const uint32_t q = act[u] ? oi - (ro ? incb[ro - 1] : 0u) : 0u;
-                rr[u] = ro;
-                qq[u] = q;
-                if (STRATEGY == TGL_MOST_RECENT)
-                    pos[u] = fb[ro] + q;
-                else
-                    pos[u] = act[u] ? fb[ro] + picks[((size_t)b * k + q) * 32 + ro] : 0u;
+        for (int u = 0; u < kCopyUnroll; ++u) {
+            const uint32_t oi = o0 + (uint32_t)(u * 32 + lane);
+            act[u] = oi < total;
+            int b = 0;
+            uint32_t r = act[u] ? oi : 0u;
+            while (b < nsb - 1 && r >= inc[b * 32 + 31]) {
+                r -= inc[b * 32 + 31];
+                ++b;
             }
-            int4 rec[kCopyUnroll];
+            const uint32_t* incb = inc + b * 32;
+            uint32_t ro = 0;  // root of output r: first with incb[ro] > r
 #pragma unroll
-            for (int u = 0; u < kCopyUnroll; ++u) {
-                if (act[u]) {
-                    if (p.recs) {
+            for (int s2 = 16; s2 > 0; s2 >>= 1)
+                if (incb[ro + s2 - 1] <= r) ro += s2;
+            ro = act[u] ? ro : 0u;
+            const uint32_t q = act[u] ? r - (ro ? incb[ro - 1] : 0u) : 0u;
+            rr[u] = ro;
+            qq[u] = q;
+            rem[u] = r;
+            bb[u] = b;
+            if (STRATEGY == TGL_MOST_RECENT)
+                pos[u] = first[b * 32 + ro] + q;
+            else
+                pos[u] = act[u] ? first[b * 32 + ro] + picks[((size_t)b * k + q) * 32 + ro] : 0u;
+        }
+        int4 rec[kCopyUnroll];
+#pragma unroll
+        for (int u = 0; u < kCopyUnroll; ++u) {
+            if (act[u]) {
+                if (p.recs) {
 #if TGL_REC_WORDS == 4
-                        rec[u] = __ldg(reinterpret_cast<const int4*>(p.recs) + pos[u]);
+                    rec[u] = __ldg(reinterpret_cast<const int4*>(p.recs) + pos[u]);
 #else
-                        const int* w = reinterpret_cast<const int*>(p.recs + pos[u]);
-                        rec[u] = make_int4(__ldg(w), __ldg(w + 1), __ldg(w + 2), 0);
+                    const int* w = reinterpret_cast<const int*>(p.recs + pos[u]);
+                    rec[u] = make_int4(__ldg(w), __ldg(w + 1), __ldg(w + 2), 0);
 #endif
-                    }
-                    else
-                        rec[u] = make_int4(__float_as_int(__ldg(p.ts + pos[u])), __ldg(p.nbr + pos[u]),
-                                           __ldg(p.eid + pos[u]), 0);
+                } else {
+                    rec[u] = make_int4(__float_as_int(__ldg(p.ts + pos[u])), __ldg(p.nbr + pos[u]),
+                                       __ldg(p.eid + pos[u]), 0);
                 }
             }
+        }
 #pragma unroll
-            for (int u = 0; u < kCopyUnroll; ++u) {
-                if (!act[u]) continue;
-                const uint64_t oi = B + o0 + (uint32_t)(u * 32 + lane);
-                const float tv = __int_as_float(rec[u].x);
-                const float tr = troot[rr[u]];
-                o.nbr[oi] = rec[u].y;
-                o.eid[oi] = rec[u].z;
-                o.dt[oi] = __fsub_rn(tr, tv);
-                if (o.ts_edge) o.ts_edge[oi] = tv;
-                if (o.child_key) o.child_key[oi] = rkey[rr[u]] * (uint64_t)k + qq[u];
-                if (o.child_lo)  // children inherit the window's lower bound (R#3)
-                    o.child_lo[oi] = p.layer == 0 ? __fsub_rn(tr, __fmul_rn((float)(b + 1), p.snapshot_len))
-                                                  : p.root_lo[warp_root0 + rr[u]];
-            }
+        for (int u = 0; u < kCopyUnroll; ++u) {
+            if (!act[u]) continue;
+            const int b = bb[u];
+            const BlockOut& o = p.out[b];
+            const uint64_t oi = base[b] + rem[u];
+            const float tv = __int_as_float(rec[u].x);
+            const float tr = troot[rr[u]];
+            o.nbr[oi] = rec[u].y;
+            o.eid[oi] = rec[u].z;
+            o.dt[oi] = __fsub_rn(tr, tv);
+            if (o.ts_edge) o.ts_edge[oi] = tv;
+            if (o.child_key) o.child_key[oi] = rkey[rr[u]] * (uint64_t)k + qq[u];
+            if (o.child_lo)  // children inherit the window's lower bound (R#3)
+                o.child_lo[oi] = p.layer == 0 ? __fsub_rn(tr, __fmul_rn((float)(b + 1), p.snapshot_len))
+                                              : p.root_lo[warp_root0 + rr[u]];
         }
     }
 }
@@ -537,7 +547,7 @@ static bool picks_fit_smem(int nsb, int k) { return (size_t)nsb * k * 32 * 4 <= 
 struct Launch {
     int layer, chain, nsb;
     int64_t roots_cap, tiles_cap;
-    uint32_t *win_first, *win_len, *tile_tot;
+    uint32_t *cuts, *tile_tot;
     uint64_t* super_tot;
     int64_t supers_cap;
     uint32_t* picks;  // global picks or null
@@ -580,8 +590,7 @@ static int plan_sample(int64_t n_roots, int L, const int32_t* fanouts, int S, in
         la.nsb = nsb;
         la.roots_cap = std::max<int64_t>(1, P.roots_cap[layer]);
         la.tiles_cap = (la.roots_cap + kTile - 1) / kTile;
-        la.win_first = c.take<uint32_t>((size_t)nsb * la.roots_cap);
-        la.win_len = c.take<uint32_t>((size_t)nsb * la.roots_cap);
+        la.cuts = c.take<uint32_t>((size_t)(nsb + 1) * la.roots_cap);
         la.tile_tot = c.take<uint32_t>((size_t)nsb * la.tiles_cap);
         la.supers_cap = (la.tiles_cap + (1 << kSuperShift) - 1) >> kSuperShift;
         la.picks = nullptr;
@@ -696,8 +705,7 @@ static int sample_impl(const tgl_tcsr* g, const int32_t* roots, const float* roo
         sp.snapshot_len = snapshot_len;
         sp.seed_lo = (uint32_t)seed;
         sp.seed_hi = (uint32_t)(seed >> 32);
-        sp.win_first = la.win_first;
-        sp.win_len = la.win_len;
+        sp.cuts = la.cuts;
         sp.tile_tot = la.tile_tot;
         sp.super_tot = la.super_tot;
         sp.supers_cap = la.supers_cap;
