@@ -59,7 +59,7 @@ def lib():
         L.oracle_tcsr_fill.argtypes = [P, P, P, P, i64, i64, i32, ctypes.c_int, P, P, P, P, P]
         L.oracle_tcsr_fill.restype = ctypes.c_int
         L.oracle_sample_block.argtypes = [P, P, P, P, i32, P, P, P, P, i64, i32, i32, f32, i32, i32,
-                                          u64, P, P, P, P, P, P, P, P, P]
+                                          i32, u64, P, P, P, P, P, P, P, P, P]
         L.oracle_sample_block.restype = i64
         L.oracle_gather.argtypes = [P, i64, P, i64, i64, P, P]
         L.oracle_gather.restype = None
@@ -162,7 +162,7 @@ def build_restricted(chunks: Iterable, *, n_nodes: int, add_reverse: bool,
 # --------------------------------------------------------------------------- sampler
 def sample_block(g: TCSR, root_node, root_ts, root_key, root_lo, *, layer: int, snapshot: int,
                  snapshot_len: float, k: int, strategy: int, seed: int,
-                 want_children: bool) -> dict:
+                 want_children: bool, replacement: bool = False) -> dict:
     """One (layer, snapshot) block of Alg. 1 -- see tgl_oracle.c."""
     root_node = np.ascontiguousarray(root_node, dtype=np.int32)
     root_ts = np.ascontiguousarray(root_ts, dtype=np.float32)
@@ -181,7 +181,7 @@ def sample_block(g: TCSR, root_node, root_ts, root_key, root_lo, *, layer: int, 
     scratch = np.zeros(max(k, 1), dtype=np.uint32)
     nnz = lib().oracle_sample_block(_p(g["indptr"]), _p(g["nbr"]), _p(g["ts"]), _p(g["eid"]),
                                     g.n_nodes, _p(root_node), _p(root_ts), _p(root_key), _p(root_lo), n,
-                                    layer, snapshot, float(snapshot_len), k, strategy,
+                                    layer, snapshot, float(snapshot_len), k, strategy, int(bool(replacement)),
                                     int(seed) & 0xFFFFFFFFFFFFFFFF, _p(offsets), _p(nbr), _p(eid), _p(dt),
                                     _p(ts_edge), _p(ckey), _p(clo), _p(err), _p(scratch))
     out = dict(offsets=offsets, nbr=nbr[:nnz], eid=eid[:nnz], dt=dt[:nnz], err=int(err[0]))
@@ -191,13 +191,19 @@ def sample_block(g: TCSR, root_node, root_ts, root_key, root_lo, *, layer: int, 
 
 
 def sample(g: TCSR, roots, root_ts, *, fanouts: List[int], strategy: int, n_snapshots: int = 1,
-           snapshot_len: float = math.inf, seed: int = 0, root_key_base: int = 0) -> List[dict]:
+           snapshot_len: float = math.inf, seed: int = 0, root_key_base: int = 0,
+           hop_time: str = "edge", replacement: bool = False) -> List[dict]:
     """Alg. 1: L x S blocks, block (l, s) at index l*S + s.
 
     Layer-0 roots are the caller's; the roots of block (l, s), l >= 1, are the outputs
     (nbr, ts_edge) of block (l-1, s) in output order, without dedup (R#14), each with
     root key parent_key * k_{l-1} + j (R#7) and inherited lower bound (R#3).
+    Variants: hop_time="root" -- hop roots carry their parent's root time
+    instead of the sampled edge's ("others use the root's timestamp", R#23);
+    replacement=True -- uniform draws with replacement (R#24).
     """
+    if hop_time not in ("edge", "root"):
+        raise ValueError("hop_time must be 'edge' or 'root'")
     L, S = len(fanouts), int(n_snapshots)
     root_node = np.ascontiguousarray(np.asarray(roots, dtype=np.int32))
     root_ts = np.ascontiguousarray(np.asarray(root_ts, dtype=np.float32))
@@ -210,10 +216,13 @@ def sample(g: TCSR, roots, root_ts, *, fanouts: List[int], strategy: int, n_snap
         for l in range(L):
             want = l < L - 1
             b = sample_block(g, rn, rt, rk, rlo, layer=l, snapshot=s, snapshot_len=snapshot_len,
-                             k=fanouts[l], strategy=strategy, seed=seed, want_children=want)
+                             k=fanouts[l], strategy=strategy, seed=seed, want_children=want,
+                             replacement=replacement)
             blocks[l * S + s] = b
             if want:
-                rn, rt, rk = b["nbr"], b["ts_edge"], b["child_key"]
+                # R#4 / R#23: the hop root's time is the sampled edge's, or its parent root's
+                t_next = b["ts_edge"] if hop_time == "edge" else np.repeat(rt, np.diff(b["offsets"]))
+                rn, rt, rk = b["nbr"], np.ascontiguousarray(t_next, dtype=np.float32), b["child_key"]
                 rlo = b["child_lo"] if need_lo else None
     return blocks
 

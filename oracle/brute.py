@@ -59,9 +59,16 @@ def floyd(c: int, k: int, seed: int, layer: int, snapshot: int, rk: int) -> List
     return sorted(picks)
 
 
+def with_replacement(c: int, k: int, seed: int, layer: int, snapshot: int, rk: int) -> List[int]:
+    """k independent uniform draws from range(c), draw j from Philox word 0 (R#24), sorted."""
+    key = (seed & MASK, (seed >> 32) & MASK)
+    return sorted((philox((j, (layer << 16) | snapshot, rk & MASK, (rk >> 32) & MASK), key)[0] * c) >> 32
+                  for j in range(k))
+
+
 def sample(src, dst, ts, eid, *, n_nodes: int, add_reverse: bool, roots, root_ts, fanouts,
            strategy: int, n_snapshots: int = 1, snapshot_len: float = math.inf, seed: int = 0,
-           root_key_base: int = 0):
+           root_key_base: int = 0, hop_time: str = "edge", replacement: bool = False):
     """Returns blocks[l*S+s] = list over roots of lists of (nbr, eid, dt, ts_edge)."""
     owner, nbr, tsl, eidl = logical_stream(src, dst, ts, eid, add_reverse)
     f32 = np.float32
@@ -89,6 +96,8 @@ def sample(src, dst, ts, eid, *, n_nodes: int, add_reverse: bool, roots, root_ts
                 c = len(cand)
                 if strategy == 0:
                     sel = cand[max(0, c - k):]
+                elif replacement:
+                    sel = cand[with_replacement(c, k, seed, l, s, rk)] if c else cand
                 elif c <= k:
                     sel = cand
                 else:
@@ -96,7 +105,8 @@ def sample(src, dst, ts, eid, *, n_nodes: int, add_reverse: bool, roots, root_ts
                 row = []
                 for j, p in enumerate(sel):
                     row.append((int(nbr[p]), int(eidl[p]), f32(t - tsl[p]), f32(tsl[p])))
-                    nxt.append((int(nbr[p]), f32(tsl[p]), (rk * k + j) & 0xFFFFFFFFFFFFFFFF,
+                    nxt.append((int(nbr[p]), f32(tsl[p]) if hop_time == "edge" else t,
+                                (rk * k + j) & 0xFFFFFFFFFFFFFFFF,
                                 Lo if math.isfinite(snapshot_len) else None))
                 out.append(row)
             blocks[l * S + s] = out

@@ -22,7 +22,8 @@
  *                            subset (used for billion-edge configs whose full T-CSR
  *                            is only needed for the sampled roots)
  *   oracle_sample_block      one (layer l, snapshot s) block of Alg. 1, P:L217-L243,
- *                            P:L260-L262 (strategies), P:L267 (no leak)
+ *                            P:L260-L262 (strategies), P:L267 (no leak); uniform with
+ *                            replacement as the variant of DESIGN.md R#24
  *   oracle_gather            out[i] = table[id[i]] byte for byte, Fig. 2 step 2
  *
  * Pins (tests/test_oracle_*.py): Philox known-answer vectors, the Fig. 3 hand example
@@ -213,7 +214,7 @@ int64_t oracle_sample_block(const int64_t *indptr, const int32_t *nbr, const flo
                             const int32_t *root_node, const float *root_ts, const uint64_t *root_key,
                             const float *root_lo, int64_t n_roots,
                             int32_t layer, int32_t snapshot, float snapshot_len, int32_t k, int32_t strategy,
-                            uint64_t seed,
+                            int32_t replacement, uint64_t seed,
                             int64_t *offsets, int32_t *out_nbr, int32_t *out_eid, float *out_dt,
                             float *out_ts_edge, uint64_t *out_child_key, float *out_child_lo,
                             int32_t *err, uint32_t *pick_scratch /* >= k entries */)
@@ -241,10 +242,27 @@ int64_t oracle_sample_block(const int64_t *indptr, const int32_t *nbr, const flo
         if (b < a) b = a;                 /* cannot happen for L <= U; kept for safety */
         int64_t c = b - a;
         int64_t n_sel = c < (int64_t)k ? c : (int64_t)k;
+        if (strategy == 1 && replacement) n_sel = c > 0 ? (int64_t)k : 0;  /* R#24 */
         uint64_t rk = root_key ? root_key[i] : 0;
 
         /* positions of the selected slots, ascending */
-        if (strategy == 0 || c <= (int64_t)k) {
+        if (strategy == 1 && replacement) {
+            /* uniform WITH replacement (R#24): k independent draws r_j uniform in [0, c), draw j
+             * from Philox word 0 with the counter of Floyd's draw j (R#6); ascending (R#13). */
+            for (int32_t j = 0; j < (int32_t)n_sel; ++j) {
+                uint32_t ctr[4] = { (uint32_t)j, ((uint32_t)layer << 16) | (uint32_t)snapshot,
+                                    (uint32_t)(rk & 0xFFFFFFFFu), (uint32_t)(rk >> 32) };
+                uint32_t x[4];
+                oracle_philox4x32_10(ctr, key, x);
+                pick_scratch[j] = (uint32_t)(((uint64_t)x[0] * (uint64_t)c) >> 32);
+            }
+            for (int32_t j = 1; j < (int32_t)n_sel; ++j) {
+                uint32_t x = pick_scratch[j];
+                int32_t q = j - 1;
+                while (q >= 0 && pick_scratch[q] > x) { pick_scratch[q + 1] = pick_scratch[q]; --q; }
+                pick_scratch[q + 1] = x;
+            }
+        } else if (strategy == 0 || c <= (int64_t)k) {
             int64_t first = (strategy == 0) ? (b - n_sel) : a;
             for (int64_t j = 0; j < n_sel; ++j) pick_scratch[j] = (uint32_t)(first + j - a);
         } else {
