@@ -181,8 +181,8 @@ TGL_API int tgl_sample_capacity(int64_t n_roots, int32_t n_layers, const int32_t
  * Device-detected errors (out-of-range root id -> ERANGE, non-finite root time -> EINVAL) give
  *   that root a count of 0 and set the sticky word read by tgl_check(g, ...).
  * workspace: >= ws_bytes from tgl_sample_capacity(), device memory, 256-byte aligned, not
- *   shared by concurrent calls.  Launches: one memset + one sampler kernel per layer (layer 0
- *   covers all S snapshots of a root in one pass; l >= 1 one launch covering all S chains).
+ *   shared by concurrent calls.  Launches: one memset, then two kernels (window, copy) per chain:
+ *   layer 0 is one chain covering all S snapshots of a root; l >= 1 one chain per snapshot.
  */
 TGL_API int tgl_sample(const tgl_tcsr *g, const int32_t *roots, const float *root_ts, int64_t n_roots,
                int32_t n_layers, const int32_t *fanouts /* host [L] */, tgl_strategy strategy,
@@ -199,6 +199,37 @@ TGL_API int tgl_sample_keyed(const tgl_tcsr *g, const int32_t *roots, const floa
                      const int32_t *fanouts /* host [L] */, tgl_strategy strategy, int32_t n_snapshots,
                      float snapshot_len, uint64_t seed, tgl_block *out /* host [L*S] */,
                      void *workspace, size_t ws_bytes, void *stream);
+
+/*
+ * Sampler variants (the other samplers the paper benchmarks; R#23,
+ * R#24).  tgl_sample_ex = tgl_sample / tgl_sample_keyed plus an options struct:
+ *   hop_time     TGL_HOP_EDGE_TIME (default, R#4): a hop root's time is its sampled edge's time;
+ *                TGL_HOP_ROOT_TIME (R#23): it is its parent root's time, so every layer samples
+ *                relative to the layer-0 root's time ("others use the root's timestamp");
+ *                dt of layer l >= 1 is then root time (-) edge time.
+ *   replacement  TGL_UNIFORM only.  0 (default): without replacement (Floyd, R#5).  1 (R#24): a
+ *                root with c > 0 candidates gets exactly k draws r_j = floor(x_j c / 2^32), x_j
+ *                from the Philox counter of Floyd's draw j (R#6), output ascending (duplicates
+ *                kept); c = 0 gives none.
+ *   reserved     must be zero.
+ * root_keys: NULL -> root_key_base + i (as tgl_sample), else explicit keys (as tgl_sample_keyed).
+ * opts: host pointer or NULL (all defaults).  Errors: TGL_EINVAL for an unknown hop_time,
+ * replacement != 0 with TGL_MOST_RECENT, or non-zero reserved words; otherwise as tgl_sample.
+ * The workspace size of tgl_sample_capacity() covers every option.
+ */
+typedef enum { TGL_HOP_EDGE_TIME = 0, TGL_HOP_ROOT_TIME = 1 } tgl_hop_time;
+typedef struct {
+    int32_t hop_time;     /* tgl_hop_time */
+    int32_t replacement;  /* 0 or 1 */
+    int32_t reserved[6];
+} tgl_sample_options;
+
+TGL_API int tgl_sample_ex(const tgl_tcsr *g, const int32_t *roots, const float *root_ts,
+                  const uint64_t *root_keys /* device [n_roots] or NULL */, int64_t n_roots, int32_t n_layers,
+                  const int32_t *fanouts /* host [L] */, tgl_strategy strategy, int32_t n_snapshots,
+                  float snapshot_len, uint64_t seed, uint64_t root_key_base,
+                  const tgl_sample_options *opts /* host or NULL */, tgl_block *out /* host [L*S] */,
+                  void *workspace, size_t ws_bytes, void *stream);
 
 /* ------------------------------------------------------------------ gather (Fig. 2 step 2) */
 

@@ -173,8 +173,15 @@ class Sampler:
     """Preallocated outputs + workspace for repeated tgl_sample calls of up to max_roots roots."""
 
     def __init__(self, g: TCSR, max_roots: int, fanouts: Sequence[int], strategy="most_recent",
-                 n_snapshots: int = 1, snapshot_len: float = math.inf, device=None, want_ts_edge_last=False):
+                 n_snapshots: int = 1, snapshot_len: float = math.inf, device=None, want_ts_edge_last=False,
+                 hop_time: str = "edge", replacement: bool = False):
+        """hop_time: "edge" (R#4) or "root" (R#23, hop roots carry the root time); replacement:
+        uniform with replacement (R#24).  Both map to tgl_sample_ex's options."""
         self.g = g
+        if hop_time not in ("edge", "root"):
+            raise ValueError("hop_time must be 'edge' or 'root'")
+        self._opts = _lib.SampleOptions(1 if hop_time == "root" else 0, 1 if replacement else 0)
+        self._default_opts = hop_time == "edge" and not replacement
         self.fanouts = [int(k) for k in fanouts]
         self.L, self.S = len(self.fanouts), int(n_snapshots)
         self.strategy = _strategy(strategy)
@@ -227,24 +234,32 @@ class Sampler:
         if root_keys is not None:
             if not (root_keys.is_cuda and root_keys.dtype == torch.int64):
                 raise TypeError("root_keys must be a CUDA int64 tensor (uint64 bit patterns)")
-            _rc(_L.tgl_sample_keyed(self.g.handle, _ptr(roots), _ptr(root_ts), _ptr(root_keys), n, self.L, self._fan,
-                                    self.strategy, self.S, self.snapshot_len, int(seed) & 0xFFFFFFFFFFFFFFFF,
-                                    self._c_blocks, _ptr(self.workspace), self.ws_bytes, _stream(stream)),
-                "tgl_sample_keyed")
+            _rc(_L.tgl_sample_ex(self.g.handle, _ptr(roots), _ptr(root_ts), _ptr(root_keys), n, self.L, self._fan,
+                                 self.strategy, self.S, self.snapshot_len, int(seed) & 0xFFFFFFFFFFFFFFFF, 0,
+                                 ctypes.byref(self._opts), self._c_blocks, _ptr(self.workspace), self.ws_bytes,
+                                 _stream(stream)), "tgl_sample_ex")
             return self.blocks
-        _rc(_L.tgl_sample(self.g.handle, _ptr(roots), _ptr(root_ts), n, self.L, self._fan, self.strategy, self.S,
-                          self.snapshot_len, int(seed) & 0xFFFFFFFFFFFFFFFF, int(root_key_base) & 0xFFFFFFFFFFFFFFFF,
-                          self._c_blocks, _ptr(self.workspace), self.ws_bytes, _stream(stream)), "tgl_sample")
+        if self._default_opts:
+            _rc(_L.tgl_sample(self.g.handle, _ptr(roots), _ptr(root_ts), n, self.L, self._fan, self.strategy, self.S,
+                              self.snapshot_len, int(seed) & 0xFFFFFFFFFFFFFFFF, int(root_key_base) & 0xFFFFFFFFFFFFFFFF,
+                              self._c_blocks, _ptr(self.workspace), self.ws_bytes, _stream(stream)), "tgl_sample")
+        else:
+            _rc(_L.tgl_sample_ex(self.g.handle, _ptr(roots), _ptr(root_ts), None, n, self.L, self._fan, self.strategy,
+                                 self.S, self.snapshot_len, int(seed) & 0xFFFFFFFFFFFFFFFF,
+                                 int(root_key_base) & 0xFFFFFFFFFFFFFFFF, ctypes.byref(self._opts), self._c_blocks,
+                                 _ptr(self.workspace), self.ws_bytes, _stream(stream)), "tgl_sample_ex")
         return self.blocks
 
 
 def sample(g: TCSR, roots: torch.Tensor, root_ts: torch.Tensor, *, fanouts: Sequence[int],
            strategy="most_recent", n_snapshots: int = 1, snapshot_len: float = math.inf, seed: int = 0,
-           root_key_base: int = 0, stream=None) -> List[Block]:
-    """tgl_sample (Alg. 1): returns L*S blocks, block (l, s) at index l*S + s."""
+           root_key_base: int = 0, stream=None, hop_time: str = "edge", replacement: bool = False) -> List[Block]:
+    """tgl_sample (Alg. 1): returns L*S blocks, block (l, s) at index l*S + s.  hop_time /
+    replacement select the variants of tgl_sample_ex (R#23, R#24)."""
     roots = _cuda(roots, torch.int32, "roots")
     root_ts = _cuda(root_ts, torch.float32, "root_ts")
-    s = Sampler(g, max(roots.numel(), 1), fanouts, strategy, n_snapshots, snapshot_len)
+    s = Sampler(g, max(roots.numel(), 1), fanouts, strategy, n_snapshots, snapshot_len, hop_time=hop_time,
+                replacement=replacement)
     return s.run(roots, root_ts, seed=seed, root_key_base=root_key_base, n_roots=roots.numel(), stream=stream)
 
 

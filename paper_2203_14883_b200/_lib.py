@@ -25,6 +25,10 @@ class Block(ctypes.Structure):
                 ("ts_edge", P), ("n_roots_dev", P), ("nnz_dev", P)]
 
 
+class SampleOptions(ctypes.Structure):
+    _fields_ = [("hop_time", ctypes.c_int32), ("replacement", ctypes.c_int32), ("reserved", ctypes.c_int32 * 6)]
+
+
 class GatherTable(ctypes.Structure):
     """tgl_gather_table (include/tgl.h)."""
     _fields_ = [("table", P), ("n_rows", i64), ("row_bytes", i64), ("out", P)]
@@ -45,6 +49,7 @@ SIGNATURES = {
     "tgl_sample_capacity": (ctypes.c_int, [i64, i32, P, i32, ctypes.c_int, f32, P, P, ctypes.POINTER(sz)]),
     "tgl_sample": (ctypes.c_int, [P, P, P, i64, i32, P, ctypes.c_int, i32, f32, u64, u64, P, P, sz, P]),
     "tgl_sample_keyed": (ctypes.c_int, [P, P, P, P, i64, i32, P, ctypes.c_int, i32, f32, u64, P, P, sz, P]),
+    "tgl_sample_ex": (ctypes.c_int, [P, P, P, P, i64, i32, P, ctypes.c_int, i32, f32, u64, u64, P, P, P, sz, P]),
     "tgl_tcsr_set_node_base": (ctypes.c_int, [P, i64]),
     "tgl_shard_unpermute_workspace": (ctypes.c_int, [i64, ctypes.POINTER(sz)]),
     "tgl_offsets_to_counts": (ctypes.c_int, [P, i64, P, P]),

@@ -60,6 +60,7 @@ struct BlockOut {
     float* ts_edge;       // may be null
     uint64_t* child_key;  // may be null
     float* child_lo;      // may be null
+    float* child_t;       // hop roots' times under TGL_HOP_ROOT_TIME (R#23), else null
     int64_t* n_roots_dev;
     int64_t* nnz_dev;
 };
@@ -83,6 +84,7 @@ struct SampleParams {
     int64_t n_roots;                // layer 0: count; l >= 1: capacity
     const int64_t* n_roots_dev_in;  // l >= 1: device count (parent block's nnz)
     int32_t layer, nsb, snap0, k;
+    int32_t replacement;  // uniform with replacement (R#24)
     float snapshot_len;
     uint32_t seed_lo, seed_hi;
     uint32_t* cuts;  // [nsb+1][roots_cap] c_0 >= c_1 >= .. >= c_nsb: window b = slots [c_(b+1), c_b)
@@ -307,7 +309,7 @@ __global__ void __launch_bounds__(kTile, TGL_WINDOW_MINB) window_kernel(const __
         for (int b = 0; b < 3; ++b) {
             if (b >= nsb) break;
             const uint32_t c = cut[b] - cut[b + 1];
-            const uint32_t take = c < k ? c : k;
+            const uint32_t take = p.replacement ? (c ? k : 0u) : (c < k ? c : k);
             if (valid) {
                 if (b == 0) p.cuts[i] = cut[0];
                 p.cuts[(size_t)(b + 1) * p.roots_cap + i] = cut[b + 1];
@@ -330,7 +332,7 @@ __global__ void __launch_bounds__(kTile, TGL_WINDOW_MINB) window_kernel(const __
                     a = __ldg(p.ts + bcur - 1) < xb ? bcur : lower_bound_ts(p, lo, bcur - 1, xb);
             }
             const uint32_t c = bcur - a;
-            const uint32_t take = c < k ? c : k;
+            const uint32_t take = p.replacement ? (c ? k : 0u) : (c < k ? c : k);
             if (valid) {
                 if (b == 0) p.cuts[i] = bcur;
                 p.cuts[(size_t)(b + 1) * p.roots_cap + i] = a;
@@ -405,7 +407,7 @@ __global__ void __launch_bounds__(kTile, TGL_COPY_MINB) copy_kernel(const __grid
     for (int b = 0; b < nsb; ++b) {
         const uint32_t cn = valid ? p.cuts[(size_t)(b + 1) * p.roots_cap + i] : 0u;  // c_(b+1)
         const uint32_t len = cb - cn;                                                 // window size c
-        const uint32_t take = len < (uint32_t)k ? len : (uint32_t)k;
+        const uint32_t take = p.replacement ? (len ? (uint32_t)k : 0u) : (len < (uint32_t)k ? len : (uint32_t)k);
         // most_recent: the take slots closest to the end pointer; uniform: picks from c_(b+1)
         first[b * 32 + lane] = STRATEGY == TGL_MOST_RECENT ? cb - take : cn;
         cb = cn;
@@ -414,11 +416,27 @@ __global__ void __launch_bounds__(kTile, TGL_COPY_MINB) copy_kernel(const __grid
         if (lane == 31) s_wsum[b][warp] = x;
         if (STRATEGY == TGL_UNIFORM) {
             uint32_t* pk = picks + (size_t)b * k * 32 + lane;  // pick q at pk[q * 32]
-            if (len <= (uint32_t)k) {
+            const uint32_t ctr1 = ((uint32_t)p.layer << 16) | (uint32_t)(p.layer == 0 ? b : p.snap0);
+            if (!p.replacement && len <= (uint32_t)k) {
                 for (uint32_t q = 0; q < len; ++q) pk[q * 32] = q;
+            } else if (p.replacement) {
+                // with replacement (R#24): r_j uniform in [0, c) from the counter of Floyd's draw j
+                for (uint32_t j = 0; j < take; ++j) {
+                    const uint4 rnd = philox4x32_10(make_uint4(j, ctr1, (uint32_t)rk, (uint32_t)(rk >> 32)),
+                                                    p.seed_lo, p.seed_hi);
+                    pk[j * 32] = __umulhi(rnd.x, len);
+                }
+                for (int j = 1; j < (int)take; ++j) {  // ascending slot order (R#13)
+                    const uint32_t xj = pk[j * 32];
+                    int q = j - 1;
+                    while (q >= 0 && pk[q * 32] > xj) {
+                        pk[(q + 1) * 32] = pk[q * 32];
+                        --q;
+                    }
+                    pk[(q + 1) * 32] = xj;
+                }
             } else {
                 // Floyd: for m = c-k .. c-1, r uniform in [0, m]; take r unless taken, else m
-                const uint32_t ctr1 = ((uint32_t)p.layer << 16) | (uint32_t)(p.layer == 0 ? b : p.snap0);
                 for (int j = 0; j < k; ++j) {
                     const uint32_t m = len - (uint32_t)k + (uint32_t)j;
                     const uint4 rnd = philox4x32_10(make_uint4((uint32_t)j, ctr1, (uint32_t)rk, (uint32_t)(rk >> 32)),
@@ -535,6 +553,7 @@ __global__ void __launch_bounds__(kTile, TGL_COPY_MINB) copy_kernel(const __grid
             o.dt[oi] = __fsub_rn(tr, tv);
             if (o.ts_edge) o.ts_edge[oi] = tv;
             if (o.child_key) o.child_key[oi] = rkey[rr[u]] * (uint64_t)k + qq[u];
+            if (o.child_t) o.child_t[oi] = tr;  // R#23: hop roots carry the root time
             if (o.child_lo)  // children inherit the window's lower bound (R#3)
                 o.child_lo[oi] = p.layer == 0 ? __fsub_rn(tr, __fmul_rn((float)(b + 1), p.snapshot_len))
                                               : p.root_lo[warp_root0 + rr[u]];
@@ -561,6 +580,7 @@ struct SamplePlan {
     size_t memset_from = 0, memset_bytes = 0;
     uint64_t* child_key[64][TGL_MAX_SNAPSHOTS];
     float* child_lo[64][TGL_MAX_SNAPSHOTS];
+    float* child_t[64][TGL_MAX_SNAPSHOTS];
     size_t bytes = 0;
 };
 
@@ -610,6 +630,7 @@ static int plan_sample(int64_t n_roots, int L, const int32_t* fanouts, int S, in
         for (int s = 0; s < S; ++s) {
             P.child_key[l][s] = strategy == TGL_UNIFORM ? c.take<uint64_t>((size_t)P.edges_cap[l]) : nullptr;
             P.child_lo[l][s] = need_lo ? c.take<float>((size_t)P.edges_cap[l]) : nullptr;
+            P.child_t[l][s] = c.take<float>((size_t)P.edges_cap[l]);  // used under TGL_HOP_ROOT_TIME
         }
     P.bytes = c.bytes();
     return TGL_OK;
@@ -644,9 +665,18 @@ extern "C" int tgl_sample_capacity(int64_t n_roots, int32_t n_layers, const int3
 
 static int sample_impl(const tgl_tcsr* g, const int32_t* roots, const float* root_ts, const uint64_t* root_keys,
                        int64_t n_roots, int32_t n_layers, const int32_t* fanouts, tgl_strategy strategy,
-                       int32_t n_snapshots, float snapshot_len, uint64_t seed, uint64_t root_key_base, tgl_block* out,
-                       void* workspace, size_t ws_bytes, void* stream) {
+                       int32_t n_snapshots, float snapshot_len, uint64_t seed, uint64_t root_key_base,
+                       const tgl_sample_options* opts, tgl_block* out, void* workspace, size_t ws_bytes,
+                       void* stream) {
     if (!g || !out || !workspace) return TGL_EINVAL;
+    tgl_sample_options o;
+    memset(&o, 0, sizeof(o));
+    if (opts) o = *opts;
+    if (o.hop_time != TGL_HOP_EDGE_TIME && o.hop_time != TGL_HOP_ROOT_TIME) return TGL_EINVAL;
+    if (o.replacement != 0 && (o.replacement != 1 || strategy != TGL_UNIFORM)) return TGL_EINVAL;
+    for (int q = 0; q < 6; ++q)
+        if (o.reserved[q]) return TGL_EINVAL;
+    const bool hop_root = o.hop_time == TGL_HOP_ROOT_TIME;
     if (n_roots > 0 && (!roots || !root_ts)) return TGL_EINVAL;
     static thread_local SamplePlan P;
     int rc = plan_sample(n_roots, n_layers, fanouts, n_snapshots, (int)strategy, snapshot_len, workspace, P);
@@ -691,7 +721,7 @@ static int sample_impl(const tgl_tcsr* g, const int32_t* roots, const float* roo
         } else {
             const tgl_block& par = out[(l - 1) * S + s];
             sp.root_node = par.nbr;
-            sp.root_ts = par.ts_edge;
+            sp.root_ts = hop_root ? P.child_t[l - 1][s] : par.ts_edge;
             sp.root_key = P.child_key[l - 1][s];
             sp.root_lo = P.child_lo[l - 1][s];
             sp.n_roots = P.roots_cap[l];
@@ -702,6 +732,7 @@ static int sample_impl(const tgl_tcsr* g, const int32_t* roots, const float* roo
         sp.nsb = la.nsb;
         sp.snap0 = s;
         sp.k = fanouts[l];
+        sp.replacement = o.replacement;
         sp.snapshot_len = snapshot_len;
         sp.seed_lo = (uint32_t)seed;
         sp.seed_hi = (uint32_t)(seed >> 32);
@@ -724,6 +755,7 @@ static int sample_impl(const tgl_tcsr* g, const int32_t* roots, const float* roo
             bo.ts_edge = ob.ts_edge;
             bo.child_key = l < L - 1 ? P.child_key[l][bs] : nullptr;
             bo.child_lo = l < L - 1 ? P.child_lo[l][bs] : nullptr;
+            bo.child_t = (l < L - 1 && hop_root) ? P.child_t[l][bs] : nullptr;
             bo.n_roots_dev = ob.n_roots_dev;
             bo.nnz_dev = ob.nnz_dev;
         }
@@ -742,7 +774,7 @@ extern "C" int tgl_sample(const tgl_tcsr* g, const int32_t* roots, const float* 
                           float snapshot_len, uint64_t seed, uint64_t root_key_base, tgl_block* out, void* workspace,
                           size_t ws_bytes, void* stream) {
     return sample_impl(g, roots, root_ts, nullptr, n_roots, n_layers, fanouts, strategy, n_snapshots, snapshot_len,
-                       seed, root_key_base, out, workspace, ws_bytes, stream);
+                       seed, root_key_base, nullptr, out, workspace, ws_bytes, stream);
 }
 
 extern "C" int tgl_sample_keyed(const tgl_tcsr* g, const int32_t* roots, const float* root_ts,
@@ -751,5 +783,14 @@ extern "C" int tgl_sample_keyed(const tgl_tcsr* g, const int32_t* roots, const f
                                 tgl_block* out, void* workspace, size_t ws_bytes, void* stream) {
     if (n_roots > 0 && !root_keys) return TGL_EINVAL;
     return sample_impl(g, roots, root_ts, root_keys, n_roots, n_layers, fanouts, strategy, n_snapshots, snapshot_len,
-                       seed, 0, out, workspace, ws_bytes, stream);
+                       seed, 0, nullptr, out, workspace, ws_bytes, stream);
+}
+
+extern "C" int tgl_sample_ex(const tgl_tcsr* g, const int32_t* roots, const float* root_ts, const uint64_t* root_keys,
+                             int64_t n_roots, int32_t n_layers, const int32_t* fanouts, tgl_strategy strategy,
+                             int32_t n_snapshots, float snapshot_len, uint64_t seed, uint64_t root_key_base,
+                             const tgl_sample_options* opts, tgl_block* out, void* workspace, size_t ws_bytes,
+                             void* stream) {
+    return sample_impl(g, roots, root_ts, root_keys, n_roots, n_layers, fanouts, strategy, n_snapshots, snapshot_len,
+                       seed, root_keys ? 0 : root_key_base, opts, out, workspace, ws_bytes, stream);
 }

@@ -1,0 +1,95 @@
+"""GPU parity of the sampler variants (tgl_sample_ex, R#23, R#24)
+against the CPU oracle, bit for bit, on random graphs (multi-tile, ragged, hubs, 1-3 layers,
+1-4 snapshots), plus the option validation of the C ABI."""
+import ctypes
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from synth.tiny import random_graph, random_roots
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def tgl():
+    if not torch.cuda.is_available():
+        pytest.fail("gpu tests need a CUDA device")
+    import paper_2203_14883_b200 as m
+    return m
+
+
+def cu(a, dtype):
+    return torch.as_tensor(np.asarray(a), dtype=dtype).cuda()
+
+
+@pytest.mark.parametrize("hop_time,replacement", [("root", False), ("edge", True), ("root", True)])
+def test_variants_bit_exact(tgl, hop_time, replacement):
+    rng = np.random.default_rng(31 + replacement + 2 * (hop_time == "root"))
+    for case in range(60):
+        n_nodes = int(rng.integers(1, 500))
+        n_edges = int(rng.integers(0, 6000))
+        add_rev = bool(case % 2)
+        src, dst, ts, eid = random_graph(900 + case, n_nodes, n_edges, integer_times=case % 3 != 0)
+        roots, rts = random_roots(900 + case, n_nodes, int(rng.integers(0, 1500)), integer_times=case % 3 != 0)
+        L = 1 + case % 3
+        fanouts = [int(rng.integers(1, 12)) for _ in range(L)]
+        strategy = 1 if replacement else int(rng.integers(0, 2))
+        S = int(rng.integers(1, 5))
+        t_s = math.inf if S == 1 and case % 4 else float(rng.choice([1.0, 2.5, 7.0]))
+        seed, base = int(rng.integers(0, 2**63)), int(rng.integers(0, 2**40))
+        go = oracle.build(src, dst, ts, eid, n_nodes=n_nodes, add_reverse=add_rev)
+        g = tgl.build(cu(src, torch.int32), cu(dst, torch.int32), cu(ts, torch.float32), None,
+                      n_nodes=n_nodes, add_reverse=add_rev, with_index=case % 5 != 2)
+        bo = oracle.sample(go, roots, rts, fanouts=fanouts, strategy=strategy, n_snapshots=S, snapshot_len=t_s,
+                           seed=seed, root_key_base=base, hop_time=hop_time, replacement=replacement)
+        b = tgl.sample(g, cu(roots, torch.int32), cu(rts, torch.float32), fanouts=fanouts, strategy=strategy,
+                       n_snapshots=S, snapshot_len=t_s, seed=seed, root_key_base=base, hop_time=hop_time,
+                       replacement=replacement)
+        for j, (x, o) in enumerate(zip(b, bo)):
+            off, nbr, e, dt, _ = x.trimmed()
+            np.testing.assert_array_equal(off.cpu().numpy(), o["offsets"], err_msg=f"case {case} block {j}")
+            np.testing.assert_array_equal(nbr.cpu().numpy(), o["nbr"])
+            np.testing.assert_array_equal(e.cpu().numpy(), o["eid"])
+            np.testing.assert_array_equal(dt.cpu().numpy().view(np.uint32), o["dt"].view(np.uint32))
+
+
+def test_keyed_variant_equals_base_keys(tgl):
+    """tgl_sample_ex with explicit keys root_key_base + i == with root_key_base (R#7)."""
+    src, dst, ts, _ = random_graph(5, 300, 5000)
+    roots, rts = random_roots(5, 300, 700)
+    g = tgl.build(cu(src, torch.int32), cu(dst, torch.int32), cu(ts, torch.float32), None, n_nodes=300,
+                  add_reverse=True)
+    smp = tgl.Sampler(g, 700, [5, 3], "uniform", hop_time="root", replacement=True)
+    a = [x.trimmed() for x in smp.run(cu(roots, torch.int32), cu(rts, torch.float32), seed=9, root_key_base=1000)]
+    a = [[t.cpu().numpy() for t in x[:4]] for x in a]
+    keys = torch.arange(1000, 1700, dtype=torch.int64, device="cuda")
+    b = [x.trimmed() for x in smp.run(cu(roots, torch.int32), cu(rts, torch.float32), seed=9, root_keys=keys)]
+    for x, y in zip(a, b):
+        for u, v in zip(x, y[:4]):
+            np.testing.assert_array_equal(u, v.cpu().numpy())
+
+
+def test_option_validation(tgl):
+    from paper_2203_14883_b200 import _lib
+    L_ = _lib.load()
+    src, dst, ts, _ = random_graph(1, 10, 50)
+    g = tgl.build(cu(src, torch.int32), cu(dst, torch.int32), cu(ts, torch.float32), None, n_nodes=10,
+                  add_reverse=False)
+    smp = tgl.Sampler(g, 4, [3], "most_recent")
+    r, t = cu([1, 2, 3, 4], torch.int32), cu([10.0, 20.0, 30.0, 40.0], torch.float32)
+    fan = (ctypes.c_int32 * 1)(3)
+
+    def call(opts, strategy=0):
+        return L_.tgl_sample_ex(g.handle, r.data_ptr(), t.data_ptr(), None, 4, 1, fan, strategy, 1, math.inf, 0, 0,
+                                ctypes.byref(opts), smp._c_blocks, smp.workspace.data_ptr(), smp.ws_bytes, None)
+    assert call(_lib.SampleOptions(0, 0)) == 0
+    assert call(_lib.SampleOptions(2, 0)) == -1            # unknown hop_time
+    assert call(_lib.SampleOptions(0, 1)) == -1            # replacement with most_recent
+    o = _lib.SampleOptions(0, 0)
+    o.reserved[3] = 1
+    assert call(o) == -1                                   # reserved words must be zero
+    torch.cuda.synchronize()
