@@ -63,6 +63,8 @@ def lib():
         L.oracle_sample_block.restype = i64
         L.oracle_gather.argtypes = [P, i64, P, i64, i64, P, P]
         L.oracle_gather.restype = None
+        L.oracle_state_write.argtypes = [P, P, i64, i32, i32, P, P, P, i64, P, P]
+        L.oracle_state_write.restype = None
         _lib = L
     return _lib
 
@@ -238,3 +240,30 @@ def gather(ids, table: np.ndarray) -> (np.ndarray, int):
     err = np.zeros(1, dtype=np.int32)
     lib().oracle_gather(_p(ids), len(ids), _p(table), n_rows, row_bytes, _p(out), _p(err))
     return out, int(err[0])
+
+
+# --------------------------------------------------------------------------- state write
+def state_write(ids, ts, *, n_nodes: int, K: int, tables, pos=None, ts_table=None) -> int:
+    """Fig. 2 step 6, reading R#25: events applied in batch order, each into
+    slot pos[v] of node v's K-slot ring, pos[v] = (pos[v] + 1) mod K.  tables: list of
+    (rows [n, ...], table [n_nodes * K, ...]) numpy pairs, updated IN PLACE; pos (int32 [n_nodes])
+    and ts_table (float32 [n_nodes * K]) likewise.  Returns the error code (0 or ERANGE)."""
+    ids = np.ascontiguousarray(ids, dtype=np.int32)
+    ts = np.ascontiguousarray(ts, dtype=np.float32)
+    n = len(ids)
+    err = np.zeros(1, dtype=np.int32)
+    pos_start = None if pos is None else pos.copy()
+    jobs = list(tables) if tables else [(None, None)]
+    last = None
+    for j, (rows, table) in enumerate(jobs):
+        p = None if pos is None else pos_start.copy()  # every table sees the same ring cursors
+        rb = 0
+        if rows is not None:
+            assert rows.flags.c_contiguous and table.flags.c_contiguous
+            rb = rows.nbytes // n if n else 0
+        lib().oracle_state_write(_p(ids), _p(ts), n, n_nodes, K, _p(p), _p(ts_table if j == 0 else None),
+                                 _p(rows), rb, _p(table), _p(err))
+        last = p
+    if pos is not None:
+        pos[:] = last
+    return int(err[0])

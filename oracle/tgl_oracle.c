@@ -25,6 +25,9 @@
  *                            P:L260-L262 (strategies), P:L267 (no leak); uniform with
  *                            replacement as the variant of DESIGN.md R#24
  *   oracle_gather            out[i] = table[id[i]] byte for byte, Fig. 2 step 2
+ *   oracle_state_write       Fig. 2 step 6: node memory / mailbox
+ *                            update, events applied one by one in batch order, each
+ *                            appended to its node's ring of K most recent slots (R#25)
  *
  * Pins (tests/test_oracle_*.py): Philox known-answer vectors, the Fig. 3 hand example
  * (P:L252), the add_reverse tie example, brute force over the whole logical stream
@@ -318,5 +321,27 @@ void oracle_gather(const int32_t *ids, int64_t n_ids, const uint8_t *table, int6
             continue;
         }
         memcpy(dst, table + id * row_bytes, (size_t)row_bytes);
+    }
+}
+
+/* State write (Fig. 2 step 6: "update the memory and the mailbox for next mini-batch";
+ * the mailbox stores "a fixed number of most recent mails"; 1 mail, 10 for APAN).
+ * Reading R#25: events i = 0..n-1 are applied one at a time in batch order (a chronological batch,
+ * P:L247).  Event i of node v = ids[i] writes its row into slot q = pos[v] of v's ring of K slots
+ * (table row (v*K + q), row_bytes bytes; ts_table[v*K + q] = ts[i] when given), then
+ * pos[v] = (q + 1) mod K.  K = 1 (node memory; pos may be NULL) is "the last event wins".  An id
+ * outside [0, n_nodes) skips the event and raises *err. */
+void oracle_state_write(const int32_t *ids, const float *ts, int64_t n, int32_t n_nodes, int32_t K,
+                        int32_t *pos, float *ts_table, const uint8_t *rows, int64_t row_bytes,
+                        uint8_t *table, int32_t *err)
+{
+    for (int64_t i = 0; i < n; ++i) {
+        int32_t v = ids[i];
+        if (v < 0 || v >= n_nodes) { if (err) *err = ORC_ERANGE; continue; }
+        int32_t q = (K > 1 && pos) ? pos[v] : 0;
+        int64_t slot = (int64_t)v * K + q;
+        if (table && rows) memcpy(table + slot * row_bytes, rows + i * row_bytes, (size_t)row_bytes);
+        if (ts_table) ts_table[slot] = ts[i];
+        if (K > 1 && pos) pos[v] = (q + 1) % K;
     }
 }
