@@ -7,6 +7,8 @@
  *                                                      (L260-L262), "Parallel Sampling" (L265-L268)
  *   tgl_gather       mini-batch row gather             Fig. 2 step 2 (L201), node memory / mailbox
  *                                                      (L154-L175, L210), edge features (Table 3)
+ *   tgl_state_write  node memory / mailbox update       Fig. 2 step 6 (L201), mailbox of the K
+ *                                                      most recent mails (L210, L322)
  *   tgl_shard_*      node-sharded exchange helpers      (not in the paper)
  *
  * Conventions (every entry point):
@@ -252,10 +254,41 @@ typedef struct {
 TGL_API int tgl_gather(const int32_t *ids, int64_t n_ids_cap, const int64_t *n_ids_dev,
                const tgl_gather_table *tables /* host [n_tables] */, int32_t n_tables, void *stream);
 
+/* ------------------------------------------------------------------ state write (Fig. 2 step 6) */
+
+/* One state table: rows of the n events (rows[i], row_bytes each) scattered into the node table
+ * laid out as n_nodes x K slots of row_bytes (slot q of node v at byte (v*K + q) * row_bytes). */
+typedef struct {
+    const void *rows;   /* device [n_events * row_bytes] */
+    int64_t row_bytes;  /* > 0 */
+    void *table;        /* device [n_nodes * K * row_bytes], updated in place */
+} tgl_state_table;
+
+/*
+ * "Update the memory and the mailbox for next mini-batch" (Fig. 2 step 6, L201; the mailbox keeps
+ * "a fixed number of most recent mails", L210; 1 mail, 10 for APAN, L322), reading R#25: the
+ * result equals applying events i = 0..n_events-1 one at a time in batch order: event i of node
+ * v = ids[i] writes rows_t[i] into slot q = pos[v] of v's ring in every table t, ts[i] into
+ * ts_table[v*K + q] (if ts_table != NULL), then pos[v] = (q + 1) mod K.
+ *   K = 1: node memory / mem_ts / a 1-mail mailbox -- the last event of each node wins; pos may
+ *          be NULL (and is not touched).  K > 1: pos (device int32 [n_nodes], caller-owned ring
+ *          cursors, values in [0, K)) is required.
+ * Deterministic (no atomic decides a value): a stable sort groups each node's events, only its
+ * last K survive, each into a distinct slot.  Device-detected errors: an id outside [0, n_nodes)
+ * skips that event and sets the sticky ERANGE word read by tgl_check(NULL, ...).
+ * Errors: TGL_EINVAL for K < 1, n_events >= 2^31, K > 1 without pos, a NULL row / table pointer,
+ * row_bytes <= 0 or n_tables > TGL_MAX_GATHER_TABLES; TGL_EWORKSPACE if ws_bytes is too small.
+ * workspace >= tgl_state_write_workspace() bytes (device, not shared by concurrent calls).
+ */
+TGL_API int tgl_state_write_workspace(int64_t n_events, int32_t n_nodes, size_t *bytes /* host */);
+TGL_API int tgl_state_write(const int32_t *ids, const float *ts, int64_t n_events, int32_t n_nodes, int32_t K,
+                    int32_t *pos, float *ts_table, const tgl_state_table *tables /* host [n_tables] */,
+                    int32_t n_tables, void *workspace, size_t ws_bytes, void *stream);
+
 /* ------------------------------------------------------------------ errors */
 
 /* Synchronises `stream`, returns the first sticky device error raised since the last check by
- * tgl_sample on g (or by tgl_gather when g == NULL) and clears it. */
+ * tgl_sample on g (or, when g == NULL, by tgl_gather and tgl_state_write) and clears it. */
 TGL_API int tgl_check(tgl_tcsr *g, void *stream);
 
 /* ------------------------------------------------------------------ node-sharded mode */

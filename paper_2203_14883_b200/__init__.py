@@ -17,6 +17,7 @@ import math
 from dataclasses import dataclass
 from typing import List, Optional, Sequence
 
+import numpy as np
 import torch
 
 from . import _lib
@@ -281,6 +282,51 @@ def gather(ids: torch.Tensor, tables: Sequence[torch.Tensor], *, n_ids_dev: Opti
         arr[j] = _lib.GatherTable(t.data_ptr(), rows, row_bytes, o.data_ptr())
     _rc(_L.tgl_gather(_ptr(ids), n, _ptr(n_ids_dev), arr, len(tables), _stream(stream)), "tgl_gather")
     return res
+
+
+class StateWriter:
+    """tgl_state_write (Fig. 2 step 6, R#25) with a preallocated workspace for up to max_events
+    events: node memory / mailbox rings updated in place, events applied in batch order."""
+
+    def __init__(self, n_nodes: int, max_events: int, device=None):
+        self.n_nodes = int(n_nodes)
+        self.max_events = int(max_events)
+        b = ctypes.c_size_t()
+        _rc(_L.tgl_state_write_workspace(self.max_events, self.n_nodes, ctypes.byref(b)), "tgl_state_write_workspace")
+        self.ws_bytes = b.value
+        self.workspace = torch.empty(max(b.value, 1), dtype=torch.uint8, device=device or "cuda")
+
+    def __call__(self, ids: torch.Tensor, ts: Optional[torch.Tensor], tables, *, K: int = 1,
+                 pos: Optional[torch.Tensor] = None, ts_table: Optional[torch.Tensor] = None, stream=None):
+        """tables: [(rows [n, ...], table [n_nodes * K, ...])]; pos: int32 [n_nodes] ring cursors
+        (required for K > 1); ts_table: float32 [n_nodes * K] (optional)."""
+        ids = _cuda(ids, torch.int32, "ids")
+        n = ids.numel()
+        if n > self.max_events:
+            raise ValueError(f"{n} events > max_events {self.max_events}")
+        if ts is not None:
+            ts = _cuda(ts, torch.float32, "ts")
+        arr = (_lib.StateTable * max(len(tables), 1))()
+        for j, (rows, table) in enumerate(tables):
+            if not (rows.is_cuda and table.is_cuda and rows.is_contiguous() and table.is_contiguous()):
+                raise TypeError("state rows / tables must be contiguous CUDA tensors")
+            rb = rows.element_size() * (rows[0].numel() if rows.dim() > 1 else 1) if rows.shape[0] else \
+                rows.element_size() * int(np.prod(rows.shape[1:], dtype=np.int64))
+            if table.numel() * table.element_size() != self.n_nodes * K * rb:
+                raise ValueError("table must hold n_nodes * K rows of the rows' width")
+            arr[j] = _lib.StateTable(rows.data_ptr(), rb, table.data_ptr())
+        if pos is not None:
+            pos = _cuda(pos, torch.int32, "pos")
+        if ts_table is not None:
+            ts_table = _cuda(ts_table, torch.float32, "ts_table")
+        _rc(_L.tgl_state_write(_ptr(ids), _ptr(ts), n, self.n_nodes, int(K), _ptr(pos), _ptr(ts_table), arr,
+                               len(tables), _ptr(self.workspace), self.ws_bytes, _stream(stream)), "tgl_state_write")
+
+
+def state_write(ids, ts, tables, *, n_nodes: int, K: int = 1, pos=None, ts_table=None, stream=None):
+    """One-shot tgl_state_write (allocates its workspace)."""
+    StateWriter(n_nodes, max(ids.numel(), 1), device=ids.device)(ids, ts, tables, K=K, pos=pos, ts_table=ts_table,
+                                                                 stream=stream)
 
 
 def check(g: Optional[TCSR] = None, stream=None) -> int:

@@ -29,6 +29,10 @@ class SampleOptions(ctypes.Structure):
     _fields_ = [("hop_time", ctypes.c_int32), ("replacement", ctypes.c_int32), ("reserved", ctypes.c_int32 * 6)]
 
 
+class StateTable(ctypes.Structure):
+    _fields_ = [("rows", ctypes.c_void_p), ("row_bytes", ctypes.c_int64), ("table", ctypes.c_void_p)]
+
+
 class GatherTable(ctypes.Structure):
     """tgl_gather_table (include/tgl.h)."""
     _fields_ = [("table", P), ("n_rows", i64), ("row_bytes", i64), ("out", P)]
@@ -55,6 +59,8 @@ SIGNATURES = {
     "tgl_offsets_to_counts": (ctypes.c_int, [P, i64, P, P]),
     "tgl_shard_unpermute": (ctypes.c_int, [P, i64, P, P, P, P, P, P, P, P, P, sz, P]),
     "tgl_gather": (ctypes.c_int, [P, i64, P, P, i32, P]),
+    "tgl_state_write_workspace": (ctypes.c_int, [i64, i32, ctypes.POINTER(sz)]),
+    "tgl_state_write": (ctypes.c_int, [P, P, i64, i32, i32, P, P, P, i32, P, sz, P]),
     "tgl_check": (ctypes.c_int, [P, P]),
     "tgl_shard_bucket_workspace": (ctypes.c_int, [i64, i32, ctypes.POINTER(sz)]),
     "tgl_shard_bucket": (ctypes.c_int, [P, i64, P, i32, P, P, P, sz, P]),

@@ -7,6 +7,7 @@
 namespace tgl {
 
 int read_and_clear_gather_err(cudaStream_t st, int* bits);  // gather.cu
+int read_and_clear_state_err(cudaStream_t st, int* bits);   // state.cu
 
 int check_device() {
     int dev = 0;
@@ -102,8 +103,13 @@ extern "C" int tgl_check(tgl_tcsr* g, void* stream) {
         if (cudaMemcpyAsync(&bits, g->err_dev, sizeof(int), cudaMemcpyDeviceToHost, st) != cudaSuccess) return TGL_ECUDA;
         if (cudaMemsetAsync(g->err_dev, 0, sizeof(int), st) != cudaSuccess) return TGL_ECUDA;
     } else {
+        int b2 = 0;
         int rc = read_and_clear_gather_err(st, &bits);
         if (rc) return rc;
+        rc = read_and_clear_state_err(st, &b2);
+        if (rc) return rc;
+        if (cudaStreamSynchronize(st) != cudaSuccess) return TGL_ECUDA;
+        bits |= b2;
     }
     if (cudaStreamSynchronize(st) != cudaSuccess) return TGL_ECUDA;
     return err_bits_to_code(bits);

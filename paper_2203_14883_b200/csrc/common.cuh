@@ -77,6 +77,24 @@ int check_device();
 // Map the last CUDA error (launch or API) to TGL_ECUDA.
 inline int cuda_rc(cudaError_t e) { return e == cudaSuccess ? TGL_OK : TGL_ECUDA; }
 
+// byte-copy vector of 2^VS bytes (row copies of tgl_gather / tgl_state_write)
+template <int VS>
+struct Vec;
+template <> struct Vec<4> { using T = uint4; };
+template <> struct Vec<3> { using T = uint2; };
+template <> struct Vec<2> { using T = uint32_t; };
+template <> struct Vec<1> { using T = uint16_t; };
+template <> struct Vec<0> { using T = uint8_t; };
+
+// widest chunk (log2 bytes, <= 4) dividing row_bytes and both base addresses
+inline uint32_t vec_shift_for(int64_t row_bytes, const void* a, const void* b) {
+    uint32_t vs = 4;
+    while (vs > 0 && ((row_bytes & ((1 << vs) - 1)) || (reinterpret_cast<uintptr_t>(a) & ((1 << vs) - 1)) ||
+                      (reinterpret_cast<uintptr_t>(b) & ((1 << vs) - 1))))
+        --vs;
+    return vs;
+}
+
 }  // namespace tgl
 
 struct tgl_tcsr {

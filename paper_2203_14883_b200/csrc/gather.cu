@@ -33,14 +33,6 @@ struct GatherParams {
     GatherTable t[TGL_MAX_GATHER_TABLES];
 };
 
-template <int VS>
-struct Vec;
-template <> struct Vec<4> { using T = uint4; };
-template <> struct Vec<3> { using T = uint2; };
-template <> struct Vec<2> { using T = uint32_t; };
-template <> struct Vec<1> { using T = uint16_t; };
-template <> struct Vec<0> { using T = uint8_t; };
-
 constexpr int kGatherThreads = 256;
 constexpr int kUnroll = 4;
 
