@@ -138,20 +138,54 @@ def gather_bytes(cfg: C.Workload, n_roots: int, nnz: int) -> int:
     return 2 * ((n_roots + nnz) * node_row + nnz * edge_row)
 
 
+def state_bytes(cfg: C.Workload, n_events: int) -> int:
+    """Algorithmic bytes of the C3 state write (Fig. 2 step 6): per event read its id + time (8 B)
+    and its new memory / mail rows, write them and the two timestamps into the node tables."""
+    node_row = sum(4 * cols for name, (rows, cols) in cfg.tables.items() if name in ("memory", "mailbox"))
+    return n_events * (8 + 2 * node_row + 2 * 4)
+
+
+def chunk_events(s0: int, r: torch.Tensor, t: torch.Tensor):
+    """The events of Fig. 2 step 6 in a root chunk: the positive-edge endpoints (src_i, dst_i at
+    ts_i; root stream R#16 = (src_i, dst_i, neg_i) per edge), in batch order.  Input setup."""
+    j = torch.arange(r.numel(), device=r.device)
+    keep = ((s0 + j) % 3) != 2
+    return r[keep].contiguous(), t[keep].contiguous()
+
+
+def state_write_launches(tgl, cfg, K: int = 1) -> int:
+    """Kernels of one tgl_state_write: keys + passes x (upsweep + 3 scan + downsweep) + slot + copy."""
+    bits = max(1, int(cfg.n_nodes).bit_length())
+    return 1 + 5 * max(1, (bits + 7) // 8) + 2 + (1 if K > 1 else 0)
+
+
 def make_gather(tgl, cfg, sampler, dev):
-    """C3 step 2 of Fig. 2: memory, mem_ts, mailbox, mail_ts for the roots and sampled
-    neighbours, edge features for the sampled eids -- preallocated outputs, device-side counts."""
+    """C3 data path of Fig. 2: step 2 -- memory, mem_ts, mailbox, mail_ts for the roots
+    and sampled neighbours, edge features for the sampled eids (preallocated outputs, device-side
+    counts) -- and step 6 -- the batch's events write their new memory (mem_ts) and mail (mail_ts)
+    into the node tables (tgl_state_write, K = 1, R#25).  The new rows are the memory updater's /
+    mail builder's outputs (model code, out of scope): resident synthetic rows stand in."""
     tabs = C.tables(cfg, device=dev)
     node_tabs = [tabs[k] for k in ("memory", "mem_ts", "mailbox", "mail_ts")]
     cap_r, cap_e = sampler.roots_cap[0], sampler.edges_cap[0]
     out_r = [torch.empty((cap_r,) + tuple(t.shape[1:]), dtype=t.dtype, device=dev) for t in node_tabs]
     out_n = [torch.empty((cap_e,) + tuple(t.shape[1:]), dtype=t.dtype, device=dev) for t in node_tabs]
     out_e = [torch.empty((cap_e, tabs["edge_feat"].shape[1]), dtype=torch.float32, device=dev)]
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(cfg.seed)
+    new_mem = torch.randn((cap_r, tabs["memory"].shape[1]), generator=gen, device=dev)
+    new_mail = torch.randn((cap_r, tabs["mailbox"].shape[1]), generator=gen, device=dev)
+    writer = tgl.StateWriter(cfg.n_nodes, cap_r, device=dev)
 
-    def run(roots, block):
+    def run(roots, block, events=None):
         tgl.gather(roots, node_tabs, outs=out_r)
         tgl.gather(block.nbr, node_tabs, n_ids_dev=block.nnz_dev, outs=out_n)
         tgl.gather(block.eid, [tabs["edge_feat"]], n_ids_dev=block.nnz_dev, outs=out_e)
+        if events is not None:
+            ids, ets = events
+            n = ids.numel()
+            writer(ids, ets, [(new_mem[:n], tabs["memory"]), (new_mail[:n], tabs["mailbox"]), (ets, tabs["mail_ts"])],
+                   K=1, ts_table=tabs["mem_ts"])
     return run
 
 
@@ -381,14 +415,19 @@ def run_ours(args):
     L, S = len(cfg.fanouts), cfg.n_snapshots
     launches_per_step = 2 * (1 + (L - 1) * S)  # window + copy kernel per chain (+1 memset, not ours)
     gather = make_gather(tgl, cfg, sampler, dev) if cfg.tables else None
+    events = {}
     if gather is not None:
-        launches_per_step += 3  # node tables by roots, node tables by nbr, edge features by eid
+        # node tables by roots, node tables by nbr, edge features by eid; the state write
+        launches_per_step += 3 + state_write_launches(tgl, cfg)
+        for (r, t), s0 in zip(chunks, mine):
+            if id(r) not in events:
+                events[id(r)] = chunk_events(s0, r, t)
 
     def step(j):
         r, t = chunks[j]
         blocks = sampler.run(r, t, seed=cfg.sampler_seed, root_key_base=mine[j])
         if gather is not None:
-            gather(r, blocks[0])
+            gather(r, blocks[0], events[id(r)])
         return blocks
 
     for w in range(args.warmup):
@@ -427,7 +466,7 @@ def run_ours(args):
         roots_total += nr[0]
         bytes_total += algorithmic_bytes(cfg, nr, nz)
         if gather is not None:
-            bytes_total += gather_bytes(cfg, nr[0], nz[0])
+            bytes_total += gather_bytes(cfg, nr[0], nz[0]) + state_bytes(cfg, events[id(r)][0].numel())
     err = tgl.check(g)
 
     edges_all, bytes_all, total_ms_max = reduce_report(edges_total, bytes_total, total_ms, world, dev)
@@ -456,9 +495,11 @@ def run_ours(args):
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic, "traffic_source": traffic_src, "peak_source": peak_src,
                      "kernel": (f"tgl_sample ({cfg.strategy}): window_kernel + copy_kernel"
-                                + (" + tgl_gather (3 launches)" if gather is not None else "") + ", timed together"),
+                                + (" + tgl_gather (3 launches) + tgl_state_write" if gather is not None else "")
+                                + ", timed together"),
                      "bytes_model": "SURVEY 8(d): per root 8+16+8*cuts+8*S, per edge 24 (+4 ts_edge if l<L-1)"
-                                    + ("; gather: 2 x row bytes per gathered id" if gather is not None else ""),
+                                    + ("; gather: 2 x row bytes per gathered id; state write: 8 + 2 x (memory + mail "
+                                       "row) + 8 B per event" if gather is not None else ""),
                      "algorithmic_bytes_per_step": bytes_total / args.steps,
                      "l2_resident": tcsr_bytes < l2_bytes,
                      "note": ("T-CSR + gather node tables fit the 126 MB L2: algorithmic bytes are mostly L2 "
@@ -479,7 +520,8 @@ def run_ours(args):
     # end to end through the public API with host buffers (rank-local), copies inside the region
     if not args.no_e2e:
         gf = (lambda smp: make_gather(tgl, cfg, smp, dev)) if gather is not None else None
-        out["e2e"] = e2e(args, tgl, sampler, chunks, mine, cfg, dev, world, gather_factory=gf)
+        out["e2e"] = e2e(args, tgl, sampler, chunks, mine, cfg, dev, world, gather_factory=gf,
+                         events=events if gather is not None else None)
         out["e2e_full_d2h"] = e2e(args, tgl, sampler, chunks, mine, cfg, dev, world, full_d2h=True)
 
     # CPU oracle baseline + parity spot check (rank 0, N = 1 only)
@@ -540,7 +582,7 @@ def per_batch(args, tgl, g, cfg, chunk, key0, dev, world, n_graph=64, reps=10):
                     "launch-latency bound; the headline value is epoch mode"}
 
 
-def e2e(args, tgl, sampler, chunks, mine, cfg, dev, world, full_d2h=False, gather_factory=None):
+def e2e(args, tgl, sampler, chunks, mine, cfg, dev, world, full_d2h=False, gather_factory=None, events=None):
     """End to end through the public API with host buffers, copies inside the timed region.
 
     Per step: pinned host roots -> H2D (copy stream) -> tgl_sample (compute stream) -> D2H of the
@@ -555,7 +597,13 @@ def e2e(args, tgl, sampler, chunks, mine, cfg, dev, world, full_d2h=False, gathe
         if id(r) not in pinned:
             pinned[id(r)] = (r.cpu().pin_memory(), t.cpu().pin_memory())
     host = [pinned[id(r)] for r, _ in chunks]
+    host_ev = None
+    if events is not None:  # step-6 events travel with their roots
+        pin_ev = {k: (a.cpu().pin_memory(), b.cpu().pin_memory()) for k, (a, b) in events.items()}
+        host_ev = [pin_ev[id(r)] for r, _ in chunks]
     cap_r = chunks[0][0].numel()
+    d_ev = [(torch.empty(cap_r, dtype=torch.int32, device=dev), torch.empty(cap_r, dtype=torch.float32, device=dev))
+            for _ in range(2)] if events is not None else None
     nb = L * S
     smps = [sampler, tgl.Sampler(sampler.g, cap_r, cfg.fanouts, cfg.strategy, S, cfg.snapshot_len)]
     gathers = [gather_factory(smp) for smp in smps] if gather_factory is not None else None
@@ -586,6 +634,11 @@ def e2e(args, tgl, sampler, chunks, mine, cfg, dev, world, full_d2h=False, gathe
                     copy_s.wait_event(roots_free[slot])
                 dr.copy_(r, non_blocking=True)
                 dt_.copy_(t, non_blocking=True)
+                if host_ev is not None:
+                    ne = host_ev[j][0].numel()
+                    d_ev[slot][0][:ne].copy_(host_ev[j][0], non_blocking=True)
+                    d_ev[slot][1][:ne].copy_(host_ev[j][1], non_blocking=True)
+                    stats["h2d"] += ne * 8
                 h2d_done = torch.cuda.Event()
                 h2d_done.record(copy_s)
             comp.wait_event(h2d_done)
@@ -593,7 +646,11 @@ def e2e(args, tgl, sampler, chunks, mine, cfg, dev, world, full_d2h=False, gathe
                 comp.wait_event(outs_free[slot])
             blocks = smps[slot].run(dr, dt_, seed=cfg.sampler_seed, root_key_base=mine[j])
             if gathers is not None:
-                gathers[slot](dr, blocks[0])
+                ev = None
+                if host_ev is not None:
+                    ne = host_ev[j][0].numel()
+                    ev = (d_ev[slot][0][:ne], d_ev[slot][1][:ne])
+                gathers[slot](dr, blocks[0], ev)
             for q, b in enumerate(blocks):
                 cnt_h[slot][2 * q:2 * q + 1].copy_(b.n_roots_dev, non_blocking=True)
                 cnt_h[slot][2 * q + 1:2 * q + 2].copy_(b.nnz_dev, non_blocking=True)
@@ -677,7 +734,8 @@ def cpu_baseline(args, cfg, src, dst, ts, tgl, g, sampler, chunks, mine):
     return ({"value": res["edges"] / res["seconds"], "unit": UNIT, "cores": cores, "kind": "oracle",
              "sample": f"{res['batches']} consecutive batches x {B} roots ({res['roots']:,} roots, "
                        f"{res['edges']:,} sampled edges) from timed step 0, single-threaded C oracle "
-                       f"(-O2 -ffp-contract=off) on a T-CSR restricted to the sampled nodes",
+                       f"(-O2 -ffp-contract=off) on a T-CSR restricted to the sampled nodes"
+                       + (" (sampler only: the oracle's gather / state write are not timed)" if cfg.tables else ""),
              "seconds": res["seconds"], "oracle_x_threads": res["threads"]},
             {"checked_roots": checked, "bit_exact": bool(ok), "against": "oracle/ (CPU), same batches"})
 
