@@ -10,6 +10,7 @@
  *   tgl_state_write  node memory / mailbox update       Fig. 2 step 6 (L201), mailbox of the K
  *                                                      most recent mails (L210, L322)
  *   tgl_shard_*      node-sharded exchange helpers      (not in the paper)
+ *   tgl_chunk_schedule  random chunk scheduling         Alg. 2 (L274-L291)
  *
  * Conventions (every entry point):
  *   - Data pointers are DEVICE pointers unless marked (host).  `stream` is a cudaStream_t passed
@@ -284,6 +285,21 @@ TGL_API int tgl_state_write_workspace(int64_t n_events, int32_t n_nodes, size_t 
 TGL_API int tgl_state_write(const int32_t *ids, const float *ts, int64_t n_events, int32_t n_nodes, int32_t K,
                     int32_t *pos, float *ts_table, const tgl_state_table *tables /* host [n_tables] */,
                     int32_t n_tables, void *workspace, size_t ws_bytes, void *stream);
+
+/* ------------------------------------------------------------------ training schedule (Alg. 2) */
+
+/*
+ * Random chunk scheduling (Alg. 2), reading R#26: the mini-batches of epoch `epoch`
+ * over the chronological training edges [0, n_edges).  The first batch starts at e_s = r * cs,
+ * r = floor(x * (bs / cs) / 2^32) with x = Philox4x32-10 word 0 of counter (epoch_lo, epoch_hi,
+ * 0x414C4732, 0) under key (seed_lo, seed_hi); batch b covers edges [e_s + b*bs, e_s + (b+1)*bs)
+ * "while e_e <= |E|".  Writes first_edge[b] (device int64 [cap]) for b < min(nb, cap) and
+ * *n_batches = nb (device int64) -- the batch's roots are then (src_i, dst_i, neg_i) of its edges.
+ * Errors: TGL_EINVAL unless 0 < chunk_size <= batch_size, n_edges >= 0; TGL_ECAPACITY if
+ * cap < n_edges / batch_size.
+ */
+TGL_API int tgl_chunk_schedule(int64_t n_edges, int64_t batch_size, int64_t chunk_size, uint64_t epoch,
+                       uint64_t seed, int64_t *first_edge, int64_t cap, int64_t *n_batches, void *stream);
 
 /* ------------------------------------------------------------------ errors */
 

@@ -267,3 +267,22 @@ def state_write(ids, ts, *, n_nodes: int, K: int, tables, pos=None, ts_table=Non
     if pos is not None:
         pos[:] = last
     return int(err[0])
+
+
+# --------------------------------------------------------------------------- Alg. 2
+def chunk_schedule(n_edges: int, bs: int, cs: int, epoch: int, seed: int) -> List[int]:
+    """Random chunk scheduling, Alg. 2, reading R#26: per epoch the first batch
+    starts at e_s = r * cs, r uniform in [0, bs // cs) (Philox word 0, counter (epoch_lo, epoch_hi,
+    0x414C4732, 0), key = seed); batches are [e_s + b*bs, e_s + (b+1)*bs) while the end <= |E|.
+    Returns the first edge of every batch of the epoch, in order."""
+    if bs <= 0 or cs <= 0 or cs > bs or n_edges < 0 or epoch < 0:
+        raise ValueError("need 0 < cs <= bs, n_edges >= 0, epoch >= 0")
+    ctr = np.array([epoch & 0xFFFFFFFF, (epoch >> 32) & 0xFFFFFFFF, 0x414C4732, 0], dtype=np.uint32)
+    key = np.array([seed & 0xFFFFFFFF, (seed >> 32) & 0xFFFFFFFF], dtype=np.uint32)
+    x = int(philox4x32_10(ctr, key)[0])
+    r = (x * (bs // cs)) >> 32
+    e_s, out = r * cs, []
+    while e_s + bs <= n_edges:          # "while e_e <= |E|"
+        out.append(e_s)
+        e_s += bs
+    return out

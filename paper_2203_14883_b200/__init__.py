@@ -329,6 +329,18 @@ def state_write(ids, ts, tables, *, n_nodes: int, K: int = 1, pos=None, ts_table
                                                                  stream=stream)
 
 
+def chunk_schedule(n_edges: int, batch_size: int, chunk_size: int, epoch: int, seed: int, device="cuda",
+                   stream=None):
+    """tgl_chunk_schedule (Alg. 2, R#26): (first_edge int64 [cap] device, n_batches int64 [1] device)
+    -- the first nb entries are the epoch's batch starts (no host sync)."""
+    cap = max(int(n_edges) // int(batch_size), 1)
+    first = torch.empty(cap, dtype=torch.int64, device=device)
+    nb = torch.empty(1, dtype=torch.int64, device=device)
+    _rc(_L.tgl_chunk_schedule(int(n_edges), int(batch_size), int(chunk_size), int(epoch), int(seed) & 0xFFFFFFFFFFFFFFFF,
+                              _ptr(first), cap, _ptr(nb), _stream(stream)), "tgl_chunk_schedule")
+    return first, nb
+
+
 def check(g: Optional[TCSR] = None, stream=None) -> int:
     """tgl_check: synchronise and return (and clear) the sticky device error code (0 = none)."""
     return _L.tgl_check(None if g is None else g.handle, _stream(stream))

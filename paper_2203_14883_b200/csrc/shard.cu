@@ -115,3 +115,38 @@ extern "C" int tgl_shard_unpermute(const int32_t* perm, int64_t n_roots, const i
                                                           nbr_out, eid_out, dt_out);
     return cudaGetLastError() == cudaSuccess ? TGL_OK : TGL_ECUDA;
 }
+
+// ---------------------------------------------------------------------------- Alg. 2 schedule
+// Random chunk scheduling (Alg. 2; R#26): the first batch of epoch
+// e starts at e_s = r * cs, r = floor(x * (bs / cs) / 2^32), x = Philox4x32-10 word 0 of counter
+// (e_lo, e_hi, 0x414C4732, 0) under key = seed; batch b covers edges [e_s + b bs, e_s + (b+1) bs)
+// while its end <= |E|.  One small kernel writes the batch starts and their count on the device.
+namespace tgl {
+__global__ void chunk_schedule_kernel(int64_t n_edges, int64_t bs, int64_t cs, uint64_t epoch, uint32_t seed_lo,
+                                      uint32_t seed_hi, int64_t* __restrict__ first_edge, int64_t cap,
+                                      int64_t* __restrict__ n_batches) {
+    const uint4 x = philox4x32_10(make_uint4((uint32_t)epoch, (uint32_t)(epoch >> 32), 0x414C4732u, 0u), seed_lo,
+                                  seed_hi);
+    const int64_t r = (int64_t)(((uint64_t)x.x * (uint64_t)(bs / cs)) >> 32);
+    const int64_t e_s = r * cs;
+    const int64_t nb = n_edges >= e_s + bs ? (n_edges - e_s) / bs : 0;
+    const int64_t m = nb < cap ? nb : cap;
+    for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < m; b += (int64_t)gridDim.x * blockDim.x)
+        first_edge[b] = e_s + b * bs;
+    if (blockIdx.x == 0 && threadIdx.x == 0) *n_batches = nb;
+}
+}  // namespace tgl
+
+extern "C" int tgl_chunk_schedule(int64_t n_edges, int64_t batch_size, int64_t chunk_size, uint64_t epoch,
+                                  uint64_t seed, int64_t* first_edge, int64_t cap, int64_t* n_batches, void* stream) {
+    if (n_edges < 0 || batch_size <= 0 || chunk_size <= 0 || chunk_size > batch_size || cap < 0 || !n_batches)
+        return TGL_EINVAL;
+    if (cap > 0 && !first_edge) return TGL_EINVAL;
+    if (cap < n_edges / batch_size) return TGL_ECAPACITY;
+    int rc = check_device();
+    if (rc) return rc;
+    const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>((cap + 255) / 256, 148 * 4));
+    chunk_schedule_kernel<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(
+        n_edges, batch_size, chunk_size, epoch, (uint32_t)seed, (uint32_t)(seed >> 32), first_edge, cap, n_batches);
+    return cudaGetLastError() == cudaSuccess ? TGL_OK : TGL_ECUDA;
+}

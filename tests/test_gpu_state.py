@@ -70,3 +70,14 @@ def test_state_write_empty_and_errors(tgl):
     assert L_.tgl_state_write(ids.data_ptr(), None, 3, 10, 0, None, None, None, 0, ws.data_ptr(), 1 << 20, None) == -1
     assert L_.tgl_state_write(ids.data_ptr(), None, 3, 10, 4, None, None, None, 0, ws.data_ptr(), 1 << 20, None) == -1
     assert L_.tgl_state_write(ids.data_ptr(), None, 3, 10, 1, None, None, None, 0, ws.data_ptr(), 16, None) == -5
+
+
+def test_chunk_schedule_equals_oracle(tgl):
+    """tgl_chunk_schedule (Alg. 2, R#26) vs the oracle's schedule, over epochs and shapes."""
+    for n, bs, cs in [(157_474, 600, 100), (1_000_000, 4000, 250), (599, 600, 100), (0, 8, 2), (10_000, 600, 600)]:
+        for epoch in (0, 1, 2, 77, 2**33 + 5):
+            first, nb = tgl.chunk_schedule(n, bs, cs, epoch, seed=42)
+            want = oracle.chunk_schedule(n, bs, cs, epoch, seed=42)
+            k = int(nb.item())
+            assert k == len(want)
+            np.testing.assert_array_equal(first[:k].cpu().numpy(), np.array(want, dtype=np.int64))
