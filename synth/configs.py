@@ -108,6 +108,10 @@ CONFIGS: Dict[str, Workload] = {
                    0x54474C00 + 4, 1.8e5),
     "C5": Workload("mag-shaped", 121_000_000, 1_300_000_000, True, [10], "most_recent", 3, 5.0, 4_000,
                    0x54474C00 + 5, 120.0),
+    # DySAT's sampler workload of Table 4 on the C1 graph --
+    # 2-layer uniform within 3 dynamic snapshots of 10,000 s; exercises reading R#3
+    "C6": Workload("wikipedia-dysat", 9_227, 157_474, True, [10, 10], "uniform", 3, 10_000.0, 600,
+                   0x54474C00 + 1, 2.7e6, bipartite_split=8_227),
 }
 
 
@@ -224,7 +228,7 @@ def _mag_chunk(cfg: Workload, lo: int, hi: int, dev) -> tuple:
 
 
 _CHUNKERS = {"C1": _bipartite_chunk, "C2": _bipartite_chunk, "C3": _bipartite_chunk, "C4": _gdelt_chunk,
-             "C5": _mag_chunk}
+             "C5": _mag_chunk, "C6": _bipartite_chunk}
 
 
 def edge_chunk(key: str, cfg: Workload, lo: int, hi: int, device="cpu"):

@@ -97,7 +97,7 @@ def _compare_call(tgl, cfg, g_gpu, g_orc, src, dst, ts, batches):
             assert root_off[q] == len(got[q][0]) - 1 and edge_off[q] == len(got[q][1])
 
 
-@pytest.mark.parametrize("key", ["C1", "C2", "C3"])
+@pytest.mark.parametrize("key", ["C1", "C2", "C3", "C6"])
 def test_small_configs_full_tcsr_and_batches(tgl, key):
     cfg = C.CONFIGS[key]
     src, dst, ts = C.edges(key, cfg, device="cuda")
