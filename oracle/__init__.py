@@ -194,7 +194,7 @@ def sample_block(g: TCSR, root_node, root_ts, root_key, root_lo, *, layer: int, 
 
 def sample(g: TCSR, roots, root_ts, *, fanouts: List[int], strategy: int, n_snapshots: int = 1,
            snapshot_len: float = math.inf, seed: int = 0, root_key_base: int = 0,
-           hop_time: str = "edge", replacement: bool = False) -> List[dict]:
+           hop_time: str = "edge", replacement: bool = False, dedup: bool = False) -> List[dict]:
     """Alg. 1: L x S blocks, block (l, s) at index l*S + s.
 
     Layer-0 roots are the caller's; the roots of block (l, s), l >= 1, are the outputs
@@ -203,10 +203,17 @@ def sample(g: TCSR, roots, root_ts, *, fanouts: List[int], strategy: int, n_snap
     Variants: hop_time="root" -- hop roots carry their parent's root time
     instead of the sampled edge's ("others use the root's timestamp", R#23);
     replacement=True -- uniform draws with replacement (R#24).
+    dedup=True (R#27, SPEC's MFG): every block also lists the distinct (node, hop time) pairs of its
+    outputs in order of first appearance (uniq_node, uniq_ts, bit-exact equality of the time) with
+    src_index[i] = the pair of output i; the next layer's roots are that list, each keyed by its
+    first occurrence's child key.  Not defined with inherited finite lower bounds (L > 1 with a
+    finite snapshot length): different windows would merge.
     """
     if hop_time not in ("edge", "root"):
         raise ValueError("hop_time must be 'edge' or 'root'")
     L, S = len(fanouts), int(n_snapshots)
+    if dedup and L > 1 and math.isfinite(snapshot_len):
+        raise ValueError("dedup needs S == 1 or an infinite snapshot length when L > 1 (R#27)")
     root_node = np.ascontiguousarray(np.asarray(roots, dtype=np.int32))
     root_ts = np.ascontiguousarray(np.asarray(root_ts, dtype=np.float32))
     n = len(root_node)
@@ -218,13 +225,32 @@ def sample(g: TCSR, roots, root_ts, *, fanouts: List[int], strategy: int, n_snap
         for l in range(L):
             want = l < L - 1
             b = sample_block(g, rn, rt, rk, rlo, layer=l, snapshot=s, snapshot_len=snapshot_len,
-                             k=fanouts[l], strategy=strategy, seed=seed, want_children=want,
+                             k=fanouts[l], strategy=strategy, seed=seed, want_children=want or dedup,
                              replacement=replacement)
-            blocks[l * S + s] = b
-            if want:
+            if want or dedup:
                 # R#4 / R#23: the hop root's time is the sampled edge's, or its parent root's
                 t_next = b["ts_edge"] if hop_time == "edge" else np.repeat(rt, np.diff(b["offsets"]))
-                rn, rt, rk = b["nbr"], np.ascontiguousarray(t_next, dtype=np.float32), b["child_key"]
+                t_next = np.ascontiguousarray(t_next, dtype=np.float32)
+            if dedup:
+                first, src_index = {}, np.zeros(len(b["nbr"]), dtype=np.int32)
+                order = []
+                for i, (v, tb) in enumerate(zip(b["nbr"].tolist(), t_next.view(np.uint32).tolist())):
+                    if (v, tb) not in first:
+                        first[(v, tb)] = len(order)
+                        order.append(i)
+                    src_index[i] = first[(v, tb)]
+                order = np.array(order, dtype=np.int64)
+                b["src_index"], b["uniq_node"], b["uniq_ts"] = src_index, b["nbr"][order], t_next[order]
+                b["uniq_key"] = b["child_key"][order]
+                if not want:
+                    for key in ("ts_edge", "child_key", "child_lo"):
+                        b.pop(key, None)
+            blocks[l * S + s] = b
+            if want:
+                if dedup:
+                    rn, rt, rk = b["uniq_node"], b["uniq_ts"], b["uniq_key"]
+                else:
+                    rn, rt, rk = b["nbr"], t_next, b["child_key"]
                 rlo = b["child_lo"] if need_lo else None
     return blocks
 

@@ -68,7 +68,7 @@ def with_replacement(c: int, k: int, seed: int, layer: int, snapshot: int, rk: i
 
 def sample(src, dst, ts, eid, *, n_nodes: int, add_reverse: bool, roots, root_ts, fanouts,
            strategy: int, n_snapshots: int = 1, snapshot_len: float = math.inf, seed: int = 0,
-           root_key_base: int = 0, hop_time: str = "edge", replacement: bool = False):
+           root_key_base: int = 0, hop_time: str = "edge", replacement: bool = False, dedup: bool = False):
     """Returns blocks[l*S+s] = list over roots of lists of (nbr, eid, dt, ts_edge)."""
     owner, nbr, tsl, eidl = logical_stream(src, dst, ts, eid, add_reverse)
     f32 = np.float32
@@ -110,6 +110,13 @@ def sample(src, dst, ts, eid, *, n_nodes: int, add_reverse: bool, roots, root_ts
                                 Lo if math.isfinite(snapshot_len) else None))
                 out.append(row)
             blocks[l * S + s] = out
+            if dedup:  # R#27: distinct (node, time bits) in first-appearance order, first key wins
+                seen, uniq = set(), []
+                for (v, t, rk, lo) in nxt:
+                    if (v, np.float32(t).view(np.uint32).item()) not in seen:
+                        seen.add((v, np.float32(t).view(np.uint32).item()))
+                        uniq.append((v, t, rk, lo))
+                nxt = uniq
             cur = nxt
     return blocks
 

@@ -99,3 +99,31 @@ def test_with_replacement_draws_uniform():
                       replacement=True)[0]
     rows = b["eid"].reshape(100, 6)
     assert np.all(np.diff(rows, axis=1) >= 0) and np.any(np.diff(rows, axis=1) == 0)
+
+
+@pytest.mark.parametrize("hop_time", ["edge", "root"])
+def test_dedup_matches_brute_force(hop_time):
+    """R#27: with dedup the hop roots are the distinct (node, time) pairs; the brute force builds
+    them with a set over its own scan of the logical stream."""
+    rng = np.random.default_rng(77 + (hop_time == "root"))
+    for case in range(60):
+        n_nodes = int(rng.integers(1, 30))
+        src, dst, ts, eid = random_graph(700 + case, n_nodes, int(rng.integers(0, 300)), integer_times=True,
+                                         t_max=8.0)  # few distinct times: many duplicate pairs
+        roots, rts = random_roots(700 + case, n_nodes, int(rng.integers(1, 30)), integer_times=True, t_max=8.0)
+        L = 1 + case % 3
+        fanouts = [int(rng.integers(1, 6)) for _ in range(L)]
+        strategy = int(rng.integers(0, 2))
+        S = 1 if L > 1 else int(rng.integers(1, 4))
+        t_s = math.inf if S == 1 else 2.5
+        seed, base = int(rng.integers(0, 2**63)), int(rng.integers(0, 2**40))
+        g = oracle.build(src, dst, ts, eid, n_nodes=n_nodes, add_reverse=bool(case % 2))
+        blocks = oracle.sample(g, roots, rts, fanouts=fanouts, strategy=strategy, n_snapshots=S, snapshot_len=t_s,
+                               seed=seed, root_key_base=base, hop_time=hop_time, dedup=True)
+        bf = brute.sample(src, dst, ts, eid, n_nodes=n_nodes, add_reverse=bool(case % 2), roots=roots, root_ts=rts,
+                          fanouts=fanouts, strategy=strategy, n_snapshots=S, snapshot_len=t_s, seed=seed,
+                          root_key_base=base, hop_time=hop_time, dedup=True)
+        _compare(blocks, bf)
+        for b in blocks:  # src_index maps every output to its (node, time) pair
+            assert np.array_equal(b["uniq_node"][b["src_index"]], b["nbr"])
+            assert len(set(zip(b["uniq_node"].tolist(), b["uniq_ts"].view(np.uint32).tolist()))) == len(b["uniq_node"])
