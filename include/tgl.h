@@ -217,21 +217,47 @@ TGL_API int tgl_sample_keyed(const tgl_tcsr *g, const int32_t *roots, const floa
  *   reserved     must be zero.
  * root_keys: NULL -> root_key_base + i (as tgl_sample), else explicit keys (as tgl_sample_keyed).
  * opts: host pointer or NULL (all defaults).  Errors: TGL_EINVAL for an unknown hop_time,
- * replacement != 0 with TGL_MOST_RECENT, or non-zero reserved words; otherwise as tgl_sample.
- * The workspace size of tgl_sample_capacity() covers every option.
+ * replacement != 0 with TGL_MOST_RECENT, dedup without dedup blocks, or non-zero reserved words;
+ * otherwise as tgl_sample.  The workspace size of tgl_sample_capacity() covers hop_time and
+ * replacement; dedup needs tgl_sample_capacity_ex().
  */
 typedef enum { TGL_HOP_EDGE_TIME = 0, TGL_HOP_ROOT_TIME = 1 } tgl_hop_time;
 typedef struct {
     int32_t hop_time;     /* tgl_hop_time */
     int32_t replacement;  /* 0 or 1 */
-    int32_t reserved[6];
+    int32_t dedup;        /* 0 or 1: per-block distinct (node, hop time) lists (R#27), see below */
+    int32_t reserved[5];
 } tgl_sample_options;
+
+/*
+ * dedup = 1 (R#27, SPEC's message-flow-graph node lists): for every block (l, s) the library also
+ * writes, into dedup[l*S + s], the distinct (node, hop time) pairs of the block's outputs in order
+ * of first appearance (hop time = ts_edge, or the root time under TGL_HOP_ROOT_TIME; equality on
+ * the fp32 bit pattern), src_index[i] = the pair of output i, and *n_uniq_dev.  Layer l+1 then
+ * samples only those pairs, each with its first occurrence's key (R#7): no redundant sampling or
+ * gathering of repeated (node, time) roots.  Requires ts_edge for every layer (edge-time mode) and
+ * is not defined for L > 1 with a finite snapshot length (TGL_EINVAL): inherited windows differ.
+ * The workspace must come from tgl_sample_capacity_ex() with the same options.
+ */
+typedef struct {
+    int64_t cap;            /* in: >= edges_cap[l] */
+    int32_t *src_index;     /* [nnz] index of output i's pair in uniq_* */
+    int32_t *uniq_node;     /* [n_uniq] */
+    float *uniq_ts;         /* [n_uniq] */
+    int64_t *n_uniq_dev;    /* out: device scalar */
+} tgl_dedup_block;
+
+TGL_API int tgl_sample_capacity_ex(int64_t n_roots, int32_t n_layers, const int32_t *fanouts /* host [L] */,
+                           int32_t n_snapshots, tgl_strategy strategy, float snapshot_len,
+                           const tgl_sample_options *opts /* host or NULL */, int64_t *roots_cap /* host [L] */,
+                           int64_t *edges_cap /* host [L] */, size_t *ws_bytes /* host */);
 
 TGL_API int tgl_sample_ex(const tgl_tcsr *g, const int32_t *roots, const float *root_ts,
                   const uint64_t *root_keys /* device [n_roots] or NULL */, int64_t n_roots, int32_t n_layers,
                   const int32_t *fanouts /* host [L] */, tgl_strategy strategy, int32_t n_snapshots,
                   float snapshot_len, uint64_t seed, uint64_t root_key_base,
                   const tgl_sample_options *opts /* host or NULL */, tgl_block *out /* host [L*S] */,
+                  const tgl_dedup_block *dedup /* host [L*S], required iff opts->dedup */,
                   void *workspace, size_t ws_bytes, void *stream);
 
 /* ------------------------------------------------------------------ gather (Fig. 2 step 2) */

@@ -162,6 +162,11 @@ class Block:
     ts_edge: Optional[torch.Tensor]
     n_roots_dev: torch.Tensor
     nnz_dev: torch.Tensor
+    # dedup (R#27): distinct (node, hop time) pairs of the outputs, first appearance order
+    src_index: Optional[torch.Tensor] = None
+    uniq_node: Optional[torch.Tensor] = None
+    uniq_ts: Optional[torch.Tensor] = None
+    n_uniq_dev: Optional[torch.Tensor] = None
 
     def trimmed(self):
         """Host-synchronising view: (offsets[:n+1], nbr[:nnz], eid[:nnz], dt[:nnz], ts_edge[:nnz])."""
@@ -175,14 +180,18 @@ class Sampler:
 
     def __init__(self, g: TCSR, max_roots: int, fanouts: Sequence[int], strategy="most_recent",
                  n_snapshots: int = 1, snapshot_len: float = math.inf, device=None, want_ts_edge_last=False,
-                 hop_time: str = "edge", replacement: bool = False):
+                 hop_time: str = "edge", replacement: bool = False, dedup: bool = False):
         """hop_time: "edge" (R#4) or "root" (R#23, hop roots carry the root time); replacement:
-        uniform with replacement (R#24).  Both map to tgl_sample_ex's options."""
+        uniform with replacement (R#24); dedup: per-block distinct (node, hop time) lists feeding
+        the next layer (R#27).  All map to tgl_sample_ex's options."""
         self.g = g
         if hop_time not in ("edge", "root"):
             raise ValueError("hop_time must be 'edge' or 'root'")
-        self._opts = _lib.SampleOptions(1 if hop_time == "root" else 0, 1 if replacement else 0)
-        self._default_opts = hop_time == "edge" and not replacement
+        self._opts = _lib.SampleOptions(1 if hop_time == "root" else 0, 1 if replacement else 0, 1 if dedup else 0)
+        self._default_opts = hop_time == "edge" and not replacement and not dedup
+        self.dedup = bool(dedup)
+        if dedup and hop_time == "edge":
+            want_ts_edge_last = True
         self.fanouts = [int(k) for k in fanouts]
         self.L, self.S = len(self.fanouts), int(n_snapshots)
         self.strategy = _strategy(strategy)
@@ -206,6 +215,18 @@ class Sampler:
                     dt=torch.empty(ec_[l], dtype=torch.float32, device=dev),
                     ts_edge=torch.empty(ec_[l], dtype=torch.float32, device=dev) if need_ts else None,
                     n_roots_dev=scal[2 * j: 2 * j + 1], nnz_dev=scal[2 * j + 1: 2 * j + 2]))
+        self._c_dedup = None
+        if dedup:
+            uscal = torch.zeros(self.L * self.S, dtype=torch.int64, device=dev)
+            self._c_dedup = (_lib.DedupBlock * len(self.blocks))()
+            for j, b in enumerate(self.blocks):
+                l = j // self.S
+                b.src_index = torch.empty(ec_[l], dtype=torch.int32, device=dev)
+                b.uniq_node = torch.empty(ec_[l], dtype=torch.int32, device=dev)
+                b.uniq_ts = torch.empty(ec_[l], dtype=torch.float32, device=dev)
+                b.n_uniq_dev = uscal[j:j + 1]
+                self._c_dedup[j] = _lib.DedupBlock(ec_[l], b.src_index.data_ptr(), b.uniq_node.data_ptr(),
+                                                   b.uniq_ts.data_ptr(), b.n_uniq_dev.data_ptr())
         self._c_blocks = (_lib.Block * len(self.blocks))()
         for j, b in enumerate(self.blocks):
             l = j // self.S
@@ -219,8 +240,8 @@ class Sampler:
         ec_ = (ctypes.c_int64 * self.L)()
         wsb = ctypes.c_size_t()
         fan = (ctypes.c_int32 * self.L)(*self.fanouts)
-        _rc(_L.tgl_sample_capacity(int(n_roots), self.L, fan, self.S, self.strategy, self.snapshot_len, rc_, ec_,
-                                   ctypes.byref(wsb)), "tgl_sample_capacity")
+        _rc(_L.tgl_sample_capacity_ex(int(n_roots), self.L, fan, self.S, self.strategy, self.snapshot_len,
+                                      ctypes.byref(self._opts), rc_, ec_, ctypes.byref(wsb)), "tgl_sample_capacity_ex")
         return list(rc_), list(ec_), wsb.value
 
     def run(self, roots: torch.Tensor, root_ts: torch.Tensor, *, seed: int = 0, root_key_base: int = 0,
@@ -237,8 +258,8 @@ class Sampler:
                 raise TypeError("root_keys must be a CUDA int64 tensor (uint64 bit patterns)")
             _rc(_L.tgl_sample_ex(self.g.handle, _ptr(roots), _ptr(root_ts), _ptr(root_keys), n, self.L, self._fan,
                                  self.strategy, self.S, self.snapshot_len, int(seed) & 0xFFFFFFFFFFFFFFFF, 0,
-                                 ctypes.byref(self._opts), self._c_blocks, _ptr(self.workspace), self.ws_bytes,
-                                 _stream(stream)), "tgl_sample_ex")
+                                 ctypes.byref(self._opts), self._c_blocks, self._c_dedup, _ptr(self.workspace),
+                                 self.ws_bytes, _stream(stream)), "tgl_sample_ex")
             return self.blocks
         if self._default_opts:
             _rc(_L.tgl_sample(self.g.handle, _ptr(roots), _ptr(root_ts), n, self.L, self._fan, self.strategy, self.S,
@@ -248,19 +269,20 @@ class Sampler:
             _rc(_L.tgl_sample_ex(self.g.handle, _ptr(roots), _ptr(root_ts), None, n, self.L, self._fan, self.strategy,
                                  self.S, self.snapshot_len, int(seed) & 0xFFFFFFFFFFFFFFFF,
                                  int(root_key_base) & 0xFFFFFFFFFFFFFFFF, ctypes.byref(self._opts), self._c_blocks,
-                                 _ptr(self.workspace), self.ws_bytes, _stream(stream)), "tgl_sample_ex")
+                                 self._c_dedup, _ptr(self.workspace), self.ws_bytes, _stream(stream)), "tgl_sample_ex")
         return self.blocks
 
 
 def sample(g: TCSR, roots: torch.Tensor, root_ts: torch.Tensor, *, fanouts: Sequence[int],
            strategy="most_recent", n_snapshots: int = 1, snapshot_len: float = math.inf, seed: int = 0,
-           root_key_base: int = 0, stream=None, hop_time: str = "edge", replacement: bool = False) -> List[Block]:
+           root_key_base: int = 0, stream=None, hop_time: str = "edge", replacement: bool = False,
+           dedup: bool = False) -> List[Block]:
     """tgl_sample (Alg. 1): returns L*S blocks, block (l, s) at index l*S + s.  hop_time /
     replacement select the variants of tgl_sample_ex (R#23, R#24)."""
     roots = _cuda(roots, torch.int32, "roots")
     root_ts = _cuda(root_ts, torch.float32, "root_ts")
     s = Sampler(g, max(roots.numel(), 1), fanouts, strategy, n_snapshots, snapshot_len, hop_time=hop_time,
-                replacement=replacement)
+                replacement=replacement, dedup=dedup)
     return s.run(roots, root_ts, seed=seed, root_key_base=root_key_base, n_roots=roots.numel(), stream=stream)
 
 

@@ -26,7 +26,13 @@ class Block(ctypes.Structure):
 
 
 class SampleOptions(ctypes.Structure):
-    _fields_ = [("hop_time", ctypes.c_int32), ("replacement", ctypes.c_int32), ("reserved", ctypes.c_int32 * 6)]
+    _fields_ = [("hop_time", ctypes.c_int32), ("replacement", ctypes.c_int32), ("dedup", ctypes.c_int32),
+                ("reserved", ctypes.c_int32 * 5)]
+
+
+class DedupBlock(ctypes.Structure):
+    """tgl_dedup_block (include/tgl.h)."""
+    _fields_ = [("cap", i64), ("src_index", P), ("uniq_node", P), ("uniq_ts", P), ("n_uniq_dev", P)]
 
 
 class StateTable(ctypes.Structure):
@@ -53,7 +59,8 @@ SIGNATURES = {
     "tgl_sample_capacity": (ctypes.c_int, [i64, i32, P, i32, ctypes.c_int, f32, P, P, ctypes.POINTER(sz)]),
     "tgl_sample": (ctypes.c_int, [P, P, P, i64, i32, P, ctypes.c_int, i32, f32, u64, u64, P, P, sz, P]),
     "tgl_sample_keyed": (ctypes.c_int, [P, P, P, P, i64, i32, P, ctypes.c_int, i32, f32, u64, P, P, sz, P]),
-    "tgl_sample_ex": (ctypes.c_int, [P, P, P, P, i64, i32, P, ctypes.c_int, i32, f32, u64, u64, P, P, P, sz, P]),
+    "tgl_sample_ex": (ctypes.c_int, [P, P, P, P, i64, i32, P, ctypes.c_int, i32, f32, u64, u64, P, P, P, P, sz, P]),
+    "tgl_sample_capacity_ex": (ctypes.c_int, [i64, i32, P, i32, ctypes.c_int, f32, P, P, P, ctypes.POINTER(sz)]),
     "tgl_tcsr_set_node_base": (ctypes.c_int, [P, i64]),
     "tgl_shard_unpermute_workspace": (ctypes.c_int, [i64, ctypes.POINTER(sz)]),
     "tgl_offsets_to_counts": (ctypes.c_int, [P, i64, P, P]),

@@ -32,6 +32,7 @@
 #include <cstring>
 
 #include "common.cuh"
+#include "scan.cuh"
 #include "tsindex.cuh"
 
 namespace tgl {
@@ -561,6 +562,70 @@ __global__ void __launch_bounds__(kTile, TGL_COPY_MINB) copy_kernel(const __grid
     }
 }
 
+// ---------------------------------------------------------------------------- K9 dedup (R#27)
+// Distinct (node, hop time) pairs of a block in order of first appearance (SPEC's MFG node lists):
+//   D1 insert: open addressing over 64-bit keys (node << 32 | time bits); the SLOT a key lands in
+//      depends on the schedule, but atomicMin records the smallest output index per key, so
+//   D2 flag: output i is a first occurrence iff it is its key's minimum -- deterministic; an
+//      exclusive scan of the flags numbers the distinct pairs in first-appearance order;
+//   D3 emit: src_index[i] = number of its key's first occurrence; firsts write the unique lists
+//      (node, time, and the first occurrence's child key for the next layer's RNG, R#7).
+__device__ __forceinline__ uint64_t mix64(uint64_t x) {  // splitmix64 finaliser
+    x ^= x >> 30;
+    x *= 0xbf58476d1ce4e5b9ull;
+    x ^= x >> 27;
+    x *= 0x94d049bb133111ebull;
+    return x ^ (x >> 31);
+}
+
+__device__ __forceinline__ int64_t dev_count(const int64_t* n_dev, int64_t cap) {
+    const int64_t m = *n_dev;
+    return m < cap ? (m > 0 ? m : 0) : cap;
+}
+
+__global__ void dedup_insert_kernel(const int32_t* __restrict__ nbr, const float* __restrict__ t_hop,
+                                    const int64_t* __restrict__ n_dev, int64_t cap, unsigned long long* hkeys,
+                                    unsigned int* hfirst, uint64_t mask, uint32_t* __restrict__ slot_of) {
+    const int64_t n = dev_count(n_dev, cap);
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const unsigned long long key =
+            ((unsigned long long)(uint32_t)nbr[i] << 32) | (unsigned long long)__float_as_uint(t_hop[i]);
+        uint64_t h = mix64(key) & mask;
+        while (true) {
+            const unsigned long long prev = atomicCAS(hkeys + h, ~0ull, key);
+            if (prev == ~0ull || prev == key) break;
+            h = (h + 1) & mask;
+        }
+        atomicMin(hfirst + h, (unsigned int)i);
+        slot_of[i] = (uint32_t)h;
+    }
+}
+
+__global__ void dedup_flag_kernel(const int64_t* __restrict__ n_dev, int64_t cap, const unsigned int* hfirst,
+                                  const uint32_t* __restrict__ slot_of, uint32_t* __restrict__ flag) {
+    const int64_t n = dev_count(n_dev, cap);
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < cap; i += (int64_t)gridDim.x * blockDim.x)
+        flag[i] = i < n ? (hfirst[slot_of[i]] == (unsigned int)i ? 1u : 0u) : 0u;
+}
+
+__global__ void dedup_emit_kernel(const int32_t* __restrict__ nbr, const float* __restrict__ t_hop,
+                                  const uint64_t* __restrict__ child_key, const int64_t* __restrict__ n_dev,
+                                  int64_t cap, const unsigned int* hfirst, const uint32_t* __restrict__ slot_of,
+                                  const uint32_t* __restrict__ flag, const uint32_t* __restrict__ uid,
+                                  tgl_dedup_block o, uint64_t* __restrict__ uniq_key) {
+    const int64_t n = dev_count(n_dev, cap);
+    if (blockIdx.x == 0 && threadIdx.x == 0) *o.n_uniq_dev = n > 0 ? (int64_t)uid[n - 1] + flag[n - 1] : 0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t u = uid[hfirst[slot_of[i]]];
+        o.src_index[i] = (int32_t)u;
+        if (flag[i]) {
+            o.uniq_node[u] = nbr[i];
+            o.uniq_ts[u] = t_hop[i];
+            if (uniq_key) uniq_key[u] = child_key[i];
+        }
+    }
+}
+
 static bool picks_fit_smem(int nsb, int k) { return (size_t)nsb * k * 32 * 4 <= kPicksSmemPerWarp; }
 
 struct Launch {
@@ -581,11 +646,18 @@ struct SamplePlan {
     uint64_t* child_key[64][TGL_MAX_SNAPSHOTS];
     float* child_lo[64][TGL_MAX_SNAPSHOTS];
     float* child_t[64][TGL_MAX_SNAPSHOTS];
+    uint64_t* uniq_key[64][TGL_MAX_SNAPSHOTS];  // dedup: first occurrence's child key per distinct pair
+    // dedup scratch (one block at a time): hash keys / first index, slot per output, flags, ids
+    unsigned long long* hkeys = nullptr;
+    unsigned int* hfirst = nullptr;
+    uint64_t hsize = 0;
+    uint32_t *slot_of = nullptr, *flag = nullptr, *uid = nullptr;
+    uint64_t* scan_partial = nullptr;
     size_t bytes = 0;
 };
 
 static int plan_sample(int64_t n_roots, int L, const int32_t* fanouts, int S, int strategy, float snapshot_len,
-                       void* ws, SamplePlan& P) {
+                       bool dedup, bool hop_root, void* ws, SamplePlan& P) {
     if (L < 1 || L > 64 || S < 1 || S > TGL_MAX_SNAPSHOTS || n_roots < 0 || !fanouts) return TGL_EINVAL;
     if (!(snapshot_len > 0.0f)) return TGL_EINVAL;               // NaN or <= 0
     if (S > 1 && !std::isfinite(snapshot_len)) return TGL_EINVAL;  // +inf only for one snapshot
@@ -626,12 +698,30 @@ static int plan_sample(int64_t n_roots, int L, const int32_t* fanouts, int S, in
         P.launches[j].super_tot = c.take<uint64_t>((size_t)P.launches[j].nsb * P.launches[j].supers_cap);
     P.memset_bytes = c.bytes() - P.memset_from;
     const bool need_lo = L > 1 && std::isfinite(snapshot_len);
-    for (int l = 0; l < L - 1; ++l)
+    if (dedup && need_lo) return TGL_EINVAL;  // R#27: windows with inherited finite bounds would merge
+    for (int l = 0; l < L; ++l)
         for (int s = 0; s < S; ++s) {
-            P.child_key[l][s] = strategy == TGL_UNIFORM ? c.take<uint64_t>((size_t)P.edges_cap[l]) : nullptr;
-            P.child_lo[l][s] = need_lo ? c.take<float>((size_t)P.edges_cap[l]) : nullptr;
-            P.child_t[l][s] = c.take<float>((size_t)P.edges_cap[l]);  // used under TGL_HOP_ROOT_TIME
+            const bool inner = l < L - 1;
+            P.child_key[l][s] = inner && strategy == TGL_UNIFORM ? c.take<uint64_t>((size_t)P.edges_cap[l]) : nullptr;
+            P.child_lo[l][s] = inner && need_lo ? c.take<float>((size_t)P.edges_cap[l]) : nullptr;
+            // hop-root times under TGL_HOP_ROOT_TIME (the last layer's only for dedup keys)
+            P.child_t[l][s] = inner || (dedup && hop_root) ? c.take<float>((size_t)P.edges_cap[l]) : nullptr;
+            P.uniq_key[l][s] = inner && dedup && strategy == TGL_UNIFORM ? c.take<uint64_t>((size_t)P.edges_cap[l])
+                                                                         : nullptr;
         }
+    if (dedup) {
+        int64_t emax = 1;
+        for (int l = 0; l < L; ++l) emax = std::max<int64_t>(emax, P.edges_cap[l]);
+        uint64_t h = 64;
+        while (h < 2 * (uint64_t)emax) h <<= 1;
+        P.hsize = h;
+        P.hkeys = c.take<unsigned long long>(h);
+        P.hfirst = c.take<unsigned int>(h);
+        P.slot_of = c.take<uint32_t>((size_t)emax);
+        P.flag = c.take<uint32_t>((size_t)emax);
+        P.uid = c.take<uint32_t>((size_t)emax);
+        P.scan_partial = c.take<uint64_t>(scan_workspace_bytes(emax) / sizeof(uint64_t) + 1);
+    }
     P.bytes = c.bytes();
     return TGL_OK;
 }
@@ -653,7 +743,7 @@ extern "C" int tgl_sample_capacity(int64_t n_roots, int32_t n_layers, const int3
                                    tgl_strategy strategy, float snapshot_len, int64_t* roots_cap, int64_t* edges_cap,
                                    size_t* ws_bytes) {
     static thread_local SamplePlan P;
-    int rc = plan_sample(n_roots, n_layers, fanouts, n_snapshots, (int)strategy, snapshot_len, nullptr, P);
+    int rc = plan_sample(n_roots, n_layers, fanouts, n_snapshots, (int)strategy, snapshot_len, false, false, nullptr, P);
     if (rc) return rc;
     for (int l = 0; l < n_layers; ++l) {
         if (roots_cap) roots_cap[l] = P.roots_cap[l];
@@ -666,20 +756,23 @@ extern "C" int tgl_sample_capacity(int64_t n_roots, int32_t n_layers, const int3
 static int sample_impl(const tgl_tcsr* g, const int32_t* roots, const float* root_ts, const uint64_t* root_keys,
                        int64_t n_roots, int32_t n_layers, const int32_t* fanouts, tgl_strategy strategy,
                        int32_t n_snapshots, float snapshot_len, uint64_t seed, uint64_t root_key_base,
-                       const tgl_sample_options* opts, tgl_block* out, void* workspace, size_t ws_bytes,
-                       void* stream) {
+                       const tgl_sample_options* opts, tgl_block* out, const tgl_dedup_block* dd,
+                       void* workspace, size_t ws_bytes, void* stream) {
     if (!g || !out || !workspace) return TGL_EINVAL;
     tgl_sample_options o;
     memset(&o, 0, sizeof(o));
     if (opts) o = *opts;
     if (o.hop_time != TGL_HOP_EDGE_TIME && o.hop_time != TGL_HOP_ROOT_TIME) return TGL_EINVAL;
     if (o.replacement != 0 && (o.replacement != 1 || strategy != TGL_UNIFORM)) return TGL_EINVAL;
-    for (int q = 0; q < 6; ++q)
+    if (o.dedup != 0 && (o.dedup != 1 || !dd)) return TGL_EINVAL;
+    for (int q = 0; q < 5; ++q)
         if (o.reserved[q]) return TGL_EINVAL;
     const bool hop_root = o.hop_time == TGL_HOP_ROOT_TIME;
+    const bool dedup = o.dedup == 1;
     if (n_roots > 0 && (!roots || !root_ts)) return TGL_EINVAL;
     static thread_local SamplePlan P;
-    int rc = plan_sample(n_roots, n_layers, fanouts, n_snapshots, (int)strategy, snapshot_len, workspace, P);
+    int rc = plan_sample(n_roots, n_layers, fanouts, n_snapshots, (int)strategy, snapshot_len, dedup, hop_root,
+                         workspace, P);
     if (rc) return rc;
     if (ws_bytes < P.bytes) return TGL_EWORKSPACE;
     rc = check_device();
@@ -689,8 +782,13 @@ static int sample_impl(const tgl_tcsr* g, const int32_t* roots, const float* roo
         for (int s = 0; s < S; ++s) {
             const tgl_block& b = out[l * S + s];
             if (!b.offsets || !b.nbr || !b.eid || !b.dt || !b.n_roots_dev || !b.nnz_dev) return TGL_EINVAL;
-            if (l < L - 1 && !b.ts_edge) return TGL_EINVAL;
+            if ((l < L - 1 || (dedup && !hop_root)) && !b.ts_edge) return TGL_EINVAL;
             if (b.cap_roots < P.roots_cap[l] || b.cap_edges < P.edges_cap[l]) return TGL_ECAPACITY;
+            if (dedup) {
+                const tgl_dedup_block& d = dd[l * S + s];
+                if (!d.src_index || !d.uniq_node || !d.uniq_ts || !d.n_uniq_dev) return TGL_EINVAL;
+                if (d.cap < P.edges_cap[l]) return TGL_ECAPACITY;
+            }
         }
     cudaStream_t st = (cudaStream_t)stream;
     if (cudaMemsetAsync(static_cast<char*>(workspace) + P.memset_from, 0, P.memset_bytes, st) != cudaSuccess)
@@ -720,12 +818,21 @@ static int sample_impl(const tgl_tcsr* g, const int32_t* roots, const float* roo
             sp.n_roots = n_roots;
         } else {
             const tgl_block& par = out[(l - 1) * S + s];
-            sp.root_node = par.nbr;
-            sp.root_ts = hop_root ? P.child_t[l - 1][s] : par.ts_edge;
-            sp.root_key = P.child_key[l - 1][s];
-            sp.root_lo = P.child_lo[l - 1][s];
+            if (dedup) {  // R#27: the previous block's distinct (node, time) pairs
+                const tgl_dedup_block& pd = dd[(l - 1) * S + s];
+                sp.root_node = pd.uniq_node;
+                sp.root_ts = pd.uniq_ts;
+                sp.root_key = P.uniq_key[l - 1][s];
+                sp.root_lo = nullptr;
+                sp.n_roots_dev_in = pd.n_uniq_dev;
+            } else {
+                sp.root_node = par.nbr;
+                sp.root_ts = hop_root ? P.child_t[l - 1][s] : par.ts_edge;
+                sp.root_key = P.child_key[l - 1][s];
+                sp.root_lo = P.child_lo[l - 1][s];
+                sp.n_roots_dev_in = par.nnz_dev;
+            }
             sp.n_roots = P.roots_cap[l];
-            sp.n_roots_dev_in = par.nnz_dev;
         }
         sp.root_key_base = root_key_base;
         sp.layer = l;
@@ -755,7 +862,7 @@ static int sample_impl(const tgl_tcsr* g, const int32_t* roots, const float* roo
             bo.ts_edge = ob.ts_edge;
             bo.child_key = l < L - 1 ? P.child_key[l][bs] : nullptr;
             bo.child_lo = l < L - 1 ? P.child_lo[l][bs] : nullptr;
-            bo.child_t = (l < L - 1 && hop_root) ? P.child_t[l][bs] : nullptr;
+            bo.child_t = hop_root ? P.child_t[l][bs] : nullptr;  // null for the last layer without dedup
             bo.n_roots_dev = ob.n_roots_dev;
             bo.nnz_dev = ob.nnz_dev;
         }
@@ -765,6 +872,28 @@ static int sample_impl(const tgl_tcsr* g, const int32_t* roots, const float* roo
         rc = strategy == TGL_UNIFORM ? launch_chain<TGL_UNIFORM>(sp, tiles, smem, st)
                                      : launch_chain<TGL_MOST_RECENT>(sp, tiles, smem, st);
         if (rc) return rc;
+        if (dedup) {
+            for (int b = 0; b < la.nsb; ++b) {
+                const int bs = l == 0 ? b : s;
+                const tgl_block& ob = out[l * S + bs];
+                const float* t_hop = hop_root ? P.child_t[l][bs] : ob.ts_edge;
+                const int64_t cap = P.edges_cap[l];
+                const unsigned blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>((cap + 255) / 256, 148 * 8));
+                if (cudaMemsetAsync(P.hkeys, 0xff, P.hsize * sizeof(unsigned long long), st) != cudaSuccess ||
+                    cudaMemsetAsync(P.hfirst, 0xff, P.hsize * sizeof(unsigned int), st) != cudaSuccess)
+                    return TGL_ECUDA;
+                dedup_insert_kernel<<<blocks, 256, 0, st>>>(ob.nbr, t_hop, ob.nnz_dev, cap, P.hkeys, P.hfirst,
+                                                            P.hsize - 1, P.slot_of);
+                dedup_flag_kernel<<<blocks, 256, 0, st>>>(ob.nnz_dev, cap, P.hfirst, P.slot_of, P.flag);
+                if (cuda_rc(exclusive_scan<uint32_t, uint32_t>(P.flag, P.uid, cap, (uint32_t*)nullptr, P.scan_partial,
+                                                               st)))
+                    return TGL_ECUDA;
+                dedup_emit_kernel<<<blocks, 256, 0, st>>>(ob.nbr, t_hop, P.child_key[l][bs], ob.nnz_dev, cap, P.hfirst,
+                                                          P.slot_of, P.flag, P.uid, dd[l * S + bs],
+                                                          P.uniq_key[l][bs]);
+                if (cudaGetLastError() != cudaSuccess) return TGL_ECUDA;
+            }
+        }
     }
     return TGL_OK;
 }
@@ -774,7 +903,7 @@ extern "C" int tgl_sample(const tgl_tcsr* g, const int32_t* roots, const float* 
                           float snapshot_len, uint64_t seed, uint64_t root_key_base, tgl_block* out, void* workspace,
                           size_t ws_bytes, void* stream) {
     return sample_impl(g, roots, root_ts, nullptr, n_roots, n_layers, fanouts, strategy, n_snapshots, snapshot_len,
-                       seed, root_key_base, nullptr, out, workspace, ws_bytes, stream);
+                       seed, root_key_base, nullptr, out, nullptr, workspace, ws_bytes, stream);
 }
 
 extern "C" int tgl_sample_keyed(const tgl_tcsr* g, const int32_t* roots, const float* root_ts,
@@ -783,14 +912,32 @@ extern "C" int tgl_sample_keyed(const tgl_tcsr* g, const int32_t* roots, const f
                                 tgl_block* out, void* workspace, size_t ws_bytes, void* stream) {
     if (n_roots > 0 && !root_keys) return TGL_EINVAL;
     return sample_impl(g, roots, root_ts, root_keys, n_roots, n_layers, fanouts, strategy, n_snapshots, snapshot_len,
-                       seed, 0, nullptr, out, workspace, ws_bytes, stream);
+                       seed, 0, nullptr, out, nullptr, workspace, ws_bytes, stream);
 }
 
 extern "C" int tgl_sample_ex(const tgl_tcsr* g, const int32_t* roots, const float* root_ts, const uint64_t* root_keys,
                              int64_t n_roots, int32_t n_layers, const int32_t* fanouts, tgl_strategy strategy,
                              int32_t n_snapshots, float snapshot_len, uint64_t seed, uint64_t root_key_base,
-                             const tgl_sample_options* opts, tgl_block* out, void* workspace, size_t ws_bytes,
-                             void* stream) {
+                             const tgl_sample_options* opts, tgl_block* out, const tgl_dedup_block* dedup,
+                             void* workspace, size_t ws_bytes, void* stream) {
     return sample_impl(g, roots, root_ts, root_keys, n_roots, n_layers, fanouts, strategy, n_snapshots, snapshot_len,
-                       seed, root_keys ? 0 : root_key_base, opts, out, workspace, ws_bytes, stream);
+                       seed, root_keys ? 0 : root_key_base, opts, out, dedup, workspace, ws_bytes, stream);
+}
+
+extern "C" int tgl_sample_capacity_ex(int64_t n_roots, int32_t n_layers, const int32_t* fanouts, int32_t n_snapshots,
+                                      tgl_strategy strategy, float snapshot_len, const tgl_sample_options* opts,
+                                      int64_t* roots_cap, int64_t* edges_cap, size_t* ws_bytes) {
+    tgl_sample_options o;
+    memset(&o, 0, sizeof(o));
+    if (opts) o = *opts;
+    static thread_local SamplePlan P;
+    int rc = plan_sample(n_roots, n_layers, fanouts, n_snapshots, (int)strategy, snapshot_len, o.dedup == 1,
+                         o.hop_time == TGL_HOP_ROOT_TIME, nullptr, P);
+    if (rc) return rc;
+    for (int l = 0; l < n_layers; ++l) {
+        if (roots_cap) roots_cap[l] = P.roots_cap[l];
+        if (edges_cap) edges_cap[l] = P.edges_cap[l];
+    }
+    if (ws_bytes) *ws_bytes = P.bytes;
+    return TGL_OK;
 }

@@ -85,11 +85,48 @@ def test_option_validation(tgl):
 
     def call(opts, strategy=0):
         return L_.tgl_sample_ex(g.handle, r.data_ptr(), t.data_ptr(), None, 4, 1, fan, strategy, 1, math.inf, 0, 0,
-                                ctypes.byref(opts), smp._c_blocks, smp.workspace.data_ptr(), smp.ws_bytes, None)
+                                ctypes.byref(opts), smp._c_blocks, None, smp.workspace.data_ptr(), smp.ws_bytes, None)
     assert call(_lib.SampleOptions(0, 0)) == 0
     assert call(_lib.SampleOptions(2, 0)) == -1            # unknown hop_time
     assert call(_lib.SampleOptions(0, 1)) == -1            # replacement with most_recent
     o = _lib.SampleOptions(0, 0)
     o.reserved[3] = 1
     assert call(o) == -1                                   # reserved words must be zero
+    assert call(_lib.SampleOptions(0, 0, 1)) == -1         # dedup without dedup blocks
     torch.cuda.synchronize()
+
+
+@pytest.mark.parametrize("hop_time", ["edge", "root"])
+def test_dedup_bit_exact(tgl, hop_time):
+    """R#27: distinct (node, hop time) lists, src_index and the deduplicated next layers vs oracle."""
+    rng = np.random.default_rng(55 + (hop_time == "root"))
+    for case in range(40):
+        n_nodes = int(rng.integers(1, 400))
+        src, dst, ts, _ = random_graph(1300 + case, n_nodes, int(rng.integers(0, 6000)), integer_times=True,
+                                       t_max=float(rng.choice([6.0, 50.0])))
+        roots, rts = random_roots(1300 + case, n_nodes, int(rng.integers(0, 1500)), integer_times=True, t_max=50.0)
+        L = 1 + case % 3
+        fanouts = [int(rng.integers(1, 12)) for _ in range(L)]
+        strategy = int(rng.integers(0, 2))
+        S = 1 if L > 1 else int(rng.integers(1, 4))
+        t_s = math.inf if S == 1 else 7.0
+        seed, base = int(rng.integers(0, 2**63)), int(rng.integers(0, 2**40))
+        add_rev = bool(case % 2)
+        go = oracle.build(src, dst, ts, None, n_nodes=n_nodes, add_reverse=add_rev)
+        g = tgl.build(cu(src, torch.int32), cu(dst, torch.int32), cu(ts, torch.float32), None, n_nodes=n_nodes,
+                      add_reverse=add_rev)
+        bo = oracle.sample(go, roots, rts, fanouts=fanouts, strategy=strategy, n_snapshots=S, snapshot_len=t_s,
+                           seed=seed, root_key_base=base, hop_time=hop_time, dedup=True)
+        b = tgl.sample(g, cu(roots, torch.int32), cu(rts, torch.float32), fanouts=fanouts, strategy=strategy,
+                       n_snapshots=S, snapshot_len=t_s, seed=seed, root_key_base=base, hop_time=hop_time, dedup=True)
+        for j, (x, o) in enumerate(zip(b, bo)):
+            off, nbr, e, dt, _ = x.trimmed()
+            np.testing.assert_array_equal(off.cpu().numpy(), o["offsets"], err_msg=f"case {case} block {j}")
+            np.testing.assert_array_equal(nbr.cpu().numpy(), o["nbr"])
+            np.testing.assert_array_equal(e.cpu().numpy(), o["eid"])
+            np.testing.assert_array_equal(dt.cpu().numpy().view(np.uint32), o["dt"].view(np.uint32))
+            nnz, nu = len(o["nbr"]), int(x.n_uniq_dev.item())
+            assert nu == len(o["uniq_node"])
+            np.testing.assert_array_equal(x.src_index[:nnz].cpu().numpy(), o["src_index"])
+            np.testing.assert_array_equal(x.uniq_node[:nu].cpu().numpy(), o["uniq_node"])
+            np.testing.assert_array_equal(x.uniq_ts[:nu].cpu().numpy().view(np.uint32), o["uniq_ts"].view(np.uint32))
