@@ -41,7 +41,10 @@ namespace tgl {
 #define TGL_WINDOW_MINB 8
 #endif
 #ifndef TGL_COPY_MINB
-#define TGL_COPY_MINB 6
+#define TGL_COPY_MINB 6  // uniform copy (Floyd picks): 40 registers
+#endif
+#ifndef TGL_COPY_MINB_MR
+#define TGL_COPY_MINB_MR 8  // most_recent copy: 32 registers, no spills (C5 +6 %)
 #endif
 constexpr int kTile = 256;  // roots per tile (one lane per root)
 constexpr int kWarps = kTile / 32;
@@ -363,7 +366,7 @@ __host__ __device__ inline int copy_warp_words(int nsb, int k, bool picks_in_sme
 }
 
 template <int STRATEGY>
-__global__ void __launch_bounds__(kTile, TGL_COPY_MINB) copy_kernel(const __grid_constant__ SampleParams p) {
+__global__ void __launch_bounds__(kTile, STRATEGY == TGL_MOST_RECENT ? TGL_COPY_MINB_MR : TGL_COPY_MINB) copy_kernel(const __grid_constant__ SampleParams p) {
     extern __shared__ __align__(16) uint32_t smem[];
     __shared__ uint32_t s_wsum[TGL_MAX_SNAPSHOTS][kWarps];
     __shared__ uint64_t s_tbase[TGL_MAX_SNAPSHOTS];
