@@ -59,7 +59,7 @@ def lib():
         L.oracle_tcsr_fill.argtypes = [P, P, P, P, i64, i64, i32, ctypes.c_int, P, P, P, P, P]
         L.oracle_tcsr_fill.restype = ctypes.c_int
         L.oracle_sample_block.argtypes = [P, P, P, P, i32, P, P, P, P, i64, i32, i32, f32, i32, i32,
-                                          i32, u64, P, P, P, P, P, P, P, P, P]
+                                          i32, u64, P, P, P, P, P, P, P, P, P, P, P]
         L.oracle_sample_block.restype = i64
         L.oracle_gather.argtypes = [P, i64, P, i64, i64, P, P]
         L.oracle_gather.restype = None
@@ -164,7 +164,7 @@ def build_restricted(chunks: Iterable, *, n_nodes: int, add_reverse: bool,
 # --------------------------------------------------------------------------- sampler
 def sample_block(g: TCSR, root_node, root_ts, root_key, root_lo, *, layer: int, snapshot: int,
                  snapshot_len: float, k: int, strategy: int, seed: int,
-                 want_children: bool, replacement: bool = False) -> dict:
+                 want_children: bool, replacement: bool = False, edge_valid=None) -> dict:
     """One (layer, snapshot) block of Alg. 1 -- see tgl_oracle.c."""
     root_node = np.ascontiguousarray(root_node, dtype=np.int32)
     root_ts = np.ascontiguousarray(root_ts, dtype=np.float32)
@@ -181,11 +181,15 @@ def sample_block(g: TCSR, root_node, root_ts, root_key, root_lo, *, layer: int, 
     clo = np.zeros(cap, dtype=np.float32) if want_children else None
     err = np.zeros(1, dtype=np.int32)
     scratch = np.zeros(max(k, 1), dtype=np.uint32)
+    cand = None
+    if edge_valid is not None:
+        edge_valid = np.ascontiguousarray(edge_valid, dtype=np.uint32)
+        cand = np.zeros(max(int(np.max(np.diff(g["indptr"]), initial=0)), 1), dtype=np.int64)
     nnz = lib().oracle_sample_block(_p(g["indptr"]), _p(g["nbr"]), _p(g["ts"]), _p(g["eid"]),
                                     g.n_nodes, _p(root_node), _p(root_ts), _p(root_key), _p(root_lo), n,
                                     layer, snapshot, float(snapshot_len), k, strategy, int(bool(replacement)),
                                     int(seed) & 0xFFFFFFFFFFFFFFFF, _p(offsets), _p(nbr), _p(eid), _p(dt),
-                                    _p(ts_edge), _p(ckey), _p(clo), _p(err), _p(scratch))
+                                    _p(ts_edge), _p(ckey), _p(clo), _p(err), _p(scratch), _p(edge_valid), _p(cand))
     out = dict(offsets=offsets, nbr=nbr[:nnz], eid=eid[:nnz], dt=dt[:nnz], err=int(err[0]))
     if want_children:
         out.update(ts_edge=ts_edge[:nnz], child_key=ckey[:nnz], child_lo=clo[:nnz])
@@ -194,7 +198,8 @@ def sample_block(g: TCSR, root_node, root_ts, root_key, root_lo, *, layer: int, 
 
 def sample(g: TCSR, roots, root_ts, *, fanouts: List[int], strategy: int, n_snapshots: int = 1,
            snapshot_len: float = math.inf, seed: int = 0, root_key_base: int = 0,
-           hop_time: str = "edge", replacement: bool = False, dedup: bool = False) -> List[dict]:
+           hop_time: str = "edge", replacement: bool = False, dedup: bool = False,
+           edge_valid=None) -> List[dict]:
     """Alg. 1: L x S blocks, block (l, s) at index l*S + s.
 
     Layer-0 roots are the caller's; the roots of block (l, s), l >= 1, are the outputs
@@ -208,6 +213,7 @@ def sample(g: TCSR, roots, root_ts, *, fanouts: List[int], strategy: int, n_snap
     src_index[i] = the pair of output i; the next layer's roots are that list, each keyed by its
     first occurrence's child key.  Not defined with inherited finite lower bounds (L > 1 with a
     finite snapshot length): different windows would merge.
+    edge_valid (uint32 bitmask over edge ids, R#28, P:L258 / L556): invalid edges are not candidates.
     """
     if hop_time not in ("edge", "root"):
         raise ValueError("hop_time must be 'edge' or 'root'")
@@ -226,7 +232,7 @@ def sample(g: TCSR, roots, root_ts, *, fanouts: List[int], strategy: int, n_snap
             want = l < L - 1
             b = sample_block(g, rn, rt, rk, rlo, layer=l, snapshot=s, snapshot_len=snapshot_len,
                              k=fanouts[l], strategy=strategy, seed=seed, want_children=want or dedup,
-                             replacement=replacement)
+                             replacement=replacement, edge_valid=edge_valid)
             if want or dedup:
                 # R#4 / R#23: the hop root's time is the sampled edge's, or its parent root's
                 t_next = b["ts_edge"] if hop_time == "edge" else np.repeat(rt, np.diff(b["offsets"]))

@@ -68,7 +68,8 @@ def with_replacement(c: int, k: int, seed: int, layer: int, snapshot: int, rk: i
 
 def sample(src, dst, ts, eid, *, n_nodes: int, add_reverse: bool, roots, root_ts, fanouts,
            strategy: int, n_snapshots: int = 1, snapshot_len: float = math.inf, seed: int = 0,
-           root_key_base: int = 0, hop_time: str = "edge", replacement: bool = False, dedup: bool = False):
+           root_key_base: int = 0, hop_time: str = "edge", replacement: bool = False, dedup: bool = False,
+           edge_valid=None):
     """Returns blocks[l*S+s] = list over roots of lists of (nbr, eid, dt, ts_edge)."""
     owner, nbr, tsl, eidl = logical_stream(src, dst, ts, eid, add_reverse)
     f32 = np.float32
@@ -92,7 +93,11 @@ def sample(src, dst, ts, eid, *, n_nodes: int, add_reverse: bool, roots, root_ts
                 else:
                     U = t
                     Lo = lo_in if lo_in is not None else f32(-np.inf)
-                cand = np.nonzero((owner == v) & (tsl >= Lo) & (tsl < U))[0]
+                ok = (owner == v) & (tsl >= Lo) & (tsl < U)
+                if edge_valid is not None:  # R#28: invalid edges are not candidates
+                    ev = np.asarray(edge_valid, dtype=np.uint64)
+                    ok &= ((ev[eidl.astype(np.int64) >> 5] >> (eidl.astype(np.uint64) & np.uint64(31))) & np.uint64(1)) == 1
+                cand = np.nonzero(ok)[0]
                 c = len(cand)
                 if strategy == 0:
                     sel = cand[max(0, c - k):]

@@ -23,7 +23,8 @@
  *                            is only needed for the sampled roots)
  *   oracle_sample_block      one (layer l, snapshot s) block of Alg. 1, P:L217-L243,
  *                            P:L260-L262 (strategies), P:L267 (no leak); uniform with
- *                            replacement as the variant of DESIGN.md R#24
+ *                            replacement as the variant of DESIGN.md R#24; an optional edge
+ *                            validity bitmask (R#28: invalid edges are not candidates)
  *   oracle_gather            out[i] = table[id[i]] byte for byte, Fig. 2 step 2
  *   oracle_state_write       Fig. 2 step 6: node memory / mailbox
  *                            update, events applied one by one in batch order, each
@@ -220,7 +221,8 @@ int64_t oracle_sample_block(const int64_t *indptr, const int32_t *nbr, const flo
                             int32_t replacement, uint64_t seed,
                             int64_t *offsets, int32_t *out_nbr, int32_t *out_eid, float *out_dt,
                             float *out_ts_edge, uint64_t *out_child_key, float *out_child_lo,
-                            int32_t *err, uint32_t *pick_scratch /* >= k entries */)
+                            int32_t *err, uint32_t *pick_scratch /* >= k entries */,
+                            const uint32_t *edge_valid, int64_t *cand_scratch /* >= max degree */)
 {
     int64_t nnz = 0;
     const uint32_t key[2] = { (uint32_t)(seed & 0xFFFFFFFFu), (uint32_t)(seed >> 32) };
@@ -244,6 +246,16 @@ int64_t oracle_sample_block(const int64_t *indptr, const int32_t *nbr, const flo
         int64_t b = lower_bound_f32(ts, lo, hi, U);
         if (b < a) b = a;                 /* cannot happen for L <= U; kept for safety */
         int64_t c = b - a;
+        /* R#28: with a validity bitmask over edge ids, the candidates are the
+         * window's slots whose edge is valid, in slot order; selection works on their ranks. */
+        if (edge_valid) {
+            int64_t cv = 0;
+            for (int64_t p = a; p < b; ++p) {
+                uint32_t e = (uint32_t)eid[p];
+                if ((edge_valid[e >> 5] >> (e & 31)) & 1u) cand_scratch[cv++] = p;
+            }
+            c = cv;
+        }
         int64_t n_sel = c < (int64_t)k ? c : (int64_t)k;
         if (strategy == 1 && replacement) n_sel = c > 0 ? (int64_t)k : 0;  /* R#24 */
         uint64_t rk = root_key ? root_key[i] : 0;
@@ -266,8 +278,10 @@ int64_t oracle_sample_block(const int64_t *indptr, const int32_t *nbr, const flo
                 pick_scratch[q + 1] = x;
             }
         } else if (strategy == 0 || c <= (int64_t)k) {
-            int64_t first = (strategy == 0) ? (b - n_sel) : a;
-            for (int64_t j = 0; j < n_sel; ++j) pick_scratch[j] = (uint32_t)(first + j - a);
+            /* ranks: most_recent -> the last n_sel candidates (closest to the end pointer);
+             * uniform with c <= k -> all of them */
+            int64_t first = (strategy == 0) ? (c - n_sel) : 0;
+            for (int64_t j = 0; j < n_sel; ++j) pick_scratch[j] = (uint32_t)(first + j);
         } else {
             /* Floyd's algorithm: for m = c-k .. c-1 draw r uniform in [0, m]; take r
              * if not yet taken, else take m.  Draw j uses Philox word 0. */
@@ -291,7 +305,7 @@ int64_t oracle_sample_block(const int64_t *indptr, const int32_t *nbr, const flo
             }
         }
         for (int64_t j = 0; j < n_sel; ++j) {
-            int64_t p = a + (int64_t)pick_scratch[j];
+            int64_t p = edge_valid ? cand_scratch[pick_scratch[j]] : a + (int64_t)pick_scratch[j];
             int64_t o = nnz + j;
             out_nbr[o] = nbr[p];
             out_eid[o] = eid[p];

@@ -794,7 +794,12 @@ static int sample_impl(const tgl_tcsr* g, const int32_t* roots, const float* roo
             }
         }
     cudaStream_t st = (cudaStream_t)stream;
-    if (cudaMemsetAsync(static_cast<char*>(workspace) + P.memset_from, 0, P.memset_bytes, st) != cudaSuccess)
+    // super totals are read only for super tiles BEFORE a copy CTA's own: a call whose chains all
+    // fit one super tile (<= 64 tiles: per-batch calls) never reads them, so needs no zeroing
+    bool need_zero = false;
+    for (int j = 0; j < P.n_launch; ++j) need_zero |= P.launches[j].tiles_cap > (1 << kSuperShift);
+    if (need_zero &&
+        cudaMemsetAsync(static_cast<char*>(workspace) + P.memset_from, 0, P.memset_bytes, st) != cudaSuccess)
         return TGL_ECUDA;
     // experiment knobs (tools/sweep.py): TGL_NO_INDEX, TGL_NO_RECS
     const bool use_recs = g->recs && !getenv("TGL_NO_RECS");

@@ -127,3 +127,48 @@ def test_dedup_matches_brute_force(hop_time):
         for b in blocks:  # src_index maps every output to its (node, time) pair
             assert np.array_equal(b["uniq_node"][b["src_index"]], b["nbr"])
             assert len(set(zip(b["uniq_node"].tolist(), b["uniq_ts"].view(np.uint32).tolist()))) == len(b["uniq_node"])
+
+
+def _mask(rng, n_edges, frac):
+    bits = rng.random(max(n_edges, 1)) < frac
+    words = np.zeros((len(bits) + 31) // 32, dtype=np.uint32)
+    for e in np.nonzero(bits)[0]:
+        words[e >> 5] |= np.uint32(1) << np.uint32(e & 31)
+    return words
+
+
+@pytest.mark.parametrize("strategy,replacement", [(0, False), (1, False), (1, True)])
+def test_edge_validity_matches_brute_force(strategy, replacement):
+    """R#28: invalid edges are skipped; vs the brute-force scan with the same mask."""
+    rng = np.random.default_rng(300 + strategy + 2 * replacement)
+    for case in range(60):
+        n_nodes = int(rng.integers(1, 40))
+        n_edges = int(rng.integers(0, 300))
+        src, dst, ts, eid = random_graph(1100 + case, n_nodes, n_edges, integer_times=case % 3 != 0)
+        roots, rts = random_roots(1100 + case, n_nodes, int(rng.integers(1, 30)), integer_times=case % 3 != 0)
+        L = 1 + case % 2
+        fanouts = [int(rng.integers(1, 6)) for _ in range(L)]
+        S = int(rng.integers(1, 4))
+        t_s = math.inf if S == 1 and case % 2 else 2.5
+        seed, base = int(rng.integers(0, 2**63)), int(rng.integers(0, 2**40))
+        valid = _mask(rng, n_edges, float(rng.choice([0.0, 0.3, 0.8, 1.0])))
+        g = oracle.build(src, dst, ts, eid, n_nodes=n_nodes, add_reverse=bool(case % 2))
+        blocks = oracle.sample(g, roots, rts, fanouts=fanouts, strategy=strategy, n_snapshots=S, snapshot_len=t_s,
+                               seed=seed, root_key_base=base, replacement=replacement, edge_valid=valid)
+        bf = brute.sample(src, dst, ts, eid, n_nodes=n_nodes, add_reverse=bool(case % 2), roots=roots, root_ts=rts,
+                          fanouts=fanouts, strategy=strategy, n_snapshots=S, snapshot_len=t_s, seed=seed,
+                          root_key_base=base, replacement=replacement, edge_valid=valid)
+        _compare(blocks, bf)
+
+
+def test_edge_validity_all_valid_and_none_valid():
+    src, dst, ts, _ = random_graph(4, 30, 400)
+    roots, rts = random_roots(4, 30, 50)
+    g = oracle.build(src, dst, ts, n_nodes=30, add_reverse=True)
+    kw = dict(fanouts=[5, 3], strategy=1, seed=8)
+    plain = oracle.sample(g, roots, rts, **kw)
+    full = oracle.sample(g, roots, rts, edge_valid=np.full(13, 0xFFFFFFFF, np.uint32), **kw)
+    for a, b in zip(plain, full):
+        assert np.array_equal(a["nbr"], b["nbr"]) and np.array_equal(a["offsets"], b["offsets"])
+    none = oracle.sample(g, roots, rts, edge_valid=np.zeros(13, np.uint32), **kw)
+    assert all(len(b["nbr"]) == 0 for b in none)
