@@ -227,6 +227,9 @@ typedef struct {
     int32_t replacement;  /* 0 or 1 */
     int32_t dedup;        /* 0 or 1: per-block distinct (node, hop time) lists (R#27), see below */
     int32_t reserved[5];
+    const uint32_t *edge_valid; /* device bitmask over edge ids (bit e of word e/32; R#28) or NULL:
+                                   an edge whose bit is 0 is not a candidate ("invalid edges could
+                                   be simply ignored"); maintained by tgl_edge_valid_set */
 } tgl_sample_options;
 
 /*
@@ -259,6 +262,15 @@ TGL_API int tgl_sample_ex(const tgl_tcsr *g, const int32_t *roots, const float *
                   const tgl_sample_options *opts /* host or NULL */, tgl_block *out /* host [L*S] */,
                   const tgl_dedup_block *dedup /* host [L*S], required iff opts->dedup */,
                   void *workspace, size_t ws_bytes, void *stream);
+
+/*
+ * Edge-validity events (R#28): set (value = 1) or clear (value = 0) the bits of the
+ * n edge ids eids[] in the bitmask valid (device uint32 [ceil(E/32)]), e.g. after a mini-batch
+ * whose events delete or re-insert edges.  Out-of-range ids are the caller's responsibility
+ * (n_bits bounds them: ids >= n_bits are skipped).
+ */
+TGL_API int tgl_edge_valid_set(uint32_t *valid, int64_t n_bits, const int32_t *eids, int64_t n, int32_t value,
+                       void *stream);
 
 /* ------------------------------------------------------------------ gather (Fig. 2 step 2) */
 

@@ -180,15 +180,23 @@ class Sampler:
 
     def __init__(self, g: TCSR, max_roots: int, fanouts: Sequence[int], strategy="most_recent",
                  n_snapshots: int = 1, snapshot_len: float = math.inf, device=None, want_ts_edge_last=False,
-                 hop_time: str = "edge", replacement: bool = False, dedup: bool = False):
+                 hop_time: str = "edge", replacement: bool = False, dedup: bool = False,
+                 edge_valid: Optional[torch.Tensor] = None):
         """hop_time: "edge" (R#4) or "root" (R#23, hop roots carry the root time); replacement:
         uniform with replacement (R#24); dedup: per-block distinct (node, hop time) lists feeding
-        the next layer (R#27).  All map to tgl_sample_ex's options."""
+        the next layer (R#27); edge_valid: int32/uint32 CUDA bitmask over edge ids (R#28), invalid
+        edges are not candidates -- its contents may change between runs (tgl_edge_valid_set).
+        All map to tgl_sample_ex's options."""
         self.g = g
         if hop_time not in ("edge", "root"):
             raise ValueError("hop_time must be 'edge' or 'root'")
         self._opts = _lib.SampleOptions(1 if hop_time == "root" else 0, 1 if replacement else 0, 1 if dedup else 0)
-        self._default_opts = hop_time == "edge" and not replacement and not dedup
+        self.edge_valid = edge_valid
+        if edge_valid is not None:
+            if not (edge_valid.is_cuda and edge_valid.dtype in (torch.int32, torch.uint32) and edge_valid.is_contiguous()):
+                raise TypeError("edge_valid must be a contiguous CUDA int32/uint32 bitmask")
+            self._opts.edge_valid = edge_valid.data_ptr()
+        self._default_opts = hop_time == "edge" and not replacement and not dedup and edge_valid is None
         self.dedup = bool(dedup)
         if dedup and hop_time == "edge":
             want_ts_edge_last = True
@@ -276,13 +284,13 @@ class Sampler:
 def sample(g: TCSR, roots: torch.Tensor, root_ts: torch.Tensor, *, fanouts: Sequence[int],
            strategy="most_recent", n_snapshots: int = 1, snapshot_len: float = math.inf, seed: int = 0,
            root_key_base: int = 0, stream=None, hop_time: str = "edge", replacement: bool = False,
-           dedup: bool = False) -> List[Block]:
+           dedup: bool = False, edge_valid: Optional[torch.Tensor] = None) -> List[Block]:
     """tgl_sample (Alg. 1): returns L*S blocks, block (l, s) at index l*S + s.  hop_time /
     replacement select the variants of tgl_sample_ex (R#23, R#24)."""
     roots = _cuda(roots, torch.int32, "roots")
     root_ts = _cuda(root_ts, torch.float32, "root_ts")
     s = Sampler(g, max(roots.numel(), 1), fanouts, strategy, n_snapshots, snapshot_len, hop_time=hop_time,
-                replacement=replacement, dedup=dedup)
+                replacement=replacement, dedup=dedup, edge_valid=edge_valid)
     return s.run(roots, root_ts, seed=seed, root_key_base=root_key_base, n_roots=roots.numel(), stream=stream)
 
 
@@ -361,6 +369,15 @@ def chunk_schedule(n_edges: int, batch_size: int, chunk_size: int, epoch: int, s
     _rc(_L.tgl_chunk_schedule(int(n_edges), int(batch_size), int(chunk_size), int(epoch), int(seed) & 0xFFFFFFFFFFFFFFFF,
                               _ptr(first), cap, _ptr(nb), _stream(stream)), "tgl_chunk_schedule")
     return first, nb
+
+
+def edge_valid_set(valid: torch.Tensor, eids: torch.Tensor, value: bool, n_bits: Optional[int] = None,
+                   stream=None) -> None:
+    """tgl_edge_valid_set (R#28): set (True) / clear (False) the bits of eids in the bitmask."""
+    eids = _cuda(eids, torch.int32, "eids")
+    nb = valid.numel() * 32 if n_bits is None else int(n_bits)
+    _rc(_L.tgl_edge_valid_set(_ptr(valid), nb, _ptr(eids), eids.numel(), 1 if value else 0, _stream(stream)),
+        "tgl_edge_valid_set")
 
 
 def check(g: Optional[TCSR] = None, stream=None) -> int:

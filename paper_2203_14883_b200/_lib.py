@@ -27,7 +27,7 @@ class Block(ctypes.Structure):
 
 class SampleOptions(ctypes.Structure):
     _fields_ = [("hop_time", ctypes.c_int32), ("replacement", ctypes.c_int32), ("dedup", ctypes.c_int32),
-                ("reserved", ctypes.c_int32 * 5)]
+                ("reserved", ctypes.c_int32 * 5), ("edge_valid", ctypes.c_void_p)]
 
 
 class DedupBlock(ctypes.Structure):
@@ -67,6 +67,7 @@ SIGNATURES = {
     "tgl_shard_unpermute": (ctypes.c_int, [P, i64, P, P, P, P, P, P, P, P, P, sz, P]),
     "tgl_gather": (ctypes.c_int, [P, i64, P, P, i32, P]),
     "tgl_chunk_schedule": (ctypes.c_int, [i64, i64, i64, u64, u64, P, i64, P, P]),
+    "tgl_edge_valid_set": (ctypes.c_int, [P, i64, P, i64, i32, P]),
     "tgl_state_write_workspace": (ctypes.c_int, [i64, i32, ctypes.POINTER(sz)]),
     "tgl_state_write": (ctypes.c_int, [P, P, i64, i32, i32, P, P, P, i32, P, sz, P]),
     "tgl_check": (ctypes.c_int, [P, P]),

@@ -89,6 +89,9 @@ struct SampleParams {
     const int64_t* n_roots_dev_in;  // l >= 1: device count (parent block's nnz)
     int32_t layer, nsb, snap0, k;
     int32_t replacement;  // uniform with replacement (R#24)
+    const uint32_t* valid;  // R#28: validity bitmask over edge ids (null: every edge valid)
+    uint32_t* vpicks;       // R#28: [nsb][roots_cap][k] selected slots (absolute), ascending
+    uint32_t* vtake;        // R#28: [nsb][roots_cap] selected count
     float snapshot_len;
     uint32_t seed_lo, seed_hi;
     uint32_t* cuts;  // [nsb+1][roots_cap] c_0 >= c_1 >= .. >= c_nsb: window b = slots [c_(b+1), c_b)
@@ -195,8 +198,72 @@ __device__ __forceinline__ uint32_t warp_incl_scan(uint32_t x, int lane) {
     return x;
 }
 
-// ---------------------------------------------------------------------------- K4a windows
+// ---------------------------------------------------------------------------- R#28 validity
+// With an edge-validity bitmask ("invalid edges could be simply ignored") the
+// candidates of window [a, e) are its slots whose edge is valid.  The window kernel then selects
+// explicitly: most_recent walks back from the end pointer collecting the last k valid slots;
+// uniform counts the valid slots, draws ranks (Floyd / with replacement, the same Philox counters)
+// and maps them to slots in one forward walk.  The copy kernel reads the selected slots.
 template <int STRATEGY>
+__device__ __forceinline__ uint32_t select_valid(const SampleParams& p, int64_t i, int b, uint32_t a, uint32_t e,
+                                                uint64_t rk) {
+    const uint32_t k = (uint32_t)p.k;
+    uint32_t* pk = p.vpicks + ((size_t)b * p.roots_cap + i) * k;
+    auto ok = [&](uint32_t s) {
+        const uint32_t id = (uint32_t)__ldg(p.eid + s);
+        return (__ldg(p.valid + (id >> 5)) >> (id & 31)) & 1u;
+    };
+    uint32_t take = 0;
+    if (STRATEGY == TGL_MOST_RECENT) {
+        for (uint32_t s = e; s > a && take < k; --s)
+            if (ok(s - 1)) pk[k - 1 - take++] = s - 1;  // filled from the back: ascending
+        for (uint32_t q = 0; q < take; ++q) pk[q] = pk[k - take + q];
+    } else {
+        uint32_t cv = 0;
+        for (uint32_t s = a; s < e; ++s) cv += ok(s);
+        const uint32_t ctr1 = ((uint32_t)p.layer << 16) | (uint32_t)(p.layer == 0 ? b : p.snap0);
+        if (p.replacement) {
+            take = cv ? k : 0u;
+            for (uint32_t j = 0; j < take; ++j)
+                pk[j] = __umulhi(philox4x32_10(make_uint4(j, ctr1, (uint32_t)rk, (uint32_t)(rk >> 32)), p.seed_lo,
+                                               p.seed_hi).x, cv);
+        } else if (cv <= k) {
+            take = cv;
+            for (uint32_t q = 0; q < cv; ++q) pk[q] = q;
+        } else {
+            take = k;
+            for (uint32_t j = 0; j < k; ++j) {  // Floyd over the ranks (R#5, R#6)
+                const uint32_t m = cv - k + j;
+                const uint32_t r = __umulhi(
+                    philox4x32_10(make_uint4(j, ctr1, (uint32_t)rk, (uint32_t)(rk >> 32)), p.seed_lo, p.seed_hi).x,
+                    m + 1u);
+                bool taken = false;
+                for (uint32_t q = 0; q < j; ++q) taken |= pk[q] == r;
+                pk[j] = taken ? m : r;
+            }
+        }
+        for (uint32_t j = 1; j < take; ++j) {  // ascending ranks (R#13)
+            const uint32_t xj = pk[j];
+            int q = (int)j - 1;
+            while (q >= 0 && pk[q] > xj) {
+                pk[q + 1] = pk[q];
+                --q;
+            }
+            pk[q + 1] = xj;
+        }
+        uint32_t r = 0, cnt = 0;  // ranks -> slots
+        for (uint32_t s = a; s < e && r < take; ++s) {
+            if (!ok(s)) continue;
+            while (r < take && pk[r] == cnt) pk[r++] = s;
+            ++cnt;
+        }
+    }
+    p.vtake[(size_t)b * p.roots_cap + i] = take;
+    return take;
+}
+
+// ---------------------------------------------------------------------------- K4a windows
+template <int STRATEGY, bool VALID>
 __global__ void __launch_bounds__(kTile, TGL_WINDOW_MINB) window_kernel(const __grid_constant__ SampleParams p) {
     __shared__ uint32_t s_red[TGL_MAX_SNAPSHOTS][kWarps];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -225,6 +292,9 @@ __global__ void __launch_bounds__(kTile, TGL_WINDOW_MINB) window_kernel(const __
     }
     float lin = -INFINITY;
     if (p.layer > 0 && p.root_lo && ok) lin = p.root_lo[i];
+    // the root key (R#7), needed here only by the validity path's uniform draws
+    const uint64_t rk0 = (VALID && STRATEGY == TGL_UNIFORM && valid)
+                             ? (p.root_key ? p.root_key[i] : p.root_key_base + (uint64_t)i) : 0ull;
     // the cut times searched through the fences: all S+1 cuts of a layer-0 root with finite t_s and
     // S <= 3 (c_0 = t, c_j = t (-) (j (x) t_s)); otherwise U = t and the first window's lower bound
     const bool multi = nsb <= 3 && p.layer == 0 && isfinite(p.snapshot_len);
@@ -313,7 +383,8 @@ __global__ void __launch_bounds__(kTile, TGL_WINDOW_MINB) window_kernel(const __
         for (int b = 0; b < 3; ++b) {
             if (b >= nsb) break;
             const uint32_t c = cut[b] - cut[b + 1];
-            const uint32_t take = p.replacement ? (c ? k : 0u) : (c < k ? c : k);
+            const uint32_t take = VALID ? (valid ? select_valid<STRATEGY>(p, i, b, cut[b + 1], cut[b], rk0) : 0u)
+                                          : (p.replacement ? (c ? k : 0u) : (c < k ? c : k));
             if (valid) {
                 if (b == 0) p.cuts[i] = cut[0];
                 p.cuts[(size_t)(b + 1) * p.roots_cap + i] = cut[b + 1];
@@ -336,7 +407,8 @@ __global__ void __launch_bounds__(kTile, TGL_WINDOW_MINB) window_kernel(const __
                     a = __ldg(p.ts + bcur - 1) < xb ? bcur : lower_bound_ts(p, lo, bcur - 1, xb);
             }
             const uint32_t c = bcur - a;
-            const uint32_t take = p.replacement ? (c ? k : 0u) : (c < k ? c : k);
+            const uint32_t take = VALID ? (valid ? select_valid<STRATEGY>(p, i, b, a, bcur, rk0) : 0u)
+                                          : (p.replacement ? (c ? k : 0u) : (c < k ? c : k));
             if (valid) {
                 if (b == 0) p.cuts[i] = bcur;
                 p.cuts[(size_t)(b + 1) * p.roots_cap + i] = a;
@@ -365,7 +437,7 @@ __host__ __device__ inline int copy_warp_words(int nsb, int k, bool picks_in_sme
     return 2 * nsb * 32 + 32 + 2 * 32 + 2 * nsb + (picks_in_smem ? nsb * k * 32 : 0);
 }
 
-template <int STRATEGY>
+template <int STRATEGY, bool VALID>
 __global__ void __launch_bounds__(kTile, STRATEGY == TGL_MOST_RECENT ? TGL_COPY_MINB_MR : TGL_COPY_MINB) copy_kernel(const __grid_constant__ SampleParams p) {
     extern __shared__ __align__(16) uint32_t smem[];
     __shared__ uint32_t s_wsum[TGL_MAX_SNAPSHOTS][kWarps];
@@ -411,14 +483,15 @@ __global__ void __launch_bounds__(kTile, STRATEGY == TGL_MOST_RECENT ? TGL_COPY_
     for (int b = 0; b < nsb; ++b) {
         const uint32_t cn = valid ? p.cuts[(size_t)(b + 1) * p.roots_cap + i] : 0u;  // c_(b+1)
         const uint32_t len = cb - cn;                                                 // window size c
-        const uint32_t take = p.replacement ? (len ? (uint32_t)k : 0u) : (len < (uint32_t)k ? len : (uint32_t)k);
+        const uint32_t take = VALID ? (valid ? p.vtake[(size_t)b * p.roots_cap + i] : 0u)
+                                      : (p.replacement ? (len ? (uint32_t)k : 0u) : (len < (uint32_t)k ? len : (uint32_t)k));
         // most_recent: the take slots closest to the end pointer; uniform: picks from c_(b+1)
         first[b * 32 + lane] = STRATEGY == TGL_MOST_RECENT ? cb - take : cn;
         cb = cn;
         const uint32_t x = warp_incl_scan(take, lane);
         inc[b * 32 + lane] = x;
         if (lane == 31) s_wsum[b][warp] = x;
-        if (STRATEGY == TGL_UNIFORM) {
+        if (STRATEGY == TGL_UNIFORM && !VALID) {
             uint32_t* pk = picks + (size_t)b * k * 32 + lane;  // pick q at pk[q * 32]
             const uint32_t ctr1 = ((uint32_t)p.layer << 16) | (uint32_t)(p.layer == 0 ? b : p.snap0);
             if (!p.replacement && len <= (uint32_t)k) {
@@ -522,7 +595,9 @@ __global__ void __launch_bounds__(kTile, STRATEGY == TGL_MOST_RECENT ? TGL_COPY_
             qq[u] = q;
             rem[u] = r;
             bb[u] = b;
-            if (STRATEGY == TGL_MOST_RECENT)
+            if (VALID)  // R#28: the window kernel's explicit selection
+                pos[u] = act[u] ? p.vpicks[((size_t)b * p.roots_cap + (size_t)(warp_root0 + ro)) * k + q] : 0u;
+            else if (STRATEGY == TGL_MOST_RECENT)
                 pos[u] = first[b * 32 + ro] + q;
             else
                 pos[u] = act[u] ? first[b * 32 + ro] + picks[((size_t)b * k + q) * 32 + ro] : 0u;
@@ -638,6 +713,7 @@ struct Launch {
     uint64_t* super_tot;
     int64_t supers_cap;
     uint32_t* picks;  // global picks or null
+    uint32_t *vpicks, *vtake;  // R#28 explicit selection (edge validity) or null
 };
 
 struct SamplePlan {
@@ -660,7 +736,7 @@ struct SamplePlan {
 };
 
 static int plan_sample(int64_t n_roots, int L, const int32_t* fanouts, int S, int strategy, float snapshot_len,
-                       bool dedup, bool hop_root, void* ws, SamplePlan& P) {
+                       bool dedup, bool hop_root, bool validity, void* ws, SamplePlan& P) {
     if (L < 1 || L > 64 || S < 1 || S > TGL_MAX_SNAPSHOTS || n_roots < 0 || !fanouts) return TGL_EINVAL;
     if (!(snapshot_len > 0.0f)) return TGL_EINVAL;               // NaN or <= 0
     if (S > 1 && !std::isfinite(snapshot_len)) return TGL_EINVAL;  // +inf only for one snapshot
@@ -691,6 +767,8 @@ static int plan_sample(int64_t n_roots, int L, const int32_t* fanouts, int S, in
         la.picks = nullptr;
         if (strategy == TGL_UNIFORM && !picks_fit_smem(nsb, fanouts[layer]))
             la.picks = c.take<uint32_t>((size_t)la.tiles_cap * kTile * nsb * fanouts[layer]);
+        la.vpicks = validity ? c.take<uint32_t>((size_t)nsb * la.roots_cap * fanouts[layer]) : nullptr;
+        la.vtake = validity ? c.take<uint32_t>((size_t)nsb * la.roots_cap) : nullptr;
     };
     add(0, 0, S);
     for (int l = 1; l < L; ++l)
@@ -729,13 +807,19 @@ static int plan_sample(int64_t n_roots, int L, const int32_t* fanouts, int S, in
     return TGL_OK;
 }
 
+template <int STRATEGY, bool VALID>
+static int launch_pair(const SampleParams& sp, int64_t grid, size_t smem, cudaStream_t st) {
+    window_kernel<STRATEGY, VALID><<<(unsigned)grid, kTile, 0, st>>>(sp);
+    if (smem > 48 * 1024)
+        cudaFuncSetAttribute(copy_kernel<STRATEGY, VALID>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    copy_kernel<STRATEGY, VALID><<<(unsigned)grid, kTile, smem, st>>>(sp);
+    return cudaGetLastError() == cudaSuccess ? TGL_OK : TGL_ECUDA;
+}
+
+// the validity path (R#28) is a separate instantiation: the default kernels carry none of it
 template <int STRATEGY>
 static int launch_chain(const SampleParams& sp, int64_t grid, size_t smem, cudaStream_t st) {
-    window_kernel<STRATEGY><<<(unsigned)grid, kTile, 0, st>>>(sp);
-    if (smem > 48 * 1024)
-        cudaFuncSetAttribute(copy_kernel<STRATEGY>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    copy_kernel<STRATEGY><<<(unsigned)grid, kTile, smem, st>>>(sp);
-    return cudaGetLastError() == cudaSuccess ? TGL_OK : TGL_ECUDA;
+    return sp.valid ? launch_pair<STRATEGY, true>(sp, grid, smem, st) : launch_pair<STRATEGY, false>(sp, grid, smem, st);
 }
 
 }  // namespace tgl
@@ -746,7 +830,8 @@ extern "C" int tgl_sample_capacity(int64_t n_roots, int32_t n_layers, const int3
                                    tgl_strategy strategy, float snapshot_len, int64_t* roots_cap, int64_t* edges_cap,
                                    size_t* ws_bytes) {
     static thread_local SamplePlan P;
-    int rc = plan_sample(n_roots, n_layers, fanouts, n_snapshots, (int)strategy, snapshot_len, false, false, nullptr, P);
+    int rc = plan_sample(n_roots, n_layers, fanouts, n_snapshots, (int)strategy, snapshot_len, false, false, false,
+                         nullptr, P);
     if (rc) return rc;
     for (int l = 0; l < n_layers; ++l) {
         if (roots_cap) roots_cap[l] = P.roots_cap[l];
@@ -775,7 +860,7 @@ static int sample_impl(const tgl_tcsr* g, const int32_t* roots, const float* roo
     if (n_roots > 0 && (!roots || !root_ts)) return TGL_EINVAL;
     static thread_local SamplePlan P;
     int rc = plan_sample(n_roots, n_layers, fanouts, n_snapshots, (int)strategy, snapshot_len, dedup, hop_root,
-                         workspace, P);
+                         o.edge_valid != nullptr, workspace, P);
     if (rc) return rc;
     if (ws_bytes < P.bytes) return TGL_EWORKSPACE;
     rc = check_device();
@@ -848,6 +933,9 @@ static int sample_impl(const tgl_tcsr* g, const int32_t* roots, const float* roo
         sp.snap0 = s;
         sp.k = fanouts[l];
         sp.replacement = o.replacement;
+        sp.valid = o.edge_valid;
+        sp.vpicks = la.vpicks;
+        sp.vtake = la.vtake;
         sp.snapshot_len = snapshot_len;
         sp.seed_lo = (uint32_t)seed;
         sp.seed_hi = (uint32_t)(seed >> 32);
@@ -940,7 +1028,7 @@ extern "C" int tgl_sample_capacity_ex(int64_t n_roots, int32_t n_layers, const i
     if (opts) o = *opts;
     static thread_local SamplePlan P;
     int rc = plan_sample(n_roots, n_layers, fanouts, n_snapshots, (int)strategy, snapshot_len, o.dedup == 1,
-                         o.hop_time == TGL_HOP_ROOT_TIME, nullptr, P);
+                         o.hop_time == TGL_HOP_ROOT_TIME, o.edge_valid != nullptr, nullptr, P);
     if (rc) return rc;
     for (int l = 0; l < n_layers; ++l) {
         if (roots_cap) roots_cap[l] = P.roots_cap[l];

@@ -150,3 +150,30 @@ extern "C" int tgl_chunk_schedule(int64_t n_edges, int64_t batch_size, int64_t c
         n_edges, batch_size, chunk_size, epoch, (uint32_t)seed, (uint32_t)(seed >> 32), first_edge, cap, n_batches);
     return cudaGetLastError() == cudaSuccess ? TGL_OK : TGL_ECUDA;
 }
+
+// ---------------------------------------------------------------------------- R#28 validity
+namespace tgl {
+__global__ void edge_valid_set_kernel(uint32_t* __restrict__ valid, int64_t n_bits, const int32_t* __restrict__ eids,
+                                      int64_t n, int32_t value) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t e = eids[i];
+        if (e < 0 || e >= n_bits) continue;
+        const uint32_t bit = 1u << (e & 31);
+        if (value)
+            atomicOr(valid + (e >> 5), bit);
+        else
+            atomicAnd(valid + (e >> 5), ~bit);
+    }
+}
+}  // namespace tgl
+
+extern "C" int tgl_edge_valid_set(uint32_t* valid, int64_t n_bits, const int32_t* eids, int64_t n, int32_t value,
+                                  void* stream) {
+    if (n < 0 || n_bits < 0 || (n > 0 && (!valid || !eids)) || (value != 0 && value != 1)) return TGL_EINVAL;
+    int rc = check_device();
+    if (rc) return rc;
+    if (n == 0) return TGL_OK;
+    const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 148 * 4));
+    edge_valid_set_kernel<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(valid, n_bits, eids, n, value);
+    return cudaGetLastError() == cudaSuccess ? TGL_OK : TGL_ECUDA;
+}

@@ -130,3 +130,58 @@ def test_dedup_bit_exact(tgl, hop_time):
             np.testing.assert_array_equal(x.src_index[:nnz].cpu().numpy(), o["src_index"])
             np.testing.assert_array_equal(x.uniq_node[:nu].cpu().numpy(), o["uniq_node"])
             np.testing.assert_array_equal(x.uniq_ts[:nu].cpu().numpy().view(np.uint32), o["uniq_ts"].view(np.uint32))
+
+
+def _np_mask(rng, n, frac):
+    bits = rng.random(max(n, 1)) < frac
+    words = np.zeros((len(bits) + 31) // 32, dtype=np.uint32)
+    idx = np.nonzero(bits)[0]
+    np.bitwise_or.at(words, idx >> 5, (np.uint32(1) << (idx & 31).astype(np.uint32)))
+    return words
+
+
+@pytest.mark.parametrize("strategy,replacement", [(0, False), (1, False), (1, True)])
+def test_edge_validity_bit_exact(tgl, strategy, replacement):
+    """R#28: invalid edges are not candidates -- GPU vs oracle on random graphs and masks."""
+    rng = np.random.default_rng(90 + strategy + 2 * replacement)
+    for case in range(40):
+        n_nodes = int(rng.integers(1, 400))
+        n_edges = int(rng.integers(0, 6000))
+        src, dst, ts, eid = random_graph(1500 + case, n_nodes, n_edges, integer_times=case % 3 != 0)
+        roots, rts = random_roots(1500 + case, n_nodes, int(rng.integers(0, 1500)), integer_times=case % 3 != 0)
+        L = 1 + case % 3
+        fanouts = [int(rng.integers(1, 12)) for _ in range(L)]
+        S = int(rng.integers(1, 5))
+        t_s = math.inf if S == 1 and case % 4 else float(rng.choice([1.0, 2.5, 7.0]))
+        seed, base = int(rng.integers(0, 2**63)), int(rng.integers(0, 2**40))
+        add_rev = bool(case % 2)
+        mask = _np_mask(rng, n_edges, float(rng.choice([0.0, 0.25, 0.7, 1.0])))
+        go = oracle.build(src, dst, ts, None, n_nodes=n_nodes, add_reverse=add_rev)
+        g = tgl.build(cu(src, torch.int32), cu(dst, torch.int32), cu(ts, torch.float32), None, n_nodes=n_nodes,
+                      add_reverse=add_rev)
+        bo = oracle.sample(go, roots, rts, fanouts=fanouts, strategy=strategy, n_snapshots=S, snapshot_len=t_s,
+                           seed=seed, root_key_base=base, replacement=replacement, edge_valid=mask)
+        b = tgl.sample(g, cu(roots, torch.int32), cu(rts, torch.float32), fanouts=fanouts, strategy=strategy,
+                       n_snapshots=S, snapshot_len=t_s, seed=seed, root_key_base=base, replacement=replacement,
+                       edge_valid=torch.from_numpy(mask.view(np.int32)).cuda())
+        for j, (x, o) in enumerate(zip(b, bo)):
+            off, nbr, e, dt, _ = x.trimmed()
+            np.testing.assert_array_equal(off.cpu().numpy(), o["offsets"], err_msg=f"case {case} block {j}")
+            np.testing.assert_array_equal(nbr.cpu().numpy(), o["nbr"])
+            np.testing.assert_array_equal(e.cpu().numpy(), o["eid"])
+            np.testing.assert_array_equal(dt.cpu().numpy().view(np.uint32), o["dt"].view(np.uint32))
+
+
+def test_edge_valid_set(tgl):
+    rng = np.random.default_rng(3)
+    n_bits = 5000
+    mask = _np_mask(rng, n_bits, 0.5)
+    g_mask = torch.from_numpy(mask.view(np.int32).copy()).cuda()
+    ids = rng.integers(-5, n_bits + 5, 800).astype(np.int32)
+    tgl.edge_valid_set(g_mask, torch.from_numpy(ids).cuda(), False, n_bits=n_bits)
+    ok = ids[(ids >= 0) & (ids < n_bits)]
+    np.bitwise_and.at(mask, ok >> 5, ~(np.uint32(1) << (ok & 31).astype(np.uint32)))
+    np.testing.assert_array_equal(g_mask.cpu().numpy().view(np.uint32), mask)
+    tgl.edge_valid_set(g_mask, torch.from_numpy(ids).cuda(), True, n_bits=n_bits)
+    np.bitwise_or.at(mask, ok >> 5, (np.uint32(1) << (ok & 31).astype(np.uint32)))
+    np.testing.assert_array_equal(g_mask.cpu().numpy().view(np.uint32), mask)
