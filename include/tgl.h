@@ -359,6 +359,12 @@ TGL_API int tgl_shard_bucket_workspace(int64_t n_roots, int32_t world, size_t *b
 TGL_API int tgl_shard_bucket(const int32_t *roots, int64_t n_roots, const int64_t *splits, int32_t world,
                      int32_t *perm, int64_t *counts, void *workspace, size_t ws_bytes, void *stream);
 
+/* inv[perm[j]] = j for a permutation perm of [0, n) (device int32): with tgl_gather it returns rows
+ * received in bucket order to request order (node-sharded gather of node memory / mailbox rows,
+ * SURVEY 8(f) rank 3; the shard-local tables are addressed with global ids through a base pointer
+ * offset by -lo rows, valid because owner bucketing only sends a shard ids in [lo, hi)). */
+TGL_API int tgl_perm_invert(const int32_t *perm, int64_t n, int32_t *inv, void *stream);
+
 /* counts[i] = offsets[i+1] - offsets[i] (device, int32), e.g. to send a block's per-root counts back. */
 TGL_API int tgl_offsets_to_counts(const int64_t *offsets, int64_t n_roots, int32_t *counts, void *stream);
 

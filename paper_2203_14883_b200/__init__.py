@@ -380,6 +380,50 @@ def edge_valid_set(valid: torch.Tensor, eids: torch.Tensor, value: bool, n_bits:
         "tgl_edge_valid_set")
 
 
+def perm_invert(perm: torch.Tensor, stream=None) -> torch.Tensor:
+    """tgl_perm_invert: inv[perm[j]] = j (int32)."""
+    perm = _cuda(perm, torch.int32, "perm")
+    inv = torch.empty_like(perm)
+    _rc(_L.tgl_perm_invert(_ptr(perm), perm.numel(), _ptr(inv), _stream(stream)), "tgl_perm_invert")
+    return inv
+
+
+def gather_rows_at(ids: torch.Tensor, table: torch.Tensor, row_lo: int, n_rows_global: int, out: torch.Tensor,
+                   n_ids_dev: Optional[torch.Tensor] = None, stream=None) -> None:
+    """tgl_gather on a shard-local table holding global rows [row_lo, row_lo + table.shape[0]),
+    addressed with GLOBAL ids: the table base is offset by -row_lo rows (the ids a shard receives
+    are >= row_lo by construction of the owner bucketing); ids >= n_rows_global give zero rows."""
+    ids = _cuda(ids, torch.int32, "ids")
+    rb = table.element_size() * (table[0].numel() if table.dim() > 1 else 1) if table.shape[0] else \
+        table.element_size() * int(np.prod(table.shape[1:], dtype=np.int64))
+    arr = (_lib.GatherTable * 1)()
+    arr[0] = _lib.GatherTable(table.data_ptr() - int(row_lo) * rb, int(n_rows_global), rb, out.data_ptr())
+    _rc(_L.tgl_gather(_ptr(ids), ids.numel(), _ptr(n_ids_dev), arr, 1, _stream(stream)), "tgl_gather")
+
+
+def state_write_at(ids: torch.Tensor, ts: Optional[torch.Tensor], tables, *, node_lo: int, n_nodes_global: int,
+                   K: int = 1, pos: Optional[torch.Tensor] = None, ts_table: Optional[torch.Tensor] = None,
+                   stream=None) -> None:
+    """tgl_state_write on shard-local state holding the rings of global nodes [node_lo, ...) and
+    addressed with GLOBAL ids (base pointers offset by -node_lo nodes; the owner bucketing only
+    sends a shard ids >= node_lo).  tables: [(rows [n, ...], local table [n_local * K, ...])]."""
+    ids = _cuda(ids, torch.int32, "ids")
+    n = ids.numel()
+    lo = int(node_lo)
+    arr = (_lib.StateTable * max(len(tables), 1))()
+    for j, (rows, table) in enumerate(tables):
+        rb = table.element_size() * (table[0].numel() if table.dim() > 1 else 1) if table.shape[0] else \
+            table.element_size() * int(np.prod(table.shape[1:], dtype=np.int64))
+        arr[j] = _lib.StateTable(rows.data_ptr() if n else None, rb, table.data_ptr() - lo * K * rb)
+    b = ctypes.c_size_t()
+    _rc(_L.tgl_state_write_workspace(n, int(n_nodes_global), ctypes.byref(b)), "tgl_state_write_workspace")
+    ws = torch.empty(max(b.value, 1), dtype=torch.uint8, device=ids.device)
+    pos_p = None if pos is None else pos.data_ptr() - lo * 4
+    tst_p = None if ts_table is None else ts_table.data_ptr() - lo * K * 4
+    _rc(_L.tgl_state_write(_ptr(ids), _ptr(ts), n, int(n_nodes_global), int(K), pos_p, tst_p, arr, len(tables),
+                           _ptr(ws), b.value, _stream(stream)), "tgl_state_write")
+
+
 def check(g: Optional[TCSR] = None, stream=None) -> int:
     """tgl_check: synchronise and return (and clear) the sticky device error code (0 = none)."""
     return _L.tgl_check(None if g is None else g.handle, _stream(stream))

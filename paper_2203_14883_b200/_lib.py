@@ -68,6 +68,7 @@ SIGNATURES = {
     "tgl_gather": (ctypes.c_int, [P, i64, P, P, i32, P]),
     "tgl_chunk_schedule": (ctypes.c_int, [i64, i64, i64, u64, u64, P, i64, P, P]),
     "tgl_edge_valid_set": (ctypes.c_int, [P, i64, P, i64, i32, P]),
+    "tgl_perm_invert": (ctypes.c_int, [P, i64, P, P]),
     "tgl_state_write_workspace": (ctypes.c_int, [i64, i32, ctypes.POINTER(sz)]),
     "tgl_state_write": (ctypes.c_int, [P, P, i64, i32, i32, P, P, P, i32, P, sz, P]),
     "tgl_check": (ctypes.c_int, [P, P]),

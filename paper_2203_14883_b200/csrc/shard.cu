@@ -177,3 +177,23 @@ extern "C" int tgl_edge_valid_set(uint32_t* valid, int64_t n_bits, const int32_t
     edge_valid_set_kernel<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(valid, n_bits, eids, n, value);
     return cudaGetLastError() == cudaSuccess ? TGL_OK : TGL_ECUDA;
 }
+
+// ---------------------------------------------------------------------------- sharded tables
+// inv[perm[j]] = j: turns a bucket-order row list back into request order with one tgl_gather
+// (node-sharded gather).
+namespace tgl {
+__global__ void perm_invert_kernel(const int32_t* __restrict__ perm, int64_t n, int32_t* __restrict__ inv) {
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x)
+        inv[perm[j]] = (int32_t)j;
+}
+}  // namespace tgl
+
+extern "C" int tgl_perm_invert(const int32_t* perm, int64_t n, int32_t* inv, void* stream) {
+    if (n < 0 || n >= (int64_t(1) << 31) || (n > 0 && (!perm || !inv))) return TGL_EINVAL;
+    int rc = check_device();
+    if (rc) return rc;
+    if (n == 0) return TGL_OK;
+    const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 148 * 8));
+    perm_invert_kernel<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(perm, n, inv);
+    return cudaGetLastError() == cudaSuccess ? TGL_OK : TGL_ECUDA;
+}

@@ -140,6 +140,89 @@ class NodeShardedSampler:
         return out
 
 
+class CudaTableOps:
+    """Product ops of the sharded node tables: libtgl.so kernels only."""
+
+    def __init__(self):
+        import paper_2203_14883_b200 as tgl
+        self.tgl = tgl
+
+    def bucket(self, ids, splits, world):
+        return self.tgl.shard_bucket(ids, splits, world)
+
+    def pack(self, perm, tensors):
+        return self.tgl.gather(perm, tensors)
+
+    def invert(self, perm):
+        return self.tgl.perm_invert(perm)
+
+    def local_gather(self, ids, table, lo, n_global):
+        out = torch.empty((ids.numel(),) + tuple(table.shape[1:]), dtype=table.dtype, device=table.device)
+        self.tgl.gather_rows_at(ids, table, lo, n_global, out)
+        return out
+
+    def local_state_write(self, ids, ts, pairs, lo, n_global, K, pos, ts_table):
+        self.tgl.state_write_at(ids, ts, pairs, node_lo=lo, n_nodes_global=n_global, K=K, pos=pos, ts_table=ts_table)
+
+
+class ShardedNodeTables:
+    """Node memory / mailbox sharded by the node-sharded T-CSR's ranges (MAG's
+    121 M x (100 + K x 428) fp32 state does not fit one GPU).  Rank r holds the rows of
+    nodes [splits[r], splits[r+1]); each local table is [n_local * K, ...] (K ring slots per node,
+    state-write layout; K = 1 for memory).
+
+      gather(ids)             Fig. 2 step 2 across shards: owner bucketing (K8), all-to-all-v of the
+                              ids, local tgl_gather, all-to-all-v of the rows back, request order
+                              restored by tgl_gather through the inverse permutation.  Returns each
+                              table's rows (a node's whole K-slot ring per id).
+      state_write(ids, ts, rows)
+                              Fig. 2 step 6 across shards: the events go to their owners (stable
+                              bucketing: each owner receives them in (source rank, batch index)
+                              order -- the global event order, R#25) and are applied there by
+                              tgl_state_write.
+    """
+
+    def __init__(self, splits: torch.Tensor, exchange, ops, tables: Sequence[torch.Tensor], K: int = 1,
+                 pos: Optional[torch.Tensor] = None, ts_table: Optional[torch.Tensor] = None):
+        self.splits = splits
+        self.ex = exchange
+        self.ops = ops
+        self.tables = list(tables)
+        self.K = int(K)
+        self.pos = pos
+        self.ts_table = ts_table
+        r = exchange.rank
+        self.lo, self.hi = int(splits[r]), int(splits[r + 1])
+        self.n_global = int(splits[-1])
+
+    def _route(self, ids):
+        W = self.ex.world
+        perm, counts = self.ops.bucket(ids, self.splits, W)
+        send = counts.to(torch.int64)
+        recv = self.ex.splits(send)
+        return perm, send.tolist(), recv.tolist()
+
+    def gather(self, ids: torch.Tensor) -> List[torch.Tensor]:
+        perm, sr, rr = self._route(ids)
+        q_ids = self.ex.exchange(self.ops.pack(perm, [ids])[0], sr, rr)
+        inv = self.ops.invert(perm)
+        outs = []
+        for t in self.tables:
+            node_rows = t.reshape((t.shape[0] // self.K, -1) if t.dim() > 1 or self.K > 1 else (t.shape[0],))
+            rows = self.ops.local_gather(q_ids, node_rows, self.lo, self.n_global)
+            back = self.ex.exchange(rows, rr, sr)
+            outs.append(self.ops.pack(inv, [back])[0])
+        return outs
+
+    def state_write(self, ids: torch.Tensor, ts: torch.Tensor, rows: Sequence[torch.Tensor]) -> None:
+        perm, sr, rr = self._route(ids)
+        packed = self.ops.pack(perm, [ids, ts] + list(rows))
+        recv = [self.ex.exchange(x, sr, rr) for x in packed]
+        q_ids, q_ts, q_rows = recv[0], recv[1], recv[2:]
+        self.ops.local_state_write(q_ids, q_ts, list(zip(q_rows, self.tables)), self.lo, self.n_global, self.K,
+                                   self.pos, self.ts_table)
+
+
 def slice_shard(g, lo: int, hi: int):
     """Setup helper: the shard of a full T-CSR for nodes [lo, hi) as its own handle (copies)."""
     import paper_2203_14883_b200 as tgl

@@ -87,3 +87,80 @@ def test_node_sharded_equals_replicated(world, strategy, S, t_s):
             assert torch.equal(got.offsets, off)
             assert torch.equal(got.nbr, nbr) and torch.equal(got.eid, eid)
             assert torch.equal(got.dt.view(torch.int32), dt.view(torch.int32))
+
+
+def _run_ranks(world, fn):
+    hub = _Hub(world)
+    errors = []
+
+    def main(r):
+        try:
+            fn(r, LocalExchange(hub, r))
+            torch.cuda.synchronize()
+        except Exception as e:  # noqa: BLE001
+            errors.append(e)
+            hub.barrier.abort()
+
+    th = [threading.Thread(target=main, args=(r,)) for r in range(world)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert not errors, errors
+
+
+@pytest.mark.parametrize("world,K", [(2, 1), (3, 3), (4, 10)])
+def test_sharded_node_tables_gather_and_state_write(world, K):
+    """SURVEY 8(f) rank 3: node tables sharded by node range.  gather == the full tables' rows;
+    state_write == the oracle's sequential state write of all ranks' events in (rank, index) order."""
+    import oracle
+    from paper_2203_14883_b200 import sharded as sh
+    rng = np.random.default_rng(world * 10 + K)
+    V, w = 2500, 37
+    splits = torch.tensor(sorted({0, V, *rng.integers(1, V, world - 1).tolist()}), dtype=torch.int64).cuda()
+    if splits.numel() != world + 1:
+        splits = torch.linspace(0, V, world + 1).round().to(torch.int64).cuda()
+    full = rng.standard_normal((V * K, w)).astype(np.float32)
+    full_ts = rng.random(V * K).astype(np.float32)
+    full_pos = rng.integers(0, K, V).astype(np.int32)
+    sp = splits.cpu().numpy()
+    local = [(torch.from_numpy(full[sp[r] * K:sp[r + 1] * K].copy()).cuda(),
+              torch.from_numpy(full_ts[sp[r] * K:sp[r + 1] * K].copy()).cuda(),
+              torch.from_numpy(full_pos[sp[r]:sp[r + 1]].copy()).cuda()) for r in range(world)]
+    q_ids = [rng.integers(-1, V, int(rng.integers(0, 3000))).astype(np.int32) for _ in range(world)]
+    ev = []
+    for r in range(world):
+        n = int(rng.integers(0, 4000))
+        ev.append(((rng.zipf(1.4, n) % V).astype(np.int32), np.sort(rng.random(n)).astype(np.float32),
+                   rng.standard_normal((n, w)).astype(np.float32)))
+    got = [None] * world
+
+    def fn(r, ex):
+        t, tts, pos = local[r]
+        tabs = sh.ShardedNodeTables(splits, ex, sh.CudaTableOps(), [t, tts], K=K, pos=pos if K > 1 else None,
+                                    ts_table=None)
+        got[r] = [x.cpu().numpy() for x in tabs.gather(torch.from_numpy(q_ids[r]).cuda())]
+        ids, ts, rows = ev[r]
+        tabs.state_write(torch.from_numpy(ids).cuda(), torch.from_numpy(ts).cuda(),
+                         [torch.from_numpy(rows).cuda(), torch.from_numpy(ts).cuda()])
+
+    _run_ranks(world, fn)
+    node_rows, node_ts = full.reshape(V, K * w), full_ts.reshape(V, K)
+    for r in range(world):
+        ids = q_ids[r]
+        want = np.where((ids >= 0)[:, None], node_rows[np.clip(ids, 0, V - 1)], 0.0)
+        np.testing.assert_array_equal(got[r][0], want)
+        np.testing.assert_array_equal(got[r][1], np.where((ids >= 0)[:, None], node_ts[np.clip(ids, 0, V - 1)], 0.0))
+    # reference: one sequential state write of every rank's events in (rank, index) order
+    ids = np.concatenate([e[0] for e in ev])
+    ts = np.concatenate([e[1] for e in ev])
+    rows = np.concatenate([e[2] for e in ev])
+    ref, ref_ts, ref_pos = full.copy(), full_ts.copy(), full_pos.copy()
+    oracle.state_write(ids, ts, n_nodes=V, K=K, tables=[(rows, ref), (ts.copy(), ref_ts)],
+                       pos=ref_pos if K > 1 else None)
+    for r in range(world):
+        t, tts, pos = local[r]
+        np.testing.assert_array_equal(t.cpu().numpy(), ref[sp[r] * K:sp[r + 1] * K])
+        np.testing.assert_array_equal(tts.cpu().numpy(), ref_ts[sp[r] * K:sp[r + 1] * K])
+        if K > 1:
+            np.testing.assert_array_equal(pos.cpu().numpy(), ref_pos[sp[r]:sp[r + 1]])

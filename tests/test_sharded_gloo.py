@@ -98,3 +98,80 @@ def test_node_sharded_protocol_gloo_world2(tmp_path, S, ts, strat):
                        env=env, capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     assert "RANK0OK" in r.stdout and "RANK1OK" in r.stdout
+
+
+TABLE_WORKER = textwrap.dedent(r'''
+    import os, sys
+    sys.path.insert(0, os.environ["REPO"])
+    import numpy as np, torch, torch.distributed as dist
+    import oracle
+    import importlib.util
+    spec = importlib.util.spec_from_file_location("sharded", os.path.join(os.environ["REPO"], "paper_2203_14883_b200", "sharded.py"))
+    sh = importlib.util.module_from_spec(spec); spec.loader.exec_module(sh)
+
+    dist.init_process_group("gloo")
+    rank, world = dist.get_rank(), dist.get_world_size()
+    K = int(os.environ["K"])
+    V, w = 300, 5
+    rng = np.random.default_rng(7)                      # same full state on every rank
+    full = rng.standard_normal((V * K, w)).astype(np.float32)
+    pos0 = rng.integers(0, K, V).astype(np.int32)
+    splits = torch.tensor([0, 131, V], dtype=torch.int64)
+    lo, hi = int(splits[rank]), int(splits[rank + 1])
+
+    class CpuTableOps:                                  # test double: numpy + the oracle's state write
+        def bucket(self, ids, splits, world):
+            owner = np.searchsorted(splits.numpy()[1:-1], ids.numpy(), side="right")
+            perm = np.argsort(owner, kind="stable").astype(np.int32)
+            return torch.from_numpy(perm), torch.from_numpy(np.bincount(owner, minlength=world).astype(np.int64))
+        def pack(self, perm, tensors):
+            return [t[perm.long()].contiguous() for t in tensors]
+        def invert(self, perm):
+            inv = np.empty(len(perm), np.int32); inv[perm.numpy()] = np.arange(len(perm), dtype=np.int32)
+            return torch.from_numpy(inv)
+        def local_gather(self, ids, table, lo, n_global):
+            return table[(ids - lo).long()].contiguous()
+        def local_state_write(self, ids, ts, pairs, lo, n_global, K, pos, ts_table):
+            loc = (ids.numpy() - lo).astype(np.int32)
+            oracle.state_write(loc, ts.numpy(), n_nodes=hi - lo, K=K,
+                               tables=[(r.numpy(), t.numpy()) for r, t in pairs],
+                               pos=None if pos is None else pos.numpy())
+
+    table = torch.from_numpy(full[lo * K:hi * K].copy())
+    pos = torch.from_numpy(pos0[lo:hi].copy())
+    tabs = sh.ShardedNodeTables(splits, sh.DistExchange(), CpuTableOps(), [table], K=K, pos=pos if K > 1 else None)
+    q = np.random.default_rng(100 + rank).integers(0, V, 50).astype(np.int32)
+    got = tabs.gather(torch.from_numpy(q))[0].numpy()
+    assert np.array_equal(got, full.reshape(V, K * w)[q])
+    evs = []
+    for r in range(world):
+        g = np.random.default_rng(200 + r)
+        n = 40 + 9 * r
+        evs.append(((g.zipf(1.5, n) % V).astype(np.int32), np.arange(n, dtype=np.float32),
+                    g.standard_normal((n, w)).astype(np.float32)))
+    ids, ts, rows = evs[rank]
+    tabs.state_write(torch.from_numpy(ids), torch.from_numpy(ts), [torch.from_numpy(rows)])
+    ref, ref_pos = full.copy(), pos0.copy()
+    oracle.state_write(np.concatenate([e[0] for e in evs]), np.concatenate([e[1] for e in evs]), n_nodes=V, K=K,
+                       tables=[(np.concatenate([e[2] for e in evs]), ref)], pos=ref_pos if K > 1 else None)
+    assert np.array_equal(table.numpy(), ref[lo * K:hi * K])
+    if K > 1:
+        assert np.array_equal(pos.numpy(), ref_pos[lo:hi])
+    dist.barrier()
+    dist.destroy_process_group()
+    print(f"RANK{rank}OK", flush=True)
+''')
+
+
+@pytest.mark.parametrize("K", [1, 3])
+def test_sharded_node_tables_protocol_gloo_world2(tmp_path, K):
+    """ShardedNodeTables (SURVEY 8(f) rank 3) over a real 2-process gloo all-to-all: gather returns
+    the full tables' rows; state_write equals one sequential write of both ranks' events."""
+    script = tmp_path / "table_worker.py"
+    script.write_text(TABLE_WORKER)
+    env = dict(os.environ, REPO=ROOT, K=str(K), MASTER_ADDR="127.0.0.1")
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+                        "--master-addr=127.0.0.1", f"--master-port={_free_port()}", str(script)],
+                       env=env, capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    assert "RANK0OK" in r.stdout and "RANK1OK" in r.stdout
