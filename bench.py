@@ -217,6 +217,25 @@ def measured_traffic(key: str, roots_per_step: float):
     return d["bytes_per_root"] * roots_per_step, src
 
 
+def measured_shares(key: str):
+    """Per-kernel DRAM bytes per root and share of the sampler kernels' time in the committed ncu
+    capture (same file as measured_traffic) -- for comparing with the live step time."""
+    import glob
+    path = os.environ.get("TGL_TRAFFIC_JSON")
+    if not path:
+        cands = sorted(glob.glob(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r*",
+                                              "traffic.json")))
+        path = cands[-1] if cands else None
+    if not path or not os.path.exists(path):
+        return None
+    d = json.load(open(path)).get(key)
+    if not d:
+        return None
+    tot = sum(v["us"] for v in d["kernels"].values())
+    return {k: {"ncu_us": v["us"], "share": v["us"] / tot, "dram_bytes_per_root": (v["dram_read"] + v["dram_write"])
+                / d["roots"]} for k, v in d["kernels"].items()}
+
+
 def reduce_report(edges: float, nbytes: float, ms: float, world: int, dev):
     """Reporting only (outside the timed region): sum of work over ranks, max of device time."""
     if world == 1:
@@ -494,6 +513,7 @@ def run_ours(args):
                           f"{n_distinct} distinct root chunks cycled over the steps")},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic, "traffic_source": traffic_src, "peak_source": peak_src,
+                     "kernels_ncu": measured_shares(key) if gather is None else None,
                      "kernel": (f"tgl_sample ({cfg.strategy}): window_kernel + copy_kernel"
                                 + (" + tgl_gather (3 launches) + tgl_state_write" if gather is not None else "")
                                 + ", timed together"),
