@@ -433,11 +433,15 @@ __global__ void __launch_bounds__(kTile, TGL_WINDOW_MINB) window_kernel(const __
 }
 
 // ---------------------------------------------------------------------------- K4b copy
+// Per warp shared memory (words): inclusive counts [nsb][32]; segment list [nsb*32] of uint2
+// {start << 9 | b << 5 | r, first slot} (the warp's non-empty (block, root) windows in output
+// order); root times [32]; root keys [32] (u64); per-block output pointers pre-offset to the
+// warp's first output {nbr, eid, dt, pad} (u64 each); uniform picks [nsb][k][32].
 __host__ __device__ inline int copy_warp_words(int nsb, int k, bool picks_in_smem) {
-    return 2 * nsb * 32 + 32 + 2 * 32 + 2 * nsb + (picks_in_smem ? nsb * k * 32 : 0);
+    return nsb * 32 + 2 * nsb * 32 + 32 + 2 * 32 + 8 * nsb + (picks_in_smem ? nsb * k * 32 : 0);
 }
 
-template <int STRATEGY, bool VALID>
+template <int STRATEGY, bool VALID, bool EXTRA>
 __global__ void __launch_bounds__(kTile, STRATEGY == TGL_MOST_RECENT ? TGL_COPY_MINB_MR : TGL_COPY_MINB) copy_kernel(const __grid_constant__ SampleParams p) {
     extern __shared__ __align__(16) uint32_t smem[];
     __shared__ uint32_t s_wsum[TGL_MAX_SNAPSHOTS][kWarps];
@@ -461,36 +465,44 @@ __global__ void __launch_bounds__(kTile, STRATEGY == TGL_MOST_RECENT ? TGL_COPY_
     const int k = p.k;
     const bool picks_smem = STRATEGY == TGL_UNIFORM && p.picks_global == nullptr;
     uint32_t* ws = smem + warp * copy_warp_words(nsb, k, picks_smem);
-    uint32_t* inc = ws;                                         // [nsb][32] inclusive counts
-    uint32_t* first = inc + nsb * 32;                           // [nsb][32]
-    float* troot = reinterpret_cast<float*>(first + nsb * 32);  // [32]
-    uint64_t* rkey = reinterpret_cast<uint64_t*>(troot + 32);   // [32] (even word offset)
-    uint64_t* base = rkey + 32;                                 // [nsb]
+    uint32_t* inc = ws;                                                   // [nsb][32]
+    uint2* seg = reinterpret_cast<uint2*>(inc + nsb * 32);                // [nsb * 32]
+    float* troot = reinterpret_cast<float*>(seg + nsb * 32);              // [32]
+    uint64_t* rkey = reinterpret_cast<uint64_t*>(troot + 32);             // [32] (even word offset)
+    uint64_t* wptr = rkey + 32;                                           // [nsb][4]
     uint32_t* picks = nullptr;
     if (STRATEGY == TGL_UNIFORM)
-        picks = picks_smem ? reinterpret_cast<uint32_t*>(base + nsb)
+        picks = picks_smem ? reinterpret_cast<uint32_t*>(wptr + 4 * nsb)
                            : p.picks_global + ((size_t)tile * kWarps + warp) * nsb * k * 32;
 
     const float t = valid ? p.root_ts[i] : 0.0f;
     troot[lane] = t;
     uint64_t rk = 0;
-    if (STRATEGY == TGL_UNIFORM) {
+    if (STRATEGY == TGL_UNIFORM || EXTRA) {
         rk = p.root_key ? (valid ? p.root_key[i] : 0ull) : p.root_key_base + (uint64_t)i;
         rkey[lane] = rk;
     }
-    // counts, warp-local prefix, window descriptors; uniform picks
+    // counts, warp-local prefix, the segment list; uniform picks
     uint32_t cb = valid ? p.cuts[i] : 0u;  // c_b
+    uint32_t flat = 0, nseg = 0;           // warp outputs / non-empty windows of the blocks before b
     for (int b = 0; b < nsb; ++b) {
         const uint32_t cn = valid ? p.cuts[(size_t)(b + 1) * p.roots_cap + i] : 0u;  // c_(b+1)
         const uint32_t len = cb - cn;                                                 // window size c
         const uint32_t take = VALID ? (valid ? p.vtake[(size_t)b * p.roots_cap + i] : 0u)
-                                      : (p.replacement ? (len ? (uint32_t)k : 0u) : (len < (uint32_t)k ? len : (uint32_t)k));
+                                    : (p.replacement ? (len ? (uint32_t)k : 0u) : (len < (uint32_t)k ? len : (uint32_t)k));
         // most_recent: the take slots closest to the end pointer; uniform: picks from c_(b+1)
-        first[b * 32 + lane] = STRATEGY == TGL_MOST_RECENT ? cb - take : cn;
+        const uint32_t first = STRATEGY == TGL_MOST_RECENT ? cb - take : cn;
         cb = cn;
         const uint32_t x = warp_incl_scan(take, lane);
         inc[b * 32 + lane] = x;
+        const uint32_t wtot = __shfl_sync(kFull, x, 31);
         if (lane == 31) s_wsum[b][warp] = x;
+        const uint32_t nz = __ballot_sync(kFull, take > 0);
+        if (take > 0)
+            seg[nseg + __popc(nz & lanemask_lt())] =
+                make_uint2(((flat + x - take) << 9) | ((uint32_t)b << 5) | (uint32_t)lane, first);
+        nseg += __popc(nz);
+        flat += wtot;
         if (STRATEGY == TGL_UNIFORM && !VALID) {
             uint32_t* pk = picks + (size_t)b * k * 32 + lane;  // pick q at pk[q * 32]
             const uint32_t ctr1 = ((uint32_t)p.layer << 16) | (uint32_t)(p.layer == 0 ? b : p.snap0);
@@ -548,59 +560,66 @@ __global__ void __launch_bounds__(kTile, STRATEGY == TGL_MOST_RECENT ? TGL_COPY_
     }
     __syncthreads();
     const bool last_tile = base_i + kTile >= n;
+    uint32_t fb = 0;  // warp-flat index of block b's first output
     for (int b = 0; b < nsb; ++b) {
         uint64_t wb = s_tbase[b];
         for (int w = 0; w < warp; ++w) wb += s_wsum[b][w];
+        const BlockOut& o = p.out[b];
         if (last_tile && threadIdx.x == 0) {  // chain totals: offsets[n], nnz, n_roots
             uint64_t tot = wb;
             for (int w = 0; w < kWarps; ++w) tot += s_wsum[b][w];
-            const BlockOut& o = p.out[b];
             o.offsets[n] = (int64_t)tot;
             *o.nnz_dev = (int64_t)tot;
             *o.n_roots_dev = n;
         }
-        if (lane == 0) base[b] = wb;
-        const uint32_t ex = lane ? inc[b * 32 + lane - 1] : 0u;
-        if (valid) p.out[b].offsets[i] = (int64_t)(wb + ex);
+        // block b's output j of this warp (warp-flat index fb + j) goes to global index wb + j
+        const int64_t adj = (int64_t)wb - (int64_t)fb;
+        if (lane < 3) wptr[b * 4 + lane] = (uint64_t)(lane == 0 ? (uintptr_t)(o.nbr + adj)
+                                                       : lane == 1 ? (uintptr_t)(o.eid + adj) : (uintptr_t)(o.dt + adj));
+        const uint32_t x = inc[b * 32 + lane];
+        const uint32_t ex = __shfl_up_sync(kFull, x, 1);
+        if (valid) o.offsets[i] = (int64_t)(wb + (lane ? ex : 0u));
+        fb += __shfl_sync(kFull, x, 31);
     }
     __syncwarp();
 
     const int64_t warp_root0 = i - lane;  // global index of this warp's first root
-    // flat copy over all snapshot blocks of the warp: output o -> block b (running over the warp's
-    // block totals) -> root r (5-step search of the block's inclusive counts) -> slot
-    uint32_t total = 0;
-    for (int b = 0; b < nsb; ++b) total += inc[b * 32 + 31];
+    // flat copy over all snapshot blocks of the warp, 32 outputs per step: the windows starting in
+    // the step's range set one bit each (one OR-reduction), so output o's window is found with a
+    // popc -- h = (windows starting <= o) - 1 -- instead of a search
+    const uint32_t total = flat;
+    const uint32_t lemask = lanemask_lt() | (1u << lane);
+    uint32_t hbase = 0;  // windows starting before o0
     for (uint32_t o0 = 0; o0 < total; o0 += 32 * kCopyUnroll) {
-        uint32_t pos[kCopyUnroll], rr[kCopyUnroll], qq[kCopyUnroll], rem[kCopyUnroll];
-        int bb[kCopyUnroll];
+        uint32_t pos[kCopyUnroll], info[kCopyUnroll], oo[kCopyUnroll];
         bool act[kCopyUnroll];
 #pragma unroll
         for (int u = 0; u < kCopyUnroll; ++u) {
-            const uint32_t oi = o0 + (uint32_t)(u * 32 + lane);
-            act[u] = oi < total;
-            int b = 0;
-            uint32_t r = act[u] ? oi : 0u;
-            while (b < nsb - 1 && r >= inc[b * 32 + 31]) {
-                r -= inc[b * 32 + 31];
-                ++b;
+            const uint32_t c0 = o0 + 32u * u;
+            const uint32_t hl = hbase + lane;
+            uint32_t bit = 0;
+            if (hl < nseg) {
+                const uint32_t st = (seg[hl].x >> 9) - c0;
+                bit = st < 32u ? 1u << st : 0u;
             }
-            const uint32_t* incb = inc + b * 32;
-            uint32_t ro = 0;  // root of output r: first with incb[ro] > r
-#pragma unroll
-            for (int s2 = 16; s2 > 0; s2 >>= 1)
-                if (incb[ro + s2 - 1] <= r) ro += s2;
-            ro = act[u] ? ro : 0u;
-            const uint32_t q = act[u] ? r - (ro ? incb[ro - 1] : 0u) : 0u;
-            rr[u] = ro;
-            qq[u] = q;
-            rem[u] = r;
-            bb[u] = b;
-            if (VALID)  // R#28: the window kernel's explicit selection
-                pos[u] = act[u] ? p.vpicks[((size_t)b * p.roots_cap + (size_t)(warp_root0 + ro)) * k + q] : 0u;
-            else if (STRATEGY == TGL_MOST_RECENT)
-                pos[u] = first[b * 32 + ro] + q;
-            else
-                pos[u] = act[u] ? first[b * 32 + ro] + picks[((size_t)b * k + q) * 32 + ro] : 0u;
+            const uint32_t heads = __reduce_or_sync(kFull, bit);
+            const uint32_t o = c0 + (uint32_t)lane;
+            act[u] = o < total;
+            const uint32_t h = hbase + __popc(heads & lemask) - 1u;
+            hbase += __popc(heads);
+            const uint2 sg = seg[act[u] ? h : 0u];
+            const uint32_t q = o - (sg.x >> 9);
+            info[u] = sg.x;
+            oo[u] = o;
+            if (VALID) {  // R#28: the window kernel's explicit selection
+                const uint32_t b = (sg.x >> 5) & 15u, r = sg.x & 31u;
+                pos[u] = act[u] ? p.vpicks[((size_t)b * p.roots_cap + (size_t)(warp_root0 + r)) * k + q] : 0u;
+            } else if (STRATEGY == TGL_MOST_RECENT) {
+                pos[u] = sg.y + q;
+            } else {
+                const uint32_t b = (sg.x >> 5) & 15u, r = sg.x & 31u;
+                pos[u] = act[u] ? sg.y + picks[((size_t)b * k + q) * 32 + r] : 0u;
+            }
         }
         int4 rec[kCopyUnroll];
 #pragma unroll
@@ -622,20 +641,25 @@ __global__ void __launch_bounds__(kTile, STRATEGY == TGL_MOST_RECENT ? TGL_COPY_
 #pragma unroll
         for (int u = 0; u < kCopyUnroll; ++u) {
             if (!act[u]) continue;
-            const int b = bb[u];
-            const BlockOut& o = p.out[b];
-            const uint64_t oi = base[b] + rem[u];
+            const uint32_t b = (info[u] >> 5) & 15u, r = info[u] & 31u;
+            const ulonglong2 pne = *reinterpret_cast<const ulonglong2*>(wptr + b * 4);
+            float* dtp = reinterpret_cast<float*>(wptr[b * 4 + 2]);
             const float tv = __int_as_float(rec[u].x);
-            const float tr = troot[rr[u]];
-            o.nbr[oi] = rec[u].y;
-            o.eid[oi] = rec[u].z;
-            o.dt[oi] = __fsub_rn(tr, tv);
-            if (o.ts_edge) o.ts_edge[oi] = tv;
-            if (o.child_key) o.child_key[oi] = rkey[rr[u]] * (uint64_t)k + qq[u];
-            if (o.child_t) o.child_t[oi] = tr;  // R#23: hop roots carry the root time
-            if (o.child_lo)  // children inherit the window's lower bound (R#3)
-                o.child_lo[oi] = p.layer == 0 ? __fsub_rn(tr, __fmul_rn((float)(b + 1), p.snapshot_len))
-                                              : p.root_lo[warp_root0 + rr[u]];
+            const float tr = troot[r];
+            reinterpret_cast<int32_t*>(pne.x)[oo[u]] = rec[u].y;
+            reinterpret_cast<int32_t*>(pne.y)[oo[u]] = rec[u].z;
+            dtp[oo[u]] = __fsub_rn(tr, tv);
+            if (EXTRA) {
+                const BlockOut& o = p.out[b];
+                const uint64_t oi = (uint64_t)((reinterpret_cast<int32_t*>(pne.x) + oo[u]) - o.nbr);
+                const uint32_t q = oo[u] - (info[u] >> 9);
+                if (o.ts_edge) o.ts_edge[oi] = tv;
+                if (o.child_key) o.child_key[oi] = rkey[r] * (uint64_t)k + q;
+                if (o.child_t) o.child_t[oi] = tr;  // R#23: hop roots carry the root time
+                if (o.child_lo)  // children inherit the window's lower bound (R#3)
+                    o.child_lo[oi] = p.layer == 0 ? __fsub_rn(tr, __fmul_rn((float)(b + 1), p.snapshot_len))
+                                                  : p.root_lo[warp_root0 + r];
+            }
         }
     }
 }
@@ -807,12 +831,26 @@ static int plan_sample(int64_t n_roots, int L, const int32_t* fanouts, int S, in
     return TGL_OK;
 }
 
+template <int STRATEGY, bool VALID, bool EXTRA>
+static void launch_copy(const SampleParams& sp, int64_t grid, size_t smem, cudaStream_t st) {
+    if (smem + 1024 > 48 * 1024)  // the dynamic part plus ~640 B of static shared memory
+        cudaFuncSetAttribute(copy_kernel<STRATEGY, VALID, EXTRA>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem);
+    copy_kernel<STRATEGY, VALID, EXTRA><<<(unsigned)grid, kTile, smem, st>>>(sp);
+}
+
+// EXTRA: the chain writes per-output data for a following layer or the dedup (ts_edge, child
+// key / time / lower bound); the last layer's copy carries none of it
 template <int STRATEGY, bool VALID>
 static int launch_pair(const SampleParams& sp, int64_t grid, size_t smem, cudaStream_t st) {
     window_kernel<STRATEGY, VALID><<<(unsigned)grid, kTile, 0, st>>>(sp);
-    if (smem > 48 * 1024)
-        cudaFuncSetAttribute(copy_kernel<STRATEGY, VALID>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    copy_kernel<STRATEGY, VALID><<<(unsigned)grid, kTile, smem, st>>>(sp);
+    bool extra = false;
+    for (int b = 0; b < sp.nsb; ++b)
+        extra |= sp.out[b].ts_edge || sp.out[b].child_key || sp.out[b].child_t || sp.out[b].child_lo;
+    if (extra)
+        launch_copy<STRATEGY, VALID, true>(sp, grid, smem, st);
+    else
+        launch_copy<STRATEGY, VALID, false>(sp, grid, smem, st);
     return cudaGetLastError() == cudaSuccess ? TGL_OK : TGL_ECUDA;
 }
 
@@ -886,7 +924,9 @@ static int sample_impl(const tgl_tcsr* g, const int32_t* roots, const float* roo
     if (need_zero &&
         cudaMemsetAsync(static_cast<char*>(workspace) + P.memset_from, 0, P.memset_bytes, st) != cudaSuccess)
         return TGL_ECUDA;
-    // experiment knobs (tools/sweep.py): TGL_NO_INDEX, TGL_NO_RECS
+    // experiment knobs (tools/sweep.py): TGL_NO_INDEX, TGL_NO_RECS, TGL_L2_FETCH (L2 fetch granularity)
+    static const char* l2f = getenv("TGL_L2_FETCH");
+    if (l2f) cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, (size_t)atoi(l2f));
     const bool use_recs = g->recs && !getenv("TGL_NO_RECS");
     const bool use_index = g->index && g->n_levels > 0 && !getenv("TGL_NO_INDEX");
     for (int j = 0; j < P.n_launch; ++j) {

@@ -150,7 +150,7 @@ def test_sharded_node_tables_gather_and_state_write(world, K):
         ids = q_ids[r]
         want = np.where((ids >= 0)[:, None], node_rows[np.clip(ids, 0, V - 1)], 0.0)
         np.testing.assert_array_equal(got[r][0], want)
-        np.testing.assert_array_equal(got[r][1], np.where((ids >= 0)[:, None], node_ts[np.clip(ids, 0, V - 1)], 0.0))
+        np.testing.assert_array_equal(got[r][1].reshape(len(ids), K), np.where((ids >= 0)[:, None], node_ts[np.clip(ids, 0, V - 1)], 0.0))
     # reference: one sequential state write of every rank's events in (rank, index) order
     ids = np.concatenate([e[0] for e in ev])
     ts = np.concatenate([e[1] for e in ev])

@@ -46,9 +46,13 @@ def test_variants_bit_exact(tgl, hop_time, replacement):
                       n_nodes=n_nodes, add_reverse=add_rev, with_index=case % 5 != 2)
         bo = oracle.sample(go, roots, rts, fanouts=fanouts, strategy=strategy, n_snapshots=S, snapshot_len=t_s,
                            seed=seed, root_key_base=base, hop_time=hop_time, replacement=replacement)
-        b = tgl.sample(g, cu(roots, torch.int32), cu(rts, torch.float32), fanouts=fanouts, strategy=strategy,
-                       n_snapshots=S, snapshot_len=t_s, seed=seed, root_key_base=base, hop_time=hop_time,
-                       replacement=replacement)
+        try:
+            b = tgl.sample(g, cu(roots, torch.int32), cu(rts, torch.float32), fanouts=fanouts, strategy=strategy,
+                           n_snapshots=S, snapshot_len=t_s, seed=seed, root_key_base=base, hop_time=hop_time,
+                           replacement=replacement)
+        except Exception as ex:
+            raise AssertionError(f"case {case}: L={L} fanouts={fanouts} strategy={strategy} S={S} t_s={t_s} "
+                                 f"roots={len(roots)}") from ex
         for j, (x, o) in enumerate(zip(b, bo)):
             off, nbr, e, dt, _ = x.trimmed()
             np.testing.assert_array_equal(off.cpu().numpy(), o["offsets"], err_msg=f"case {case} block {j}")
