@@ -430,6 +430,9 @@ __global__ void __launch_bounds__(kTile, TGL_WINDOW_MINB) window_kernel(const __
                                                         (tile >> kSuperShift)),
                   (unsigned long long)s);
     }
+    // programmatic dependent launch: the copy kernel may be scheduled once every window CTA got
+    // here (its griddepcontrol.wait still waits for this grid's completion and memory flush)
+    asm volatile("griddepcontrol.launch_dependents;");
 }
 
 // ---------------------------------------------------------------------------- K4b copy
@@ -482,6 +485,9 @@ __global__ void __launch_bounds__(kTile, STRATEGY == TGL_MOST_RECENT ? TGL_COPY_
         rk = p.root_key ? (valid ? p.root_key[i] : 0ull) : p.root_key_base + (uint64_t)i;
         rkey[lane] = rk;
     }
+    // everything below reads the window kernel's outputs: wait for that grid (a no-op when the
+    // copy kernel was launched without programmatic stream serialisation)
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     // counts, warp-local prefix, the segment list; uniform picks
     uint32_t cb = valid ? p.cuts[i] : 0u;  // c_b
     uint32_t flat = 0, nseg = 0;           // warp outputs / non-empty windows of the blocks before b
@@ -836,7 +842,24 @@ static void launch_copy(const SampleParams& sp, int64_t grid, size_t smem, cudaS
     if (smem + 1024 > 48 * 1024)  // the dynamic part plus ~640 B of static shared memory
         cudaFuncSetAttribute(copy_kernel<STRATEGY, VALID, EXTRA>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)smem);
-    copy_kernel<STRATEGY, VALID, EXTRA><<<(unsigned)grid, kTile, smem, st>>>(sp);
+    // programmatic dependent launch (PDL): the copy grid is launched while the window grid's last
+    // CTAs finish and waits in griddepcontrol.wait -- hides the launch gap between the two
+    static const bool no_pdl = getenv("TGL_NO_PDL") != nullptr;  // A/B knob
+    if (no_pdl) {
+        copy_kernel<STRATEGY, VALID, EXTRA><<<(unsigned)grid, kTile, smem, st>>>(sp);
+        return;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)grid);
+    cfg.blockDim = dim3(kTile);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, copy_kernel<STRATEGY, VALID, EXTRA>, sp);
 }
 
 // EXTRA: the chain writes per-output data for a following layer or the dedup (ts_edge, child
