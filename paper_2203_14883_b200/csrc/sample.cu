@@ -155,7 +155,8 @@ __device__ __forceinline__ uint32_t lower_bound_ts(const SampleParams& p, uint32
     return lo;
 }
 
-// Up to 4 cuts searched together, cut j in [a[j], b[j]] (a fence gap, or the whole list):
+// Up to 4 cuts searched together, cut j in [a[j], b[j]] (a fence gap, or the whole list); called
+// by all 32 lanes of the warp (lanes with nothing to search pass empty gaps):
 // interleaved binary searches, one independent probe per live cut per step, so a root costs
 // max(log2 gap) dependent steps instead of the sum over cuts.  Gaps longer than kIndexMin (hub
 // lists) descend the 16-ary index first.
@@ -164,27 +165,25 @@ __device__ __forceinline__ void lower_bound_multi(const SampleParams& p, uint32_
 #pragma unroll
     for (int j = 0; j < 4; ++j)
         if (p.n_levels > 0 && b[j] - a[j] > kIndexMin) b[j] = a[j] = lower_bound_ts(p, a[j], b[j], x[j]);
-    while (true) {
-        bool live = false;
+    // a gap of g slots needs ceil(log2(g + 1)) halvings: the warp runs its lanes' maximum as a
+    // counted loop (no per-step liveness vote), every cut stepping branch-free while a < b
+    uint32_t g = 0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) g = max(g, b[j] - a[j]);
+    const int steps = 32 - __clz((int)__reduce_max_sync(kFull, g));  // all 32 lanes call this
+    for (int it = 0; it < steps; ++it) {
         float v[4];
         uint32_t mid[4];
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
             mid[j] = a[j] + ((b[j] - a[j]) >> 1);
-            if (a[j] < b[j]) {
-                v[j] = __ldg(p.ts + mid[j]);
-                live = true;
-            }
+            v[j] = a[j] < b[j] ? __ldg(p.ts + mid[j]) : 0.0f;
         }
-        if (!live) break;
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
-            if (a[j] < b[j]) {
-                if (v[j] < x[j])
-                    a[j] = mid[j] + 1;
-                else
-                    b[j] = mid[j];
-            }
+            const bool go = a[j] < b[j], lt = v[j] < x[j];
+            a[j] = go && lt ? mid[j] + 1 : a[j];
+            b[j] = go && !lt ? mid[j] : b[j];
         }
     }
 }
@@ -373,12 +372,14 @@ __global__ void __launch_bounds__(kTile, TGL_WINDOW_MINB) window_kernel(const __
         }
     }
     if (multi) {
-        uint32_t cut[4] = {lo, lo, lo, lo};
-        if (early) {
-            lower_bound_multi(p, ga, gb, x);
+        uint32_t cut[4];
+        if (!early) {  // no slot before t: every cut is lo (empty gaps: no probes)
 #pragma unroll
-            for (int j = 0; j < 4; ++j) cut[j] = ga[j];
+            for (int j = 0; j < 4; ++j) ga[j] = gb[j] = lo;
         }
+        lower_bound_multi(p, ga, gb, x);  // the whole warp: its step count is a warp reduction
+#pragma unroll
+        for (int j = 0; j < 4; ++j) cut[j] = ga[j];
 #pragma unroll
         for (int b = 0; b < 3; ++b) {
             if (b >= nsb) break;

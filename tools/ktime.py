@@ -62,8 +62,14 @@ for env in json.loads(args.settings):
         if e.device_type == torch.autograd.DeviceType.CUDA:
             name = e.name.split("<")[0].split("(")[0].replace("void ", "").replace("tgl::", "")
             per[name] += e.device_time_total / args.reps
-    edges = sum(int(x.nnz_dev.item()) for x in smp.run(*chunks[-1], seed=cfg.sampler_seed,
-                                                       root_key_base=starts[-1]))
-    print(json.dumps({"env": env, "ms_per_call": round(ms, 4), "G_edges_per_s": round(edges / ms / 1e6, 2),
+    out_blocks = smp.run(*chunks[-1], seed=cfg.sampler_seed, root_key_base=starts[-1])
+    edges = sum(int(x.nnz_dev.item()) for x in out_blocks)
+    digest = 0  # output fingerprint: settings must agree bit for bit
+    for x in out_blocks:
+        off, nbr, eid, dt, _ = x.trimmed()
+        for a in (off.view(torch.int32), nbr, eid, dt.view(torch.int32)):
+            w = torch.arange(1, a.numel() + 1, device=a.device, dtype=torch.int64)
+            digest = (digest * 1000003 + int(((a.to(torch.int64) & 0xFFFFFFFF) * w).sum().item())) % (1 << 61)
+    print(json.dumps({"env": env, "digest": digest, "ms_per_call": round(ms, 4), "G_edges_per_s": round(edges / ms / 1e6, 2),
                       "kernels_us": {k: round(v, 1) for k, v in sorted(per.items(), key=lambda x: -x[1])}}),
           flush=True)
