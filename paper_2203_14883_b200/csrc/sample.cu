@@ -390,9 +390,7 @@ __global__ void __launch_bounds__(kTile, TGL_WINDOW_MINB) window_kernel(const __
                 if (b == 0) p.cuts[i] = cut[0];
                 p.cuts[(size_t)(b + 1) * p.roots_cap + i] = cut[b + 1];
             }
-            uint32_t s2 = take;
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) s2 += __shfl_xor_sync(kFull, s2, o);
+            const uint32_t s2 = __reduce_add_sync(kFull, take);
             if (lane == 0) s_red[b][warp] = s2;
         }
     } else {
@@ -414,9 +412,7 @@ __global__ void __launch_bounds__(kTile, TGL_WINDOW_MINB) window_kernel(const __
                 if (b == 0) p.cuts[i] = bcur;
                 p.cuts[(size_t)(b + 1) * p.roots_cap + i] = a;
             }
-            uint32_t s2 = take;
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) s2 += __shfl_xor_sync(kFull, s2, o);
+            const uint32_t s2 = __reduce_add_sync(kFull, take);
             if (lane == 0) s_red[b][warp] = s2;
             bcur = a;
         }

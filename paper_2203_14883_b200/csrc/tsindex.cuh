@@ -78,6 +78,9 @@ struct NodeRec {
 static_assert(sizeof(NodeRec) == 64, "node record is one 64-byte DRAM atom");
 
 __host__ __device__ inline uint32_t fence_pos(uint32_t lo, uint32_t d, int j) {
+    // j (d - 1) < 2^32 for d <= 2^28: one 32-bit multiply-high for the division by 13 (the window
+    // kernel runs this 8 times per root); longer lists take the 64-bit path -- same value
+    if (d <= (1u << 28)) return lo + ((uint32_t)j * (d - 1u)) / (uint32_t)(kFences - 1);
     return lo + (uint32_t)(((uint64_t)j * (uint64_t)(d - 1)) / (uint64_t)(kFences - 1));
 }
 
