@@ -15,8 +15,9 @@
 //                      most_recent -> the min(k, c) "closest to the end pointer";
 //                      uniform -> a uniform min(k, c)-subset (R#5).
 //   (K5) tile bases   the window kernel also adds its tile totals into per-64-tile super totals
-//                      (integer atomics: order-independent, so deterministic); a copy CTA sums
-//                      the super totals and tile totals before it -- no scan kernel, no waiting.
+//                      and per-4096-tile hyper totals (integer atomics: order-independent, so
+//                      deterministic); a copy CTA sums the hyper, super and tile totals before it
+//                      (<= 3 x 63 + hyper loads) -- no scan kernel, no waiting.
 //   K4b copy_kernel    one warp per 32 roots: warp scan of its counts + tile base -> offsets[i];
 //                      uniform: Floyd's k-subset with Philox4x32-10 draws, ascending (R#5, R#6);
 //                      then the tile's outputs are copied as one flat range per snapshot -- lane o
@@ -98,6 +99,8 @@ struct SampleParams {
     uint32_t* tile_tot;    // [nsb][tiles_cap] edges emitted per 256-root tile
     uint64_t* super_tot;   // [nsb][supers_cap] per 64 tiles (integer atomics: order-independent), zeroed per call
     int64_t supers_cap;
+    uint64_t* hyper_tot;   // [nsb][hypers_cap] per 64 super tiles (4,096 tiles), same rules
+    int64_t hypers_cap;
     int64_t roots_cap, tiles_cap;
     uint32_t* picks_global;  // null -> picks in shared memory; else [tiles_cap * 8 warps][nsb*k][32]
     int* err;
@@ -426,6 +429,9 @@ __global__ void __launch_bounds__(kTile, TGL_WINDOW_MINB) window_kernel(const __
         atomicAdd(reinterpret_cast<unsigned long long*>(p.super_tot + (size_t)threadIdx.x * p.supers_cap +
                                                         (tile >> kSuperShift)),
                   (unsigned long long)s);
+        atomicAdd(reinterpret_cast<unsigned long long*>(p.hyper_tot + (size_t)threadIdx.x * p.hypers_cap +
+                                                        (tile >> (2 * kSuperShift))),
+                  (unsigned long long)s);
     }
     // programmatic dependent launch: the copy kernel may be scheduled once every window CTA got
     // here (its griddepcontrol.wait still waits for this grid's completion and memory flush)
@@ -550,12 +556,14 @@ __global__ void __launch_bounds__(kTile, STRATEGY == TGL_MOST_RECENT ? TGL_COPY_
             }
         }
     }
-    // tile base per snapshot: warp b sums the super totals before this tile's super tile and the
-    // tile totals before this tile inside it (all final: the window kernel has completed)
+    // tile base per snapshot: warp b sums the hyper totals before this tile's hyper tile, the super
+    // totals before its super tile inside it and the tile totals before it inside its super tile
+    // (all final: the window kernel has completed)
     for (int b = warp; b < nsb; b += kWarps) {
-        const int64_t t = tile, sup = t >> kSuperShift;
+        const int64_t t = tile, sup = t >> kSuperShift, hyp = t >> (2 * kSuperShift);
         uint64_t acc = 0;
-        for (int64_t q = lane; q < sup; q += 32) acc += p.super_tot[(size_t)b * p.supers_cap + q];
+        for (int64_t q = lane; q < hyp; q += 32) acc += p.hyper_tot[(size_t)b * p.hypers_cap + q];
+        for (int64_t q = (hyp << kSuperShift) + lane; q < sup; q += 32) acc += p.super_tot[(size_t)b * p.supers_cap + q];
         for (int64_t q = (sup << kSuperShift) + lane; q < t; q += 32) acc += p.tile_tot[(size_t)b * p.tiles_cap + q];
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(kFull, acc, o);
@@ -739,6 +747,8 @@ struct Launch {
     uint32_t *cuts, *tile_tot;
     uint64_t* super_tot;
     int64_t supers_cap;
+    uint64_t* hyper_tot;
+    int64_t hypers_cap;
     uint32_t* picks;  // global picks or null
     uint32_t *vpicks, *vtake;  // R#28 explicit selection (edge validity) or null
 };
@@ -791,6 +801,7 @@ static int plan_sample(int64_t n_roots, int L, const int32_t* fanouts, int S, in
         la.cuts = c.take<uint32_t>((size_t)(nsb + 1) * la.roots_cap);
         la.tile_tot = c.take<uint32_t>((size_t)nsb * la.tiles_cap);
         la.supers_cap = (la.tiles_cap + (1 << kSuperShift) - 1) >> kSuperShift;
+        la.hypers_cap = (la.supers_cap + (1 << kSuperShift) - 1) >> kSuperShift;
         la.picks = nullptr;
         if (strategy == TGL_UNIFORM && !picks_fit_smem(nsb, fanouts[layer]))
             la.picks = c.take<uint32_t>((size_t)la.tiles_cap * kTile * nsb * fanouts[layer]);
@@ -804,6 +815,8 @@ static int plan_sample(int64_t n_roots, int L, const int32_t* fanouts, int S, in
     P.memset_from = c.bytes();
     for (int j = 0; j < P.n_launch; ++j)
         P.launches[j].super_tot = c.take<uint64_t>((size_t)P.launches[j].nsb * P.launches[j].supers_cap);
+    for (int j = 0; j < P.n_launch; ++j)
+        P.launches[j].hyper_tot = c.take<uint64_t>((size_t)P.launches[j].nsb * P.launches[j].hypers_cap);
     P.memset_bytes = c.bytes() - P.memset_from;
     const bool need_lo = L > 1 && std::isfinite(snapshot_len);
     if (dedup && need_lo) return TGL_EINVAL;  // R#27: windows with inherited finite bounds would merge
@@ -1003,6 +1016,8 @@ static int sample_impl(const tgl_tcsr* g, const int32_t* roots, const float* roo
         sp.tile_tot = la.tile_tot;
         sp.super_tot = la.super_tot;
         sp.supers_cap = la.supers_cap;
+        sp.hyper_tot = la.hyper_tot;
+        sp.hypers_cap = la.hypers_cap;
         sp.roots_cap = la.roots_cap;
         sp.tiles_cap = la.tiles_cap;
         sp.picks_global = la.picks;
