@@ -39,6 +39,14 @@ UNIT = "edges/s"
 
 
 # ----------------------------------------------------------------------------- helpers
+def workload_name(key: str, cfg: C.Workload) -> str:
+    """config.workload of every bench line (ours, node-sharded and the reference arm): one name per config."""
+    return (f"{key} {cfg.name}: {cfg.n_nodes:,} nodes, {cfg.n_edges:,} edges"
+            f"{' (+reverse)' if cfg.add_reverse else ''}, {len(cfg.fanouts)}-layer "
+            f"{cfg.strategy} k={cfg.fanouts}, {cfg.n_snapshots} snapshot(s)"
+            f"{'' if not math.isfinite(cfg.snapshot_len) else f' of {cfg.snapshot_len:g}'}")
+
+
 def algorithmic_bytes(cfg: C.Workload, n_roots_per_layer, nnz_per_layer) -> int:
     """Bytes the method must move, element granularity.
 
@@ -325,7 +333,7 @@ def run_node_sharded(args):
     out = {"metric": METRIC, "value": float(tot[0]) / (float(mx[0]) / 1e3), "unit": UNIT, "n_gpus": world,
            "steps": args.steps, "warmup": args.warmup, "ms_per_step": float(mx[0]) / args.steps,
            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-           "config": {"workload": f"{key} {cfg.name}", "batch_roots": B, "batches_per_step": args.batches,
+           "config": {"workload": workload_name(key, cfg), "batch_roots": B, "batches_per_step": args.batches,
                       "roots_per_step_per_gpu": chunk,
                       "parallelism": f"node-sharded T-CSR over {world} rank(s), edge-balanced node ranges; "
                                      "requests/replies by all-to-all-v (NCCL)",
@@ -503,10 +511,7 @@ def run_ours(args):
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": total_ms_max / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": f"{key} {cfg.name}: {cfg.n_nodes:,} nodes, {cfg.n_edges:,} edges"
-                               f"{' (+reverse)' if cfg.add_reverse else ''}, {len(cfg.fanouts)}-layer "
-                               f"{cfg.strategy} k={cfg.fanouts}, {cfg.n_snapshots} snapshot(s)"
-                               f"{'' if not math.isfinite(cfg.snapshot_len) else f' of {cfg.snapshot_len:g}'}",
+        "config": {"workload": workload_name(key, cfg),
                    "batch_roots": B, "batches_per_step": M, "roots_per_step_per_gpu": chunk,
                    "parallelism": f"root-sharded dp{world}, replicated T-CSR",
                    "l2": ("no flush: T-CSR and per-step roots exceed L2 (126 MB); "
@@ -805,7 +810,7 @@ def run_reference(args):
     out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
            "warmup": args.warmup, "ms_per_step": secs * 1e3 / args.steps, "higher_is_better": True,
            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic", "impl": "reference",
-           "config": {"workload": f"{key} {cfg.name}", "batch_roots": B, "batches_per_step": per_step},
+           "config": {"workload": workload_name(key, cfg), "batch_roots": B, "batches_per_step": per_step},
            "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
                             "sample": f"{args.steps} steps x {per_step} batches x {B} roots, spread over the epoch"},
            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
