@@ -34,8 +34,8 @@
  * (P:L252), the add_reverse tie example, brute force over the whole logical stream
  * (oracle/brute.py, numpy) on random tiny graphs, numpy stable argsort for the build,
  * invariants (no leak, counts, sortedness, partition of snapshot windows) and the
- * uniform-subset distribution.  Parity pinned for every function except the l>=1 with
- * S>1 window reading (R#3), which is "parity unpinned".
+ * uniform-subset distribution.  Parity pinned for every function; the l>=1 with S>1
+ * window reading (R#3) by the hand example tests/golden/r3_hops.json and the brute force.
  */
 #include <stdint.h>
 #include <stddef.h>

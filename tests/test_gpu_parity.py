@@ -249,3 +249,27 @@ def test_shard_bucket_stable(tgl):
     want = np.argsort(owner, kind="stable")
     np.testing.assert_array_equal(perm.cpu().numpy(), want)
     np.testing.assert_array_equal(counts.cpu().numpy(), np.bincount(owner, minlength=world))
+
+
+# ----------------------------------------------------------------------------- golden fixtures
+@pytest.mark.parametrize("name", ["fig3.json", "ties.json", "r3_hops.json"])
+def test_golden_examples_on_gpu(tgl, golden_dir, name):
+    """The paper's worked examples (Fig. 3), the tie rule (R#8) and the R#3 hop-window
+    example, through the C ABI: expected values are the fixtures' hand-worked ones, not the oracle's."""
+    import json
+    import os
+    gd = json.load(open(os.path.join(golden_dir, name)))
+    e = gd["edges"]
+    g = gpu_build(tgl, e["src"], e["dst"], np.float32(e["ts"]), None, gd["n_nodes"], bool(gd["add_reverse"]))
+    for case in gd["cases"]:
+        t_s = math.inf if case["snapshot_len"] == "inf" else float(case["snapshot_len"])
+        blocks = tgl.sample(g, cu([case["root"]], torch.int32), cu([case["t"]], torch.float32),
+                            fanouts=case["fanouts"], strategy=case["strategy"], n_snapshots=case["n_snapshots"],
+                            snapshot_len=t_s, seed=0, root_key_base=0)
+        assert len(blocks) == len(case["blocks"]), case["what"]
+        for b, want in zip(blocks, case["blocks"]):
+            off, nbr, eid, dt, _ = b.trimmed()
+            assert nbr.cpu().tolist() == want["nbr"], case["what"]
+            assert eid.cpu().tolist() == want["eid"], case["what"]
+            assert [float(x) for x in dt.cpu().tolist()] == want["dt"], case["what"]
+            assert off.cpu().tolist() == [0, len(want["nbr"])], case["what"]

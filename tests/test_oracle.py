@@ -50,7 +50,7 @@ def _run_case(g, case, n_nodes):
                          snapshot_len=ts_len, seed=0, root_key_base=0)
 
 
-@pytest.mark.parametrize("name", ["fig3.json", "ties.json"])
+@pytest.mark.parametrize("name", ["fig3.json", "ties.json", "r3_hops.json"])
 def test_golden_examples(golden_dir, name):
     gd = json.load(open(os.path.join(golden_dir, name)))
     e = gd["edges"]
