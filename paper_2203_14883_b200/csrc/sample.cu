@@ -893,6 +893,33 @@ static int launch_chain(const SampleParams& sp, int64_t grid, size_t smem, cudaS
     return sp.valid ? launch_pair<STRATEGY, true>(sp, grid, smem, st) : launch_pair<STRATEGY, false>(sp, grid, smem, st);
 }
 
+// Layer l >= 1 chains of different snapshots are independent (chain (l, s) reads only block
+// (l-1, s), Alg. 1 L227 / R#3, and each chain has its own workspace slice): with S > 1 they run
+// on S forked streams joined back by events, so one snapshot's tail overlaps the next one's
+// kernels.  Library-owned, created once per (thread, device); not used while the caller's
+// stream is being captured into a CUDA graph (the sequential order is captured instead).
+struct ForkStreams {
+    int dev = -1;
+    cudaStream_t side[TGL_MAX_SNAPSHOTS] = {};
+    cudaEvent_t fork = nullptr, join[TGL_MAX_SNAPSHOTS] = {};
+};
+
+static ForkStreams* fork_streams(int S) {
+    static thread_local ForkStreams F[16];
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 16) return nullptr;
+    ForkStreams& f = F[dev];
+    if (f.dev != dev) {
+        if (cudaEventCreateWithFlags(&f.fork, cudaEventDisableTiming) != cudaSuccess) return nullptr;
+        f.dev = dev;
+    }
+    for (int s = 0; s < S; ++s)
+        if (!f.side[s] && (cudaStreamCreateWithFlags(&f.side[s], cudaStreamNonBlocking) != cudaSuccess ||
+                           cudaEventCreateWithFlags(&f.join[s], cudaEventDisableTiming) != cudaSuccess))
+            return nullptr;
+    return &f;
+}
+
 }  // namespace tgl
 
 using namespace tgl;
@@ -962,9 +989,22 @@ static int sample_impl(const tgl_tcsr* g, const int32_t* roots, const float* roo
     if (l2f) cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, (size_t)atoi(l2f));
     const bool use_recs = g->recs && !getenv("TGL_NO_RECS");
     const bool use_index = g->index && g->n_levels > 0 && !getenv("TGL_NO_INDEX");
+    static const bool no_fork = getenv("TGL_NO_FORK") != nullptr;  // A/B knob
+    ForkStreams* fk = nullptr;
+    if (S > 1 && L > 1 && !dedup && !no_fork) {  // dedup shares one scratch across chains: sequential
+        cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+        if (cudaStreamIsCapturing(st, &cs) == cudaSuccess && cs == cudaStreamCaptureStatusNone)
+            fk = fork_streams(S);
+    }
     for (int j = 0; j < P.n_launch; ++j) {
         const Launch& la = P.launches[j];
         const int l = la.layer, s = la.chain;
+        if (fk && j == 1) {  // after layer 0: fork the snapshot chains
+            if (cudaEventRecord(fk->fork, st) != cudaSuccess) return TGL_ECUDA;
+            for (int q = 0; q < S; ++q)
+                if (cudaStreamWaitEvent(fk->side[q], fk->fork, 0) != cudaSuccess) return TGL_ECUDA;
+        }
+        cudaStream_t cst = fk && l > 0 ? fk->side[s] : st;
         SampleParams sp;
         memset(&sp, 0, sizeof(sp));
         sp.indptr = g->indptr;
@@ -1040,8 +1080,8 @@ static int sample_impl(const tgl_tcsr* g, const int32_t* roots, const float* roo
         const int64_t tiles = l == 0 ? std::max<int64_t>(1, (n_roots + kTile - 1) / kTile) : la.tiles_cap;
         const size_t smem =
             (size_t)kWarps * copy_warp_words(la.nsb, sp.k, strategy == TGL_UNIFORM && la.picks == nullptr) * 4;
-        rc = strategy == TGL_UNIFORM ? launch_chain<TGL_UNIFORM>(sp, tiles, smem, st)
-                                     : launch_chain<TGL_MOST_RECENT>(sp, tiles, smem, st);
+        rc = strategy == TGL_UNIFORM ? launch_chain<TGL_UNIFORM>(sp, tiles, smem, cst)
+                                     : launch_chain<TGL_MOST_RECENT>(sp, tiles, smem, cst);
         if (rc) return rc;
         if (dedup) {
             for (int b = 0; b < la.nsb; ++b) {
@@ -1066,6 +1106,10 @@ static int sample_impl(const tgl_tcsr* g, const int32_t* roots, const float* roo
             }
         }
     }
+    if (fk)  // join: the caller's stream waits for every snapshot chain
+        for (int q = 0; q < S; ++q)
+            if (cudaEventRecord(fk->join[q], fk->side[q]) != cudaSuccess || cudaStreamWaitEvent(st, fk->join[q], 0) != cudaSuccess)
+                return TGL_ECUDA;
     return TGL_OK;
 }
 
