@@ -538,8 +538,9 @@ def run_ours(args):
                                        "row) + 8 B per event" if gather is not None else ""),
                      "algorithmic_bytes_per_step": bytes_total / args.steps,
                      "l2_resident": tcsr_bytes < l2_bytes,
-                     "note": ("T-CSR + gather node tables fit the 126 MB L2: algorithmic bytes are mostly L2 "
-                              "traffic, so frac vs the HBM peak is not meaningful here (SURVEY 8(d))")
+                     "note": ("T-CSR + gather node tables fit the 126 MB L2 (flushed between steps, but the "
+                              "re-reads inside a step hit L2): algorithmic bytes are mostly L2 traffic, so frac "
+                              "vs the HBM peak is not meaningful here (SURVEY 8(d))")
                              if tcsr_bytes < l2_bytes else "T-CSR exceeds L2: HBM-bound random access"},
         "gpu_launches": launches_per_step * args.steps,
         "clocks": clocks.summary(),
