@@ -273,3 +273,36 @@ def test_golden_examples_on_gpu(tgl, golden_dir, name):
             assert eid.cpu().tolist() == want["eid"], case["what"]
             assert [float(x) for x in dt.cpu().tolist()] == want["dt"], case["what"]
             assert off.cpu().tolist() == [0, len(want["nbr"])], case["what"]
+
+
+@pytest.mark.parametrize("strategy", ["most_recent", "uniform"])
+def test_forked_snapshot_chains_equal_captured_sequential(tgl, strategy):
+    """S > 1, L > 1: eager calls fork the layer >= 1 snapshot chains onto side streams; under CUDA-graph
+    capture they run in order on the caller's stream.  Both orders give the oracle's blocks, bit for bit,
+    on a non-default caller stream."""
+    src, dst, ts, _ = random_graph(31, 200, 40_000, integer_times=True, t_max=4000)
+    roots, rts = random_roots(31, 200, 3000, integer_times=True, t_max=4000)
+    g = gpu_build(tgl, src, dst, ts, None, 200, True)
+    go = oracle.build(src, dst, ts, None, n_nodes=200, add_reverse=True)
+    bo = oracle.sample(go, roots, rts, fanouts=[6, 4], strategy=0 if strategy == "most_recent" else 1, n_snapshots=3,
+                       snapshot_len=300.0, seed=9, root_key_base=0)
+    R, T = cu(roots, torch.int32), cu(rts, torch.float32)
+    smp = tgl.Sampler(g, 3000, [6, 4], strategy, 3, 300.0)
+    side = torch.cuda.Stream()
+    side.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(side):
+        eager = [[x.clone() for x in b.trimmed()[:4]] for b in smp.run(R, T, seed=9, root_key_base=0)]
+        torch.cuda.synchronize()
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph, stream=side):
+            blocks = smp.run(R, T, seed=9, root_key_base=0)
+    for b in blocks:  # poison the outputs, then replay the captured (sequential) calls
+        b.nbr.fill_(-7)
+    graph.replay()
+    torch.cuda.synchronize()
+    for j, (e, b, o) in enumerate(zip(eager, blocks, bo)):
+        c = b.trimmed()[:4]
+        for u, w in zip(e, c):
+            assert torch.equal(u, w), f"block {j}"
+        np.testing.assert_array_equal(e[1].cpu().numpy(), o["nbr"], err_msg=f"block {j}")
+        np.testing.assert_array_equal(e[3].cpu().numpy().view(np.uint32), o["dt"].view(np.uint32))
