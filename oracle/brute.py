@@ -48,21 +48,22 @@ def logical_stream(src, dst, ts, eid, add_reverse: bool):
 
 
 def floyd(c: int, k: int, seed: int, layer: int, snapshot: int, rk: int) -> List[int]:
-    """Floyd's uniform k-subset of range(c), draw j from Philox word 0 (R#5, R#6)."""
+    """Floyd's uniform k-subset of range(c); draw j = word j % 4 of the Philox block at counter
+    j // 4 (R#5, R#6)."""
     picks: List[int] = []
     key = (seed & MASK, (seed >> 32) & MASK)
     for j in range(k):
         m = c - k + j
-        x = philox((j, (layer << 16) | snapshot, rk & MASK, (rk >> 32) & MASK), key)[0]
+        x = philox((j // 4, (layer << 16) | snapshot, rk & MASK, (rk >> 32) & MASK), key)[j % 4]
         r = (x * (m + 1)) >> 32
         picks.append(m if r in picks else r)
     return sorted(picks)
 
 
 def with_replacement(c: int, k: int, seed: int, layer: int, snapshot: int, rk: int) -> List[int]:
-    """k independent uniform draws from range(c), draw j from Philox word 0 (R#24), sorted."""
+    """k independent uniform draws from range(c), draw j as in Floyd (R#24, R#6), sorted."""
     key = (seed & MASK, (seed >> 32) & MASK)
-    return sorted((philox((j, (layer << 16) | snapshot, rk & MASK, (rk >> 32) & MASK), key)[0] * c) >> 32
+    return sorted((philox((j // 4, (layer << 16) | snapshot, rk & MASK, (rk >> 32) & MASK), key)[j % 4] * c) >> 32
                   for j in range(k))
 
 

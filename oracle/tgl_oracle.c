@@ -263,13 +263,13 @@ int64_t oracle_sample_block(const int64_t *indptr, const int32_t *nbr, const flo
         /* positions of the selected slots, ascending */
         if (strategy == 1 && replacement) {
             /* uniform WITH replacement (R#24): k independent draws r_j uniform in [0, c), draw j
-             * from Philox word 0 with the counter of Floyd's draw j (R#6); ascending (R#13). */
+             * = Floyd's draw j (R#6: word j mod 4 of the block at counter j / 4); ascending (R#13). */
             for (int32_t j = 0; j < (int32_t)n_sel; ++j) {
-                uint32_t ctr[4] = { (uint32_t)j, ((uint32_t)layer << 16) | (uint32_t)snapshot,
+                uint32_t ctr[4] = { (uint32_t)j / 4u, ((uint32_t)layer << 16) | (uint32_t)snapshot,
                                     (uint32_t)(rk & 0xFFFFFFFFu), (uint32_t)(rk >> 32) };
                 uint32_t x[4];
                 oracle_philox4x32_10(ctr, key, x);
-                pick_scratch[j] = (uint32_t)(((uint64_t)x[0] * (uint64_t)c) >> 32);
+                pick_scratch[j] = (uint32_t)(((uint64_t)x[j % 4] * (uint64_t)c) >> 32);
             }
             for (int32_t j = 1; j < (int32_t)n_sel; ++j) {
                 uint32_t x = pick_scratch[j];
@@ -284,14 +284,15 @@ int64_t oracle_sample_block(const int64_t *indptr, const int32_t *nbr, const flo
             for (int64_t j = 0; j < n_sel; ++j) pick_scratch[j] = (uint32_t)(first + j);
         } else {
             /* Floyd's algorithm: for m = c-k .. c-1 draw r uniform in [0, m]; take r
-             * if not yet taken, else take m.  Draw j uses Philox word 0. */
+             * if not yet taken, else take m.  Draw j uses word j mod 4 of the Philox block at
+             * counter j / 4 (R#6). */
             for (int32_t j = 0; j < k; ++j) {
                 uint32_t m = (uint32_t)(c - k + j);
-                uint32_t ctr[4] = { (uint32_t)j, ((uint32_t)layer << 16) | (uint32_t)snapshot,
+                uint32_t ctr[4] = { (uint32_t)j / 4u, ((uint32_t)layer << 16) | (uint32_t)snapshot,
                                     (uint32_t)(rk & 0xFFFFFFFFu), (uint32_t)(rk >> 32) };
                 uint32_t x[4];
                 oracle_philox4x32_10(ctr, key, x);
-                uint32_t r = (uint32_t)(((uint64_t)x[0] * ((uint64_t)m + 1)) >> 32);
+                uint32_t r = (uint32_t)(((uint64_t)x[j % 4] * ((uint64_t)m + 1)) >> 32);
                 int taken = 0;
                 for (int32_t q = 0; q < j; ++q) if (pick_scratch[q] == r) { taken = 1; break; }
                 pick_scratch[j] = taken ? m : r;

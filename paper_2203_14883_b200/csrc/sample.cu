@@ -206,6 +206,12 @@ __device__ __forceinline__ uint32_t warp_incl_scan(uint32_t x, int lane) {
 // explicitly: most_recent walks back from the end pointer collecting the last k valid slots;
 // uniform counts the valid slots, draws ranks (Floyd / with replacement, the same Philox counters)
 // and maps them to slots in one forward walk.  The copy kernel reads the selected slots.
+// uniform draws (R#6): draw j is word j mod 4 of Philox4x32-10 at counter (j / 4, l << 16 | s, rk)
+__device__ __forceinline__ uint32_t draw_word(const uint4& r, uint32_t j) {
+    const uint32_t q = j & 3u;
+    return q == 0 ? r.x : q == 1 ? r.y : q == 2 ? r.z : r.w;
+}
+
 template <int STRATEGY>
 __device__ __forceinline__ uint32_t select_valid(const SampleParams& p, int64_t i, int b, uint32_t a, uint32_t e,
                                                 uint64_t rk) {
@@ -224,11 +230,14 @@ __device__ __forceinline__ uint32_t select_valid(const SampleParams& p, int64_t 
         uint32_t cv = 0;
         for (uint32_t s = a; s < e; ++s) cv += ok(s);
         const uint32_t ctr1 = ((uint32_t)p.layer << 16) | (uint32_t)(p.layer == 0 ? b : p.snap0);
+        uint4 rnd = make_uint4(0u, 0u, 0u, 0u);
         if (p.replacement) {
             take = cv ? k : 0u;
-            for (uint32_t j = 0; j < take; ++j)
-                pk[j] = __umulhi(philox4x32_10(make_uint4(j, ctr1, (uint32_t)rk, (uint32_t)(rk >> 32)), p.seed_lo,
-                                               p.seed_hi).x, cv);
+            for (uint32_t j = 0; j < take; ++j) {
+                if ((j & 3u) == 0)
+                    rnd = philox4x32_10(make_uint4(j >> 2, ctr1, (uint32_t)rk, (uint32_t)(rk >> 32)), p.seed_lo, p.seed_hi);
+                pk[j] = __umulhi(draw_word(rnd, j), cv);
+            }
         } else if (cv <= k) {
             take = cv;
             for (uint32_t q = 0; q < cv; ++q) pk[q] = q;
@@ -236,9 +245,9 @@ __device__ __forceinline__ uint32_t select_valid(const SampleParams& p, int64_t 
             take = k;
             for (uint32_t j = 0; j < k; ++j) {  // Floyd over the ranks (R#5, R#6)
                 const uint32_t m = cv - k + j;
-                const uint32_t r = __umulhi(
-                    philox4x32_10(make_uint4(j, ctr1, (uint32_t)rk, (uint32_t)(rk >> 32)), p.seed_lo, p.seed_hi).x,
-                    m + 1u);
+                if ((j & 3u) == 0)
+                    rnd = philox4x32_10(make_uint4(j >> 2, ctr1, (uint32_t)rk, (uint32_t)(rk >> 32)), p.seed_lo, p.seed_hi);
+                const uint32_t r = __umulhi(draw_word(rnd, j), m + 1u);
                 bool taken = false;
                 for (uint32_t q = 0; q < j; ++q) taken |= pk[q] == r;
                 pk[j] = taken ? m : r;
@@ -515,14 +524,16 @@ __global__ void __launch_bounds__(kTile, STRATEGY == TGL_MOST_RECENT ? TGL_COPY_
         if (STRATEGY == TGL_UNIFORM && !VALID) {
             uint32_t* pk = picks + (size_t)b * k * 32 + lane;  // pick q at pk[q * 32]
             const uint32_t ctr1 = ((uint32_t)p.layer << 16) | (uint32_t)(p.layer == 0 ? b : p.snap0);
+            uint4 rnd = make_uint4(0u, 0u, 0u, 0u);
             if (!p.replacement && len <= (uint32_t)k) {
                 for (uint32_t q = 0; q < len; ++q) pk[q * 32] = q;
             } else if (p.replacement) {
                 // with replacement (R#24): r_j uniform in [0, c) from the counter of Floyd's draw j
                 for (uint32_t j = 0; j < take; ++j) {
-                    const uint4 rnd = philox4x32_10(make_uint4(j, ctr1, (uint32_t)rk, (uint32_t)(rk >> 32)),
-                                                    p.seed_lo, p.seed_hi);
-                    pk[j * 32] = __umulhi(rnd.x, len);
+                    if ((j & 3u) == 0)
+                        rnd = philox4x32_10(make_uint4(j >> 2, ctr1, (uint32_t)rk, (uint32_t)(rk >> 32)), p.seed_lo,
+                                            p.seed_hi);
+                    pk[j * 32] = __umulhi(draw_word(rnd, j), len);
                 }
                 for (int j = 1; j < (int)take; ++j) {  // ascending slot order (R#13)
                     const uint32_t xj = pk[j * 32];
@@ -537,9 +548,10 @@ __global__ void __launch_bounds__(kTile, STRATEGY == TGL_MOST_RECENT ? TGL_COPY_
                 // Floyd: for m = c-k .. c-1, r uniform in [0, m]; take r unless taken, else m
                 for (int j = 0; j < k; ++j) {
                     const uint32_t m = len - (uint32_t)k + (uint32_t)j;
-                    const uint4 rnd = philox4x32_10(make_uint4((uint32_t)j, ctr1, (uint32_t)rk, (uint32_t)(rk >> 32)),
-                                                    p.seed_lo, p.seed_hi);
-                    const uint32_t rr = __umulhi(rnd.x, m + 1u);
+                    if ((j & 3) == 0)
+                        rnd = philox4x32_10(make_uint4((uint32_t)j >> 2, ctr1, (uint32_t)rk, (uint32_t)(rk >> 32)),
+                                            p.seed_lo, p.seed_hi);
+                    const uint32_t rr = __umulhi(draw_word(rnd, (uint32_t)j), m + 1u);
                     bool taken = false;
                     for (int q = 0; q < j; ++q) taken |= (pk[q * 32] == rr);
                     pk[j * 32] = taken ? m : rr;
