@@ -552,18 +552,22 @@ __global__ void __launch_bounds__(kTile, STRATEGY == TGL_MOST_RECENT ? TGL_COPY_
                         rnd = philox4x32_10(make_uint4((uint32_t)j >> 2, ctr1, (uint32_t)rk, (uint32_t)(rk >> 32)),
                                             p.seed_lo, p.seed_hi);
                     const uint32_t rr = __umulhi(draw_word(rnd, (uint32_t)j), m + 1u);
-                    bool taken = false;
-                    for (int q = 0; q < j; ++q) taken |= (pk[q * 32] == rr);
-                    pk[j * 32] = taken ? m : rr;
-                }
-                for (int j = 1; j < k; ++j) {  // ascending slot order (R#13)
-                    const uint32_t xj = pk[j * 32];
+                    // the picks so far are kept ascending (R#13): one downward pass shifts those
+                    // > rr up a slot; if rr is already taken, Floyd takes m instead, which exceeds
+                    // every earlier pick (<= m - 1): shift back and append it.  The set -- hence
+                    // the output -- is Floyd's; only the sort is merged into the draws.
                     int q = j - 1;
-                    while (q >= 0 && pk[q * 32] > xj) {
-                        pk[(q + 1) * 32] = pk[q * 32];
+                    uint32_t v = 0;
+                    while (q >= 0 && (v = pk[q * 32]) > rr) {
+                        pk[(q + 1) * 32] = v;
                         --q;
                     }
-                    pk[(q + 1) * 32] = xj;
+                    if (q >= 0 && v == rr) {
+                        for (int u = q + 1; u < j; ++u) pk[u * 32] = pk[(u + 1) * 32];
+                        pk[j * 32] = m;
+                    } else {
+                        pk[(q + 1) * 32] = rr;
+                    }
                 }
             }
         }
