@@ -456,7 +456,9 @@ __host__ __device__ inline int copy_warp_words(int nsb, int k, bool picks_in_sme
     return nsb * 32 + 2 * nsb * 32 + 32 + 2 * 32 + 8 * nsb + (picks_in_smem ? nsb * k * 32 : 0);
 }
 
-template <int STRATEGY, bool VALID, bool EXTRA>
+// PSMEM: uniform picks in shared memory (known at compile time, so LDS/STS instead of generic
+// 64-bit accesses); else in the global workspace
+template <int STRATEGY, bool VALID, bool EXTRA, bool PSMEM>
 __global__ void __launch_bounds__(kTile, STRATEGY == TGL_MOST_RECENT ? TGL_COPY_MINB_MR : TGL_COPY_MINB) copy_kernel(const __grid_constant__ SampleParams p) {
     extern __shared__ __align__(16) uint32_t smem[];
     __shared__ uint32_t s_wsum[TGL_MAX_SNAPSHOTS][kWarps];
@@ -478,7 +480,7 @@ __global__ void __launch_bounds__(kTile, STRATEGY == TGL_MOST_RECENT ? TGL_COPY_
     const bool valid = i < n;
     const int nsb = p.nsb;
     const int k = p.k;
-    const bool picks_smem = STRATEGY == TGL_UNIFORM && p.picks_global == nullptr;
+    constexpr bool picks_smem = STRATEGY == TGL_UNIFORM && PSMEM;
     uint32_t* ws = smem + warp * copy_warp_words(nsb, k, picks_smem);
     uint32_t* inc = ws;                                                   // [nsb][32]
     uint2* seg = reinterpret_cast<uint2*>(inc + nsb * 32);                // [nsb * 32]
@@ -863,16 +865,16 @@ static int plan_sample(int64_t n_roots, int L, const int32_t* fanouts, int S, in
     return TGL_OK;
 }
 
-template <int STRATEGY, bool VALID, bool EXTRA>
-static void launch_copy(const SampleParams& sp, int64_t grid, size_t smem, cudaStream_t st) {
+template <int STRATEGY, bool VALID, bool EXTRA, bool PSMEM>
+static void launch_copy_ps(const SampleParams& sp, int64_t grid, size_t smem, cudaStream_t st) {
     if (smem + 1024 > 48 * 1024)  // the dynamic part plus ~640 B of static shared memory
-        cudaFuncSetAttribute(copy_kernel<STRATEGY, VALID, EXTRA>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaFuncSetAttribute(copy_kernel<STRATEGY, VALID, EXTRA, PSMEM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)smem);
     // programmatic dependent launch (PDL): the copy grid is launched while the window grid's last
     // CTAs finish and waits in griddepcontrol.wait -- hides the launch gap between the two
     static const bool no_pdl = getenv("TGL_NO_PDL") != nullptr;  // A/B knob
     if (no_pdl) {
-        copy_kernel<STRATEGY, VALID, EXTRA><<<(unsigned)grid, kTile, smem, st>>>(sp);
+        copy_kernel<STRATEGY, VALID, EXTRA, PSMEM><<<(unsigned)grid, kTile, smem, st>>>(sp);
         return;
     }
     cudaLaunchConfig_t cfg = {};
@@ -885,7 +887,15 @@ static void launch_copy(const SampleParams& sp, int64_t grid, size_t smem, cudaS
     at[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    cudaLaunchKernelEx(&cfg, copy_kernel<STRATEGY, VALID, EXTRA>, sp);
+    cudaLaunchKernelEx(&cfg, copy_kernel<STRATEGY, VALID, EXTRA, PSMEM>, sp);
+}
+
+template <int STRATEGY, bool VALID, bool EXTRA>
+static void launch_copy(const SampleParams& sp, int64_t grid, size_t smem, cudaStream_t st) {
+    if (STRATEGY == TGL_UNIFORM && sp.picks_global == nullptr)
+        launch_copy_ps<STRATEGY, VALID, EXTRA, true>(sp, grid, smem, st);
+    else
+        launch_copy_ps<STRATEGY, VALID, EXTRA, false>(sp, grid, smem, st);
 }
 
 // EXTRA: the chain writes per-output data for a following layer or the dedup (ts_edge, child
