@@ -54,6 +54,9 @@ constexpr int kWarps = kTile / 32;
 #endif
 constexpr int kCopyUnroll = TGL_COPY_UNROLL;  // outputs in flight per lane in the flat copy
 constexpr int kSuperShift = 6;  // 64 tiles per super tile (tile bases: super totals + tile totals)
+#ifndef TGL_STCS
+#define TGL_STCS 0
+#endif
 #ifndef TGL_INDEX_MIN
 #define TGL_INDEX_MIN 4096  // C4 A/B: 256 73.9, 1024 74.5, 4096 75.3 G edges/s; C5 unchanged
 #endif
@@ -610,7 +613,11 @@ __global__ void __launch_bounds__(kTile, STRATEGY == TGL_MOST_RECENT ? TGL_COPY_
                                                        : lane == 1 ? (uintptr_t)(o.eid + adj) : (uintptr_t)(o.dt + adj));
         const uint32_t x = inc[b * 32 + lane];
         const uint32_t ex = __shfl_up_sync(kFull, x, 1);
+#if TGL_STCS
+        if (valid) __stcs(reinterpret_cast<long long*>(o.offsets) + i, (long long)(wb + (lane ? ex : 0u)));
+#else
         if (valid) o.offsets[i] = (int64_t)(wb + (lane ? ex : 0u));
+#endif
         fb += __shfl_sync(kFull, x, 31);
     }
     __syncwarp();
@@ -678,9 +685,16 @@ __global__ void __launch_bounds__(kTile, STRATEGY == TGL_MOST_RECENT ? TGL_COPY_
             float* dtp = reinterpret_cast<float*>(wptr[b * 4 + 2]);
             const float tv = __int_as_float(rec[u].x);
             const float tr = troot[r];
+#if TGL_STCS
+            // block outputs are not read again by this kernel: streaming (evict-first) global stores
+            __stcs(reinterpret_cast<int32_t*>(pne.x) + oo[u], rec[u].y);
+            __stcs(reinterpret_cast<int32_t*>(pne.y) + oo[u], rec[u].z);
+            __stcs(dtp + oo[u], __fsub_rn(tr, tv));
+#else
             reinterpret_cast<int32_t*>(pne.x)[oo[u]] = rec[u].y;
             reinterpret_cast<int32_t*>(pne.y)[oo[u]] = rec[u].z;
             dtp[oo[u]] = __fsub_rn(tr, tv);
+#endif
             if (EXTRA) {
                 const BlockOut& o = p.out[b];
                 const uint64_t oi = (uint64_t)((reinterpret_cast<int32_t*>(pne.x) + oo[u]) - o.nbr);
