@@ -54,6 +54,9 @@ constexpr int kWarps = kTile / 32;
 #endif
 constexpr int kCopyUnroll = TGL_COPY_UNROLL;  // outputs in flight per lane in the flat copy
 constexpr int kSuperShift = 6;  // 64 tiles per super tile (tile bases: super totals + tile totals)
+#ifndef TGL_CUT0_MULTI
+#define TGL_CUT0_MULTI 0
+#endif
 #ifndef TGL_STCS
 #define TGL_STCS 0
 #endif
@@ -412,7 +415,19 @@ __global__ void __launch_bounds__(kTile, TGL_WINDOW_MINB) window_kernel(const __
             if (lane == 0) s_red[b][warp] = s2;
         }
     } else {
+#if TGL_CUT0_MULTI
+        // the upper cut through the warp's counted, branch-free search (all 32 lanes reach here;
+        // lanes with no slot before t search an empty gap)
+        uint32_t bcur;
+        {
+            uint32_t a4[4] = {early ? ga[0] : lo, lo, lo, lo}, b4[4] = {early ? gb[0] : lo, lo, lo, lo};
+            const float x4[4] = {t, 0.0f, 0.0f, 0.0f};
+            lower_bound_multi(p, a4, b4, x4);
+            bcur = a4[0];
+        }
+#else
         uint32_t bcur = early ? lower_bound_ts(p, ga[0], gb[0], t) : lo;
+#endif
         for (int b = 0; b < nsb; ++b) {
             // lower bound of window b: layer 0 -> t (-) ((b+1) (x) t_s); l >= 1 -> inherited
             const float xb = p.layer == 0 ? __fsub_rn(t, __fmul_rn((float)(b + 1), p.snapshot_len)) : lin;
