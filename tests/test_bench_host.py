@@ -70,3 +70,12 @@ def test_reduce_report_gloo_world2(tmp_path):
                        env=env, capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stderr[-3000:]
     assert r.stdout.count("ok") == 2
+
+
+def test_workload_names_distinct_and_shared_by_both_arms():
+    """One config.workload per config, used by our arm, the node-sharded mode and the reference arm."""
+    names = {k: bench.workload_name(k, C.CONFIGS[k]) for k in C.CONFIGS}
+    assert len(set(names.values())) == len(names)
+    assert names["C5"].startswith("C5 ") and "121,000,000 nodes" in names["C5"] and "3 snapshot(s) of 5" in names["C5"]
+    src = open(os.path.join(ROOT, "bench.py")).read()
+    assert src.count('"workload": workload_name(key, cfg)') == 3
