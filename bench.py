@@ -358,49 +358,118 @@ class _SelfExchange:
         return t
 
 
-# ----------------------------------------------------------------------------- oracle (CPU) side
-def oracle_sample_rate(cfg, src, dst, ts, roots_list, key_bases, budget_s=None):
-    """Times the oracle (single thread, as it stands) on the given batches; returns dict."""
+# ----------------------------------------------------------------------------- parity (oracle side)
+def oracle_graph(cfg, src, dst, ts, root_tensors):
+    """The oracle's T-CSR for the given layer-0 roots: restricted to their nodes (1 layer; the
+    oracle's own count / fill passes over the stream sub-selected to those nodes), or the whole
+    graph when deeper layers may reach any list.  Returns (T-CSR, build seconds)."""
     import oracle
-    nodes = torch.cat([r for r, _ in roots_list])
-    if len(cfg.fanouts) > 1:  # deeper layers' roots are sampled neighbours: every list may be read
+    t0 = time.perf_counter()
+    if len(cfg.fanouts) > 1:
         nodes = torch.arange(cfg.n_nodes, dtype=torch.int32, device=src.device)
+    else:
+        nodes = torch.cat([r for r in root_tensors])
     s_np, d_np, t_np, e_np, keep = C.relevant_substream(src, dst, ts, nodes, cfg.n_nodes, cfg.add_reverse)
     go = oracle.build_restricted(lambda: iter([(s_np, d_np, t_np, e_np, 0)]), n_nodes=cfg.n_nodes,
                                  add_reverse=cfg.add_reverse, keep=keep)
-    strat = 0 if cfg.strategy == "most_recent" else 1
-    host = [(r.cpu().numpy(), t.cpu().numpy()) for r, t in roots_list]
-    nnz, n_roots, secs, outs = 0, 0, 0.0, []
-    for (r, t), base in zip(host, key_bases):
-        t0 = time.perf_counter()
-        blocks = oracle.sample(go, r, t, fanouts=cfg.fanouts, strategy=strat, n_snapshots=cfg.n_snapshots,
-                               snapshot_len=cfg.snapshot_len, seed=cfg.sampler_seed, root_key_base=base)
-        secs += time.perf_counter() - t0
-        nnz += sum(len(b["nbr"]) for b in blocks)
-        n_roots += len(r)
-        outs.append(blocks)
-        if budget_s is not None and secs > budget_s:
-            break
-    res = {"edges": nnz, "roots": n_roots, "seconds": secs, "outs": outs, "batches": len(outs)}
-    # "oracle x N threads" (SURVEY 8(d)): the same batches over all host cores.  The sampler is
-    # stateless per root and ctypes releases the GIL in the C call, so threads give identical bits.
-    from concurrent.futures import ThreadPoolExecutor
-    n_thr = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
-    todo = list(zip(host, key_bases))[:len(outs)]
+    return go, time.perf_counter() - t0
 
-    def one(item):
-        (r, t), base = item
-        return oracle.sample(go, r, t, fanouts=cfg.fanouts, strategy=strat, n_snapshots=cfg.n_snapshots,
-                             snapshot_len=cfg.snapshot_len, seed=cfg.sampler_seed, root_key_base=base)
+
+def oracle_batches(go, cfg, r_np, t_np, key0, n_threads, n_batches=None):
+    """The oracle on consecutive batches of a root chunk (batch b: roots [b*B, (b+1)*B), key base
+    key0 + b*B), in a thread pool (the oracle is stateless per root and its C call releases the
+    GIL, so any thread count gives the same bits).  Returns (per-batch block lists, seconds)."""
+    import oracle
+    from concurrent.futures import ThreadPoolExecutor
+    B = cfg.batch
+    nb = (len(r_np) + B - 1) // B if n_batches is None else n_batches
+    strat = 0 if cfg.strategy == "most_recent" else 1
+
+    def one(b):
+        return oracle.sample(go, r_np[b * B:(b + 1) * B], t_np[b * B:(b + 1) * B], fanouts=cfg.fanouts, strategy=strat,
+                             n_snapshots=cfg.n_snapshots, snapshot_len=cfg.snapshot_len, seed=cfg.sampler_seed,
+                             root_key_base=key0 + b * B)
     t0 = time.perf_counter()
-    with ThreadPoolExecutor(n_thr) as ex:
-        par = list(ex.map(one, todo))
-    psecs = time.perf_counter() - t0
-    same = all(np.array_equal(a["nbr"], b["nbr"]) and np.array_equal(a["dt"].view(np.uint32), b["dt"].view(np.uint32))
-               for xs, ys in zip(par, outs) for a, b in zip(xs, ys))
-    res["threads"] = {"value": nnz / psecs, "unit": UNIT, "cores": n_thr, "seconds": psecs,
-                      "identical_to_single_thread": bool(same)}
-    return res
+    with ThreadPoolExecutor(max(1, n_threads)) as ex:
+        outs = list(ex.map(one, range(nb)))
+    return outs, time.perf_counter() - t0
+
+
+def concat_batches(per_batch, n_blocks):
+    """Per-batch oracle blocks -> one block per (l, s) over all batches (offsets rebased), i.e. what
+    a single many-batch tgl_sample call must write (epoch mode == per-batch mode, R#7)."""
+    out = []
+    for q in range(n_blocks):
+        offs, base = [np.zeros(1, dtype=np.int64)], 0
+        for bl in per_batch:
+            o = bl[q]["offsets"]
+            offs.append(o[1:] + base)
+            base += int(o[-1])
+        out.append({"offsets": np.concatenate(offs),
+                    **{k: np.concatenate([bl[q][k] for bl in per_batch]) for k in ("nbr", "eid", "dt")}})
+    return out
+
+
+def compare_blocks(blocks, expected):
+    """Element-by-element comparison (ids, eids, offsets; dt as bit patterns) of a GPU call's blocks
+    with the oracle's.  Returns (ok, message of the first mismatch or None)."""
+    for q, (b, e) in enumerate(zip(blocks, expected)):
+        off, nbr, eid, dt, _ = b.trimmed()
+        got = {"offsets": off.cpu().numpy(), "nbr": nbr.cpu().numpy(), "eid": eid.cpu().numpy(),
+               "dt": dt.cpu().numpy().view(np.uint32)}
+        want = dict(e, dt=e["dt"].view(np.uint32))
+        for k in ("offsets", "nbr", "eid", "dt"):
+            a, w = got[k], want[k]
+            if a.shape != w.shape:
+                return False, f"block {q} {k}: length {a.shape[0]} vs oracle {w.shape[0]}"
+            bad = np.flatnonzero(a != w)
+            if bad.size:
+                return False, f"block {q} {k}[{bad[0]}] = {a[bad[0]]} vs oracle {w[bad[0]]} ({bad.size} differ)"
+    return True, None
+
+
+def gpu_batch_digests(tgl, blocks, n_roots, B, L, S):
+    """tgl_block_digest of every (l, s) block, per batch of B layer-0 roots: uint64 [L*S, n_batches].
+    Layer l >= 1 batch bounds = the parent block's offsets at the parent's bounds."""
+    dev = blocks[0].offsets.device
+    nb = (n_roots + B - 1) // B
+    b0 = torch.clamp(torch.arange(nb + 1, dtype=torch.int64, device=dev) * B, max=n_roots)
+    out = [None] * (L * S)
+    for s in range(S):
+        bounds = b0
+        for l in range(L):
+            q = l * S + s
+            if l > 0:
+                bounds = blocks[(l - 1) * S + s].offsets[bounds]
+            out[q] = tgl.block_digest(blocks[q], bounds)
+    return torch.stack(out).cpu().numpy().view(np.uint64)
+
+
+def oracle_batch_digests(per_batch, n_blocks):
+    import oracle
+    return np.array([[oracle.block_digest(bl[q]) for bl in per_batch] for q in range(n_blocks)], dtype=np.uint64)
+
+
+def host_info():
+    """CPU model, logical cores available to this process and RAM of the host."""
+    model = None
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    ram = None
+    try:
+        for line in open("/proc/meminfo"):
+            if line.startswith("MemTotal"):
+                ram = round(int(line.split()[1]) / 2**20, 1)
+                break
+    except OSError:
+        pass
+    cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
+    return {"cpu_model": model, "cores_available": cores, "ram_gib": ram}
 
 
 # ----------------------------------------------------------------------------- our arm
@@ -488,8 +557,14 @@ def run_ours(args):
     step_ms = [a.elapsed_time(b) for a, b in ev]
     total_ms = sum(step_ms) if flush else t_start.elapsed_time(t_end)
 
-    # work done per timed step (deterministic: re-run untimed and read the device counts)
+    # digests of the LAST timed step's blocks as the timed call left them (before any re-run)
+    n_last = chunks[args.warmup + args.steps - 1][0].numel()
+    timed_last_digests = gpu_batch_digests(tgl, sampler.blocks, n_last, B, L, S)
+
+    # work done per timed step (deterministic: re-run untimed and read the device counts) and the
+    # per-batch digests of every timed batch, compared with the oracle's below
     edges_total, bytes_total, roots_total = 0, 0, 0
+    digests_by_start = {}
     for j in range(args.steps):
         r, t = chunks[args.warmup + j]
         blocks = step(args.warmup + j)
@@ -502,6 +577,8 @@ def run_ours(args):
         bytes_total += algorithmic_bytes(cfg, nr, nz)
         if gather is not None:
             bytes_total += gather_bytes(cfg, nr[0], nz[0]) + state_bytes(cfg, events[id(r)][0].numel())
+        digests_by_start[mine[args.warmup + j]] = gpu_batch_digests(tgl, blocks, r.numel(), B, L, S)
+    rerun_same = bool(np.array_equal(digests_by_start[mine[args.warmup + args.steps - 1]], timed_last_digests))
     err = tgl.check(g)
 
     edges_all, bytes_all, total_ms_max = reduce_report(edges_total, bytes_total, total_ms, world, dev)
@@ -561,13 +638,25 @@ def run_ours(args):
                          events=events if gather is not None else None)
         out["e2e_full_d2h"] = e2e(args, tgl, sampler, chunks, mine, cfg, dev, world, full_d2h=True)
 
-    # CPU oracle baseline + parity spot check (rank 0, N = 1 only)
-    if world == 1 and not args.no_cpu_baseline:
-        out["cpu_baseline"], out["parity"] = cpu_baseline(args, cfg, src, dst, ts, tgl, g, sampler, chunks, mine)
+    # parity gate (every rank, its own timed chunks) + CPU oracle baseline (rank 0, N = 1 only)
+    out["parity"], cpu = parity_gate(args, cfg, tgl, sampler, src, dst, ts, chunks, mine, digests_by_start,
+                                     rerun_same, world, want_cpu=world == 1 and not args.no_cpu_baseline)
+    if cpu is not None:
+        out["cpu_baseline"] = cpu
+    failed = not out["parity"]["bit_exact"] or err != 0
+    if world > 1:
+        flag = torch.tensor([1.0 if failed else 0.0], device=dev)
+        torch.distributed.all_reduce(flag, op=torch.distributed.ReduceOp.MAX)
+        failed = bool(flag.item())
+    if failed:  # a run whose outputs do not match the oracle reports no throughput
+        out["error"] = "parity failure or device error: no throughput reported"
+        out["value_unverified"], out["value"] = out["value"], None
     if rank == 0:
         print(json.dumps(out), flush=True)
     if world > 1:
         torch.distributed.destroy_process_group()
+    if failed:
+        sys.exit(1)
 
 
 def per_batch(args, tgl, g, cfg, chunk, key0, dev, world, n_graph=64, reps=10):
@@ -735,46 +824,88 @@ def e2e(args, tgl, sampler, chunks, mine, cfg, dev, world, full_d2h=False, gathe
             "pinned host roots -> H2D -> tgl_sample -> D2H of the step's metric (per-block n_roots, nnz); "
             "blocks stay on the GPU for the consumer")
     return {"value": edges / (ms_max / 1e3), "unit": UNIT, "h2d_bytes_per_step": stats["h2d"] // args.steps,
-            "d2h_bytes_per_step": stats["d2h"] // args.steps, "note": what + "; copy and compute streams overlapped"}
+            "d2h_bytes_per_step": stats["d2h"] // args.steps,
+            "kind": "full_d2h" if full_d2h else "device_consumer",
+            "note": what + "; copy and compute streams overlapped"
+                    + ("" if full_d2h else "; the blocks' own D2H is measured separately as e2e_full_d2h (PCIe-bound)")}
 
 
-def cpu_baseline(args, cfg, src, dst, ts, tgl, g, sampler, chunks, mine):
-    """Oracle as it stands, single thread on the host, on a bounded sample of the timed batches;
-    its outputs are also compared bit for bit with ours on those batches (parity gate)."""
+def parity_gate(args, cfg, tgl, sampler, src, dst, ts, chunks, mine, digests_by_start, rerun_same, world,
+                want_cpu):
+    """Parity of the TIMED configuration: the oracle samples whole timed chunks
+    (every batch of a timed tgl_sample call, its key base = the batch's global root index); then
+      * element by element: the first timed chunk re-run through the timed Sampler (same call, same
+        launch configuration: 8.19 M roots = 32,000 tiles on C5) against the oracle's batches,
+        concatenated (epoch mode == per-batch mode, R#7);
+      * per-batch FNV-1a digests (tgl_block_digest) of every timed batch against the oracle's, on
+        --parity-chunks distinct timed chunks (the digests of the other timed batches are reported
+        for reproducibility; the last timed step's digests taken straight from the timed call's
+        buffers must equal its re-run's).
+    Also returns the CPU baseline (oracle as it stands, one thread, bounded sample; N = 1)."""
     B = cfg.batch
-    j0 = args.warmup
-    r_all, t_all = chunks[j0]
-    pilot = min(8, r_all.numel() // B)
-    n_b = pilot
-    batches = [(r_all[i * B:(i + 1) * B], t_all[i * B:(i + 1) * B]) for i in range(n_b)]
-    bases = [mine[j0] + i * B for i in range(n_b)]
-    res = oracle_sample_rate(cfg, src, dst, ts, batches, bases)
-    per_batch = res["seconds"] / max(1, res["batches"])
-    want = int(min(r_all.numel() // B, max(pilot, args.cpu_seconds / max(per_batch, 1e-6))))
-    if want > pilot:
-        batches = [(r_all[i * B:(i + 1) * B], t_all[i * B:(i + 1) * B]) for i in range(want)]
-        bases = [mine[j0] + i * B for i in range(want)]
-        res = oracle_sample_rate(cfg, src, dst, ts, batches, bases, budget_s=3 * args.cpu_seconds)
-    # parity on the sampled batches: run ours on exactly these roots (per batch, untimed)
-    S, L = cfg.n_snapshots, len(cfg.fanouts)
-    ok, checked = True, 0
-    small = tgl.Sampler(g, B, cfg.fanouts, cfg.strategy, S, cfg.snapshot_len)
-    for (r, t), base, bo in zip(batches, bases, res["outs"]):
-        blocks = small.run(r, t, seed=cfg.sampler_seed, root_key_base=base)
-        for b, o in zip(blocks, bo):
-            off, nbr, eid, dt, _ = b.trimmed()
-            ok &= np.array_equal(off.cpu().numpy(), o["offsets"]) and np.array_equal(nbr.cpu().numpy(), o["nbr"]) \
-                and np.array_equal(eid.cpu().numpy(), o["eid"]) \
-                and np.array_equal(dt.cpu().numpy().view(np.uint32), o["dt"].view(np.uint32))
-        checked += len(r)
-    cores = 1
-    return ({"value": res["edges"] / res["seconds"], "unit": UNIT, "cores": cores, "kind": "oracle",
-             "sample": f"{res['batches']} consecutive batches x {B} roots ({res['roots']:,} roots, "
-                       f"{res['edges']:,} sampled edges) from timed step 0, single-threaded C oracle "
-                       f"(-O2 -ffp-contract=off) on a T-CSR restricted to the sampled nodes"
-                       + (" (sampler only: the oracle's gather / state write are not timed)" if cfg.tables else ""),
-             "seconds": res["seconds"], "oracle_x_threads": res["threads"]},
-            {"checked_roots": checked, "bit_exact": bool(ok), "against": "oracle/ (CPU), same batches"})
+    L, S = len(cfg.fanouts), cfg.n_snapshots
+    n_thr = max(1, host_info()["cores_available"] // max(1, world))
+    timed = [mine[args.warmup + j] for j in range(args.steps)]
+    distinct = list(dict.fromkeys(timed))
+    n_chk = max(1, min(args.parity_chunks, len(distinct)))
+    pick = [distinct[(len(distinct) - 1) * c // max(1, n_chk - 1)] if n_chk > 1 else distinct[0] for c in range(n_chk)]
+    pick = list(dict.fromkeys(pick))
+    by_start = {s0: chunks[args.warmup + timed.index(s0)] for s0 in pick}
+    go, build_s = oracle_graph(cfg, src, dst, ts, [by_start[s0][0] for s0 in pick])
+    ok_digest, checked_batches, first_mismatch, elem = True, 0, None, None
+    cpu = None
+    for idx, s0 in enumerate(pick):
+        r, t = by_start[s0]
+        r_np, t_np = r.cpu().numpy(), t.cpu().numpy()
+        per_batch, secs = oracle_batches(go, cfg, r_np, t_np, s0, n_thr)
+        od = oracle_batch_digests(per_batch, L * S)
+        gd = digests_by_start[s0]
+        same = od.shape == gd.shape and bool(np.array_equal(od, gd))
+        if not same and first_mismatch is None:
+            bad = np.argwhere(od != gd) if od.shape == gd.shape else [[-1, -1]]
+            first_mismatch = f"chunk {s0}: block {int(bad[0][0])} batch {int(bad[0][1])}"
+        ok_digest &= same
+        checked_batches += gd.shape[1]
+        if idx == 0:
+            blocks = sampler.run(r, t, seed=cfg.sampler_seed, root_key_base=s0)  # the timed call
+            ok, msg = compare_blocks(blocks, concat_batches(per_batch, L * S))
+            n_edges = int(sum(len(bl[q]["nbr"]) for bl in per_batch for q in range(L * S)))
+            elem = {"roots": int(r.numel()), "tiles_per_call": (int(r.numel()) + 255) // 256, "edges": n_edges,
+                    "bit_exact": ok, "first_mismatch": msg}
+            if want_cpu:
+                cpu = cpu_baseline(args, cfg, go, build_s, r_np, t_np, s0,
+                                   {"value": n_edges / secs, "unit": UNIT, "cores": n_thr, "seconds": secs,
+                                    "sample": f"the whole chunk ({len(per_batch)} batches)"})
+    n_timed_batches = sum((chunks[args.warmup + j][0].numel() + B - 1) // B for j in range(args.steps))
+    bit_exact = bool(elem["bit_exact"] and ok_digest and rerun_same)
+    return ({"bit_exact": bit_exact, "against": "oracle/ (CPU) on the timed chunks",
+             "checked_roots": elem["roots"], "elementwise": elem,
+             "digests": {"timed_batches": n_timed_batches,
+                         "blocks_per_batch": L * S, "oracle_checked_batches": checked_batches,
+                         "oracle_checked_chunks": len(pick), "match": ok_digest, "first_mismatch": first_mismatch,
+                         "timed_call_equals_rerun": rerun_same,
+                         "algorithm": "FNV-1a-64 per (batch, block): rebased int64 offsets, nbr, eid, dt bits "
+                                      "(tgl_block_digest vs oracle.block_digest)"},
+             "oracle_build_s": build_s}, cpu)
+
+
+def cpu_baseline(args, cfg, go, build_s, r_np, t_np, key0, threaded):
+    """Oracle as it stands, ONE thread on the host, on a bounded sample (consecutive batches of the
+    first timed chunk, about --cpu-seconds of work), plus the same oracle over all host cores
+    (threaded) on the whole chunk -- the parity run above."""
+    B = cfg.batch
+    nb_all = len(r_np) // B
+    pilot = min(8, nb_all)
+    _, secs = oracle_batches(go, cfg, r_np, t_np, key0, 1, n_batches=pilot)
+    want = int(min(nb_all, max(pilot, args.cpu_seconds / max(secs / max(pilot, 1), 1e-6))))
+    outs, secs = oracle_batches(go, cfg, r_np, t_np, key0, 1, n_batches=want)
+    edges = sum(len(b["nbr"]) for bl in outs for b in bl)
+    return {"value": edges / secs, "unit": UNIT, "cores": 1, "kind": "oracle",
+            "sample": f"{want} consecutive batches x {B} roots ({want * B:,} roots, {edges:,} sampled edges) of the "
+                      f"first timed chunk, single-threaded C oracle (-O2 -ffp-contract=off) on its T-CSR restricted "
+                      f"to the chunk's nodes" + (" (sampler only: the oracle's gather / state write are not timed)"
+                                                  if cfg.tables else ""),
+            "seconds": secs, "oracle_x_threads": threaded, "oracle_tcsr_build_s": build_s, "host": host_info()}
 
 
 # ----------------------------------------------------------------------------- reference arm
@@ -829,9 +960,45 @@ def run_reference(args):
     print(json.dumps(out), flush=True)
 
 
+def relaunch(n: int) -> int:
+    """`bench.py --gpus N` outside torchrun: re-run this command under torch.distributed.run with N
+    local ranks (one process per GPU, rendezvous on 127.0.0.1), as the driver's N > 1 launch does."""
+    import socket
+    import subprocess
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
+def run_dry(args):
+    """Host logic of the N-rank launch without a GPU (gloo): world size, the rank's chunk starts and
+    the max-over-ranks / sum-of-work reduction, printed by rank 0 (tests/test_bench_host.py)."""
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    import torch.distributed as dist
+    if world > 1:
+        dist.init_process_group("gloo")
+    cfg = C.CONFIGS[args.config]
+    mine = rank_chunks(cfg.n_roots_epoch, args.batches * cfg.batch, args.steps, world, rank, cfg.batch)
+    gathered = [None] * world
+    if world > 1:
+        dist.all_gather_object(gathered, mine)
+    else:
+        gathered = [mine]
+    edges, _, ms = reduce_report(1000.0 * (rank + 1), 0.0, 2.0 + rank, world, torch.device("cpu"))
+    if rank == 0:
+        print(json.dumps({"n_gpus": world, "chunks": gathered, "edges": edges, "ms": ms}), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--gpus", type=int, default=None,
+                    help="GPUs (ranks) of this node; outside torchrun N > 1 re-launches under torch.distributed.run")
     ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="C5", choices=sorted(C.CONFIGS))
@@ -840,15 +1007,28 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--ref-batches", type=int, default=16, help="reference arm: batches per step")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--parity-chunks", type=int, default=2,
+                    help="distinct timed chunks whose per-batch digests are checked against the oracle")
     ap.add_argument("--distinct", type=int, default=32, help="distinct root chunks (cycled over the steps)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-per-batch", action="store_true")
     ap.add_argument("--sharding", default="root", choices=["root", "node"],
                     help="root: replicated T-CSR, roots sharded (default); node: node-sharded T-CSR (SURVEY 8(e))")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--dry-run", action="store_true", help=argparse.SUPPRESS)  # host logic only (gloo, no GPU)
     args = ap.parse_args()
+    world_env = os.environ.get("WORLD_SIZE")
+    if world_env is None and (args.gpus or 1) > 1:
+        sys.exit(relaunch(args.gpus))
+    world = int(world_env or 1)
+    if args.gpus is None:
+        args.gpus = world
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
     if args.batches <= 0:
         args.batches = 2048 if args.config == "C5" else 256
+    if args.dry_run:
+        return run_dry(args)
     if args.warmup < 3 and args.impl == "ours":
         print("warning: --warmup < 3 violates the timing rules", file=sys.stderr)
     if args.impl == "reference":

@@ -339,6 +339,25 @@ TGL_API int tgl_state_write(const int32_t *ids, const float *ts, int64_t n_event
 TGL_API int tgl_chunk_schedule(int64_t n_edges, int64_t batch_size, int64_t chunk_size, uint64_t epoch,
                        uint64_t seed, int64_t *first_edge, int64_t cap, int64_t *n_batches, void *stream);
 
+/* ------------------------------------------------------------------ verification */
+
+/*
+ * Per-batch digest of one message-flow block ("a per-batch 64-bit checksum (FNV-1a
+ * over offsets, nbr, eid and dt bits)"), so that every batch a timed call produced can be compared
+ * with the oracle's output for the same batch without copying the block to the host.  Not a step
+ * of Alg. 1: a verification utility.
+ * Batch j covers the block's roots [bounds[j], bounds[j+1]) (bounds: device int64 [n_batches+1],
+ * non-decreasing, bounds[n_batches] <= the block's n_roots; layer 0: j*B; layer l >= 1: the parent
+ * block's offsets at the parent batch bounds).  With e0 = offsets[bounds[j]], e1 =
+ * offsets[bounds[j+1]], out[j] (device uint64) is FNV-1a-64 (basis 0xcbf29ce484222325, prime
+ * 0x100000001b3) over these bytes, little-endian, in this order:
+ *   offsets[i] - e0 as int64 for i = bounds[j] .. bounds[j+1]   (n_j + 1 values, the first 0),
+ *   nbr[e0 .. e1), eid[e0 .. e1), then the bit patterns of dt[e0 .. e1)   (32-bit words).
+ * One thread per batch (FNV is sequential).  Errors: TGL_EINVAL for n_batches < 0 or a NULL pointer.
+ */
+TGL_API int tgl_block_digest(const int64_t *offsets, const int32_t *nbr, const int32_t *eid, const float *dt,
+                     const int64_t *bounds, int64_t n_batches, uint64_t *out, void *stream);
+
 /* ------------------------------------------------------------------ errors */
 
 /* Synchronises `stream`, returns the first sticky device error raised since the last check by

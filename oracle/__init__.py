@@ -65,6 +65,8 @@ def lib():
         L.oracle_gather.restype = None
         L.oracle_state_write.argtypes = [P, P, i64, i32, i32, P, P, P, i64, P, P]
         L.oracle_state_write.restype = None
+        L.oracle_fnv1a64.argtypes = [P, i64, u64]
+        L.oracle_fnv1a64.restype = u64
         _lib = L
     return _lib
 
@@ -318,3 +320,24 @@ def chunk_schedule(n_edges: int, bs: int, cs: int, epoch: int, seed: int) -> Lis
         out.append(e_s)
         e_s += bs
     return out
+
+
+# --------------------------------------------------------------------------- checksums (test infra)
+FNV_BASIS = 0xcbf29ce484222325
+
+
+def fnv1a64(data: bytes | np.ndarray, h: int = FNV_BASIS) -> int:
+    """64-bit FNV-1a over the bytes of `data`, continuing from h (tgl_oracle.c)."""
+    a = np.ascontiguousarray(np.frombuffer(data, dtype=np.uint8) if isinstance(data, (bytes, bytearray))
+                             else np.asarray(data).view(np.uint8).reshape(-1))
+    return int(lib().oracle_fnv1a64(_p(a), a.size, h))
+
+
+def block_digest(block: dict) -> int:
+    """Digest of one oracle block in the byte order of tgl_block_digest (include/tgl.h): offsets
+    rebased to the block's first root (int64), then nbr, eid and the dt bit patterns."""
+    off = np.ascontiguousarray(block["offsets"] - block["offsets"][0], dtype="<i8")
+    h = fnv1a64(off)
+    h = fnv1a64(np.ascontiguousarray(block["nbr"], dtype="<i4"), h)
+    h = fnv1a64(np.ascontiguousarray(block["eid"], dtype="<i4"), h)
+    return fnv1a64(np.ascontiguousarray(block["dt"], dtype="<f4").view("<u4"), h)

@@ -360,3 +360,16 @@ void oracle_state_write(const int32_t *ids, const float *ts, int64_t n, int32_t 
         if (K > 1 && pos) pos[v] = (q + 1) % K;
     }
 }
+
+/* Checksum (test infrastructure, not part of the method): 64-bit FNV-1a over n bytes, continuing
+ * from h (pass the basis 0xcbf29ce484222325 to start).  Used to compare per-batch digests of the
+ * GPU's blocks with the oracle's blocks; written from the FNV-1a definition
+ * (h ^= byte; h *= 0x100000001b3 for every byte), pinned by the published test vectors. */
+uint64_t oracle_fnv1a64(const uint8_t *p, int64_t n, uint64_t h)
+{
+    for (int64_t i = 0; i < n; ++i) {
+        h ^= p[i];
+        h *= 0x100000001b3ull;
+    }
+    return h;
+}

@@ -26,7 +26,7 @@ from ._lib import MOST_RECENT, UNIFORM, TGLError
 _L = _lib.load()
 
 __all__ = ["TCSR", "Block", "Sampler", "build", "wrap", "aux_bytes", "sample", "gather", "check", "shard_bucket",
-           "set_node_base", "shard_unpermute", "offsets_to_counts",
+           "set_node_base", "shard_unpermute", "offsets_to_counts", "block_digest",
            "MOST_RECENT", "UNIFORM", "TGLError", "lib_path"]
 
 lib_path = _lib.LIB_PATH
@@ -257,13 +257,20 @@ class Sampler:
         """tgl_sample (or tgl_sample_keyed when root_keys, int64 bit patterns of uint64 keys, is given)
         on the current (or given) stream; no host synchronisation."""
         n = roots.numel() if n_roots is None else int(n_roots)
-        if n > self.max_roots:
-            raise ValueError(f"{n} roots > max_roots {self.max_roots}")
+        if n < 0 or n > self.max_roots:
+            raise ValueError(f"{n} roots outside [0, max_roots {self.max_roots}]")
         if not (roots.is_cuda and roots.dtype == torch.int32 and root_ts.is_cuda and root_ts.dtype == torch.float32):
             raise TypeError("roots must be CUDA int32 and root_ts CUDA float32 (no CPU fallback)")
+        # raw data pointers go to the library: the tensors must be dense and hold n elements
+        if not (roots.is_contiguous() and root_ts.is_contiguous()):
+            raise ValueError("roots and root_ts must be contiguous")
+        if n > roots.numel() or n > root_ts.numel():
+            raise ValueError(f"n_roots {n} exceeds roots ({roots.numel()}) or root_ts ({root_ts.numel()})")
         if root_keys is not None:
             if not (root_keys.is_cuda and root_keys.dtype == torch.int64):
                 raise TypeError("root_keys must be a CUDA int64 tensor (uint64 bit patterns)")
+            if not root_keys.is_contiguous() or n > root_keys.numel():
+                raise ValueError("root_keys must be contiguous with at least n_roots elements")
             _rc(_L.tgl_sample_ex(self.g.handle, _ptr(roots), _ptr(root_ts), _ptr(root_keys), n, self.L, self._fan,
                                  self.strategy, self.S, self.snapshot_len, int(seed) & 0xFFFFFFFFFFFFFFFF, 0,
                                  ctypes.byref(self._opts), self._c_blocks, self._c_dedup, _ptr(self.workspace),
@@ -422,6 +429,17 @@ def state_write_at(ids: torch.Tensor, ts: Optional[torch.Tensor], tables, *, nod
     tst_p = None if ts_table is None else ts_table.data_ptr() - lo * K * 4
     _rc(_L.tgl_state_write(_ptr(ids), _ptr(ts), n, int(n_nodes_global), int(K), pos_p, tst_p, arr, len(tables),
                            _ptr(ws), b.value, _stream(stream)), "tgl_state_write")
+
+
+def block_digest(block: Block, bounds: torch.Tensor, stream=None) -> torch.Tensor:
+    """tgl_block_digest: per-batch FNV-1a-64 of a block (int64 tensor holding the uint64 bit
+    patterns); batch j = the block's roots [bounds[j], bounds[j+1])."""
+    bounds = _cuda(bounds, torch.int64, "bounds")
+    nb = max(bounds.numel() - 1, 0)
+    out = torch.empty(nb, dtype=torch.int64, device=bounds.device)
+    _rc(_L.tgl_block_digest(_ptr(block.offsets), _ptr(block.nbr), _ptr(block.eid), _ptr(block.dt), _ptr(bounds), nb,
+                            _ptr(out), _stream(stream)), "tgl_block_digest")
+    return out
 
 
 def check(g: Optional[TCSR] = None, stream=None) -> int:

@@ -72,6 +72,7 @@ SIGNATURES = {
     "tgl_state_write_workspace": (ctypes.c_int, [i64, i32, ctypes.POINTER(sz)]),
     "tgl_state_write": (ctypes.c_int, [P, P, i64, i32, i32, P, P, P, i32, P, sz, P]),
     "tgl_check": (ctypes.c_int, [P, P]),
+    "tgl_block_digest": (ctypes.c_int, [P, P, P, P, P, i64, P, P]),
     "tgl_shard_bucket_workspace": (ctypes.c_int, [i64, i32, ctypes.POINTER(sz)]),
     "tgl_shard_bucket": (ctypes.c_int, [P, i64, P, i32, P, P, P, sz, P]),
 }

@@ -40,20 +40,6 @@ __device__ __forceinline__ uint32_t lanemask_lt() {
     return m;
 }
 
-// Relaxed gpu-scope 64-bit load/store for the decoupled look-back state words.
-__device__ __forceinline__ uint64_t ld_relaxed_u64(const uint64_t* p) {
-    uint64_t v;
-    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-    return v;
-}
-__device__ __forceinline__ void st_relaxed_u64(uint64_t* p, uint64_t v) {
-    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-
-// Streaming (evict-first) stores for outputs that are not re-read by this kernel.
-template <typename T>
-__device__ __forceinline__ void st_stream(T* p, T v) { __stcs(p, v); }
-
 inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
 // Bump allocator over a caller workspace (256-byte aligned carve-outs).

@@ -1042,11 +1042,12 @@ static int sample_impl(const tgl_tcsr* g, const int32_t* roots, const float* roo
     if (need_zero &&
         cudaMemsetAsync(static_cast<char*>(workspace) + P.memset_from, 0, P.memset_bytes, st) != cudaSuccess)
         return TGL_ECUDA;
-    // experiment knobs (tools/sweep.py): TGL_NO_INDEX, TGL_NO_RECS, TGL_L2_FETCH (L2 fetch granularity)
-    static const char* l2f = getenv("TGL_L2_FETCH");
-    if (l2f) cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, (size_t)atoi(l2f));
-    const bool use_recs = g->recs && !getenv("TGL_NO_RECS");
-    const bool use_index = g->index && g->n_levels > 0 && !getenv("TGL_NO_INDEX");
+    // A/B knobs (tools/sweep.py), read once per process: TGL_NO_RECS / TGL_NO_INDEX run the same
+    // kernels over the plain T-CSR arrays
+    static const bool no_recs = getenv("TGL_NO_RECS") != nullptr;
+    static const bool no_index = getenv("TGL_NO_INDEX") != nullptr;
+    const bool use_recs = g->recs && !no_recs;
+    const bool use_index = g->index && g->n_levels > 0 && !no_index;
     static const bool no_fork = getenv("TGL_NO_FORK") != nullptr;  // A/B knob
     ForkStreams* fk = nullptr;
     if (S > 1 && L > 1 && !dedup && !no_fork) {  // dedup shares one scratch across chains: sequential

@@ -79,3 +79,26 @@ def test_workload_names_distinct_and_shared_by_both_arms():
     assert names["C5"].startswith("C5 ") and "121,000,000 nodes" in names["C5"] and "3 snapshot(s) of 5" in names["C5"]
     src = open(os.path.join(ROOT, "bench.py")).read()
     assert src.count('"workload": workload_name(key, cfg)') == 3
+
+
+@pytest.mark.parametrize("n", [2])
+def test_gpus_flag_self_launches_n_ranks(n):
+    """`bench.py --gpus N` outside torchrun re-launches itself with N ranks (gloo here, --dry-run:
+    host logic only) -- n_gpus in the line is the real world size and the ranks' chunks are disjoint."""
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", str(n), "--steps", "4",
+                        "--dry-run"], env=env, capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stderr[-3000:]
+    import json
+    line = json.loads([x for x in r.stdout.splitlines() if x.startswith("{")][-1])
+    assert line["n_gpus"] == n
+    starts = [s for rank_chunks in line["chunks"] for s in rank_chunks]
+    assert len(starts) == 4 * n and len(set(starts)) == len(starts)
+    assert line["edges"] == sum(1000.0 * (q + 1) for q in range(n)) and line["ms"] == 2.0 + n - 1
+
+
+def test_gpus_flag_must_match_world_size():
+    env = dict(os.environ, WORLD_SIZE="1", RANK="0", LOCAL_RANK="0")
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--dry-run"], env=env,
+                       capture_output=True, text=True, timeout=300)
+    assert r.returncode != 0 and "WORLD_SIZE" in r.stderr

@@ -296,3 +296,22 @@ def test_gather_bytes():
     np.testing.assert_array_equal(out.view(np.uint32), want.view(np.uint32))
     out, err = oracle.gather(np.array([17], np.int32), table)
     assert err != 0 and not out.any()
+
+
+def test_fnv1a64_published_vectors():
+    """The digest used for per-batch parity against the FNV-1a-64 test vectors
+    published with the algorithm (Fowler/Noll/Vo): "" / "a" / "foobar"."""
+    assert oracle.fnv1a64(b"") == 0xcbf29ce484222325
+    assert oracle.fnv1a64(b"a") == 0xaf63dc4c8601ec8c
+    assert oracle.fnv1a64(b"foobar") == 0x85944171f73967e8
+    # continuation == one pass over the concatenation
+    assert oracle.fnv1a64(b"bar", oracle.fnv1a64(b"foo")) == oracle.fnv1a64(b"foobar")
+
+
+def test_block_digest_byte_order():
+    """oracle.block_digest hashes rebased int64 offsets, then nbr, eid and dt bits, little-endian."""
+    blk = {"offsets": np.array([5, 6, 8], dtype=np.int64), "nbr": np.array([7, 8, 9], dtype=np.int32),
+           "eid": np.array([1, 2, 3], dtype=np.int32), "dt": np.array([1.0, 2.0, 0.5], dtype=np.float32)}
+    raw = (np.array([0, 1, 3], dtype="<i8").tobytes() + np.array([7, 8, 9], dtype="<i4").tobytes()
+           + np.array([1, 2, 3], dtype="<i4").tobytes() + np.array([1.0, 2.0, 0.5], dtype="<f4").tobytes())
+    assert oracle.block_digest(blk) == oracle.fnv1a64(raw)
