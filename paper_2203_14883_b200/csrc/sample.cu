@@ -284,8 +284,9 @@ __device__ __forceinline__ uint32_t select_valid(const SampleParams& p, int64_t 
 
 // ---------------------------------------------------------------------------- K4a windows
 template <int STRATEGY, bool VALID>
-__global__ void __launch_bounds__(kTile, TGL_WINDOW_MINB) window_kernel(const __grid_constant__ SampleParams p) {
+__global__ void __launch_bounds__(kTile, VALID ? 6 : TGL_WINDOW_MINB) window_kernel(const __grid_constant__ SampleParams p) {
     __shared__ uint32_t s_red[TGL_MAX_SNAPSHOTS][kWarps];
+    __shared__ int4 s_rec[kTile * 4];  // the tile's 64-byte node records (16 KB)
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int64_t n = chain_roots(p);
     const int64_t tile = (int64_t)blockIdx.x;
@@ -333,10 +334,13 @@ __global__ void __launch_bounds__(kTile, TGL_WINDOW_MINB) window_kernel(const __
     bool early;                             // some slot is earlier than t: the list must be searched
     if (p.nodes) {
         // 4 lanes read one 64-byte node record (one request per record): rounds q = 0..3 cover the
-        // warp's roots q*8 .. q*8+7; per round each quad counts its fences below the root's cut
-        // times and hands lo, hi and the counts to the root's lane
-        int4 ch[4];
+        // warp's roots q*8 .. q*8+7 and park the records in shared memory (16-byte chunk c of root r
+        // at chunk slot c ^ ((r >> 1) & 3): the 8 lanes of a quarter-warp then read 8 distinct
+        // bank groups); then every lane counts its own root's 14 fences below each cut time with a
+        // branch-free binary search over the record (fences are sorted)
+        int4* wrec = s_rec + warp * 32 * 4;
         const int quad = lane >> 2, part = lane & 3;
+        int4 ch[4];
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
             const int src = q * 8 + quad;
@@ -345,32 +349,29 @@ __global__ void __launch_bounds__(kTile, TGL_WINDOW_MINB) window_kernel(const __
             ch[q] = okq ? __ldg(p.nodes + (size_t)vq * 4 + part)
                         : make_int4(part ? 0x7f800000 : 0, part ? 0x7f800000 : 0, 0x7f800000, 0x7f800000);
         }
-        uint32_t packed = 0;
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
             const int src = q * 8 + quad;
-            float xq[4];
-            cuts_of(__shfl_sync(kFull, t, src), __shfl_sync(kFull, lin, src), xq);
-            const float f[4] = {__int_as_float(ch[q].x), __int_as_float(ch[q].y), __int_as_float(ch[q].z),
-                                __int_as_float(ch[q].w)};
-            uint32_t c = 0;
+            wrec[src * 4 + (part ^ ((src >> 1) & 3))] = ch[q];
+        }
+        __syncwarp();
+        const int sw = (lane >> 1) & 3;
+        const float* rec = reinterpret_cast<const float*>(wrec + lane * 4);
+        auto word = [&](int w) { return rec[(((w >> 2) ^ sw) << 2) | (w & 3)]; };  // record word w
+        lo = __float_as_uint(word(0));
+        hi = __float_as_uint(word(1));
+        uint32_t packed = 0;
 #pragma unroll
-            for (int e = 0; e < 4; ++e) {
-                if (part == 0 && e < 2) continue;  // lo, hi
+        for (int j = 0; j < 4; ++j) {
+            // number of fences f[0..13] (= words 2..15) below x[j]; positions >= 14 act as +inf
+            int c = 0;
 #pragma unroll
-                for (int j = 0; j < 4; ++j) c += (f[e] < xq[j] ? 1u : 0u) << (8 * j);
+            for (int step = 8; step >= 1; step >>= 1) {
+                const int e = c + step - 1;
+                const bool below = e < kFences && word(2 + min(e, kFences - 1)) < x[j];
+                c += below ? step : 0;
             }
-            c += __shfl_xor_sync(kFull, c, 1);
-            c += __shfl_xor_sync(kFull, c, 2);
-            const int from = 4 * (lane & 7);  // lane q*8 + g takes quad g's result
-            const uint32_t cq = __shfl_sync(kFull, c, from);
-            const uint32_t loq = (uint32_t)__shfl_sync(kFull, ch[q].x, from);
-            const uint32_t hiq = (uint32_t)__shfl_sync(kFull, ch[q].y, from);
-            if ((lane >> 3) == q) {
-                packed = cq;
-                lo = loq;
-                hi = hiq;
-            }
+            packed |= (uint32_t)c << (8 * j);
         }
         const uint32_t d = hi - lo;
 #pragma unroll
