@@ -3,9 +3,10 @@ NVCC ?= /usr/local/cuda/bin/nvcc
 PKG := paper_2203_14883_b200
 SRCS := $(wildcard $(PKG)/csrc/*.cu)
 HDRS := $(wildcard $(PKG)/csrc/*.cuh) include/tgl.h
-NVFLAGS := -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 \
+NCCL_INC ?= $(shell python3 -c 'import nvidia.nccl, os; print(os.path.join(list(nvidia.nccl.__path__)[0], "include"))' 2>/dev/null || echo /usr/include)
+NVFLAGS := -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -I$(NCCL_INC) \
            -Xcompiler -fPIC -Xcompiler -fvisibility=hidden -shared -ftz=false -prec-div=true -prec-sqrt=true \
-           -fmad=true -Xptxas -v
+           -fmad=true -Xptxas -v -ldl
 
 all: $(PKG)/libtgl.so oracle/liboracle.so
 

@@ -9,7 +9,8 @@
  *                                                      (L154-L175, L210), edge features (Table 3)
  *   tgl_state_write  node memory / mailbox update       Fig. 2 step 6 (L201), mailbox of the K
  *                                                      most recent mails (L210, L322)
- *   tgl_shard_*      node-sharded exchange helpers      (not in the paper)
+ *   tgl_shard_*, tgl_sample_sharded, tgl_tcsr_build_range
+ *                    node-sharded T-CSR + exchange      (not in the paper)
  *   tgl_chunk_schedule  random chunk scheduling         Alg. 2 (L274-L291)
  *
  * Conventions (every entry point):
@@ -59,7 +60,7 @@ enum {
     TGL_ECAPACITY = -4,  /* an output buffer is smaller than tgl_sample_capacity() says */
     TGL_EWORKSPACE = -5, /* workspace smaller than the *_workspace() query says */
     TGL_ECUDA = -6,      /* CUDA runtime error (launch failure, ...) */
-    TGL_ENCCL = -7,      /* reserved: collective failure in the node-sharded mode */
+    TGL_ENCCL = -7,      /* collective failure (NCCL) in the node-sharded mode */
     TGL_ENOTSUP = -8     /* device is not sm_100 */
 };
 
@@ -398,6 +399,82 @@ TGL_API int tgl_shard_unpermute(const int32_t *perm, int64_t n_roots, const int3
                         const int32_t *nbr_in, const int32_t *eid_in, const float *dt_in,
                         int64_t *offsets_out, int32_t *nbr_out, int32_t *eid_out, float *dt_out,
                         void *workspace, size_t ws_bytes, void *stream);
+
+/* ------------------------------------------------------------------ node-sharded T-CSR */
+
+/*
+ * Build only the lists of the nodes [node_lo, node_hi) of a chronological stream: the rank-local
+ * T-CSR of the node-sharded mode (its memory ~ E_s / world).  Same method and bits as
+ * tgl_tcsr_build restricted to the logical edges whose owner is in the range: the
+ * local lists equal the full build's lists of those nodes, element for element.
+ * n_local_stored = the range's E_s (e.g. indptr[node_hi] - indptr[node_lo] of the full degree
+ * scan); the call fails with TGL_ECAPACITY if it is not.  Outputs: indptr[node_hi - node_lo + 1]
+ * (local, starting at 0), nbr / ts_out / eid_out [n_local_stored] (ts_out 64-byte aligned, padded
+ * to a multiple of 16 floats, as tgl_tcsr_build), aux optional (tgl_tcsr_aux_bytes(n_local_stored,
+ * node_hi - node_lo)).  The whole stream is validated (synchronously).  The returned handle has its
+ * node base set to node_lo (tgl_tcsr_set_node_base): roots and neighbours keep global ids.
+ * src / dst / ts / eid may be device memory or mapped pinned host memory (read once per pass).
+ */
+/* The full graph's indptr [n_nodes+1] only (validation + degree histogram + scan, synchronous like
+ * tgl_tcsr_build): what a rank needs to choose edge-balanced node ranges before building its own. */
+TGL_API int tgl_tcsr_indptr_workspace(int64_t n_edges, int32_t n_nodes, size_t *bytes /* host */);
+TGL_API int tgl_tcsr_indptr(const int32_t *src, const int32_t *dst, const float *ts, int64_t n_edges, int32_t n_nodes,
+                    int add_reverse, int64_t *indptr, void *workspace, size_t ws_bytes, void *stream);
+
+TGL_API int tgl_tcsr_build_range_workspace(int64_t n_edges, int32_t n_nodes, int add_reverse, int32_t node_lo,
+                                   int32_t node_hi, int64_t n_local_stored, size_t *bytes /* host */);
+TGL_API int tgl_tcsr_build_range(const int32_t *src, const int32_t *dst, const float *ts, const int32_t *eid,
+                         int64_t n_edges, int32_t n_nodes, int add_reverse, int32_t node_lo, int32_t node_hi,
+                         int64_t n_local_stored, int64_t *indptr, int32_t *nbr, float *ts_out, int32_t *eid_out,
+                         void *aux, size_t aux_bytes, void *workspace, size_t ws_bytes, void *stream,
+                         tgl_tcsr **out /* host */);
+
+/*
+ * A rank of the node-sharded sampler: its range's T-CSR handle (node base = splits[rank], e.g.
+ * from tgl_tcsr_build_range), the ranges of all ranks (splits: host int64 [world+1], splits[0] = 0,
+ * non-decreasing, splits[world] = V) and a transport, exactly one of:
+ *   nccl_id  host pointer to TGL_NCCL_ID_BYTES from tgl_shard_nccl_id() on one rank, broadcast to
+ *            the others by the caller (e.g. torch.distributed): the library creates an NCCL
+ *            communicator of `world` ranks (one process per GPU, the current device);
+ *   group    an in-process group (tgl_shard_group_create): ranks are threads of one process that
+ *            exchange by device copies -- for tests and single-device runs.
+ * Ownership: the shard borrows `local` (it must outlive the shard) and owns its communicator and
+ * its internal device buffers (grown by tgl_sample_sharded on first use, freed by
+ * tgl_shard_destroy).  Errors: TGL_EINVAL (bad splits, local range != splits[rank]..splits[rank+1],
+ * both or neither transport), TGL_ENCCL (NCCL missing or communicator creation failed).
+ */
+#define TGL_NCCL_ID_BYTES 128
+typedef struct tgl_shard tgl_shard;             /* opaque, host-side */
+typedef struct tgl_shard_group tgl_shard_group; /* opaque, host-side */
+TGL_API int tgl_shard_nccl_id(void *id /* host, TGL_NCCL_ID_BYTES */);
+TGL_API int tgl_shard_group_create(int32_t world, tgl_shard_group **out /* host */);
+TGL_API int tgl_shard_group_destroy(tgl_shard_group *group);
+TGL_API int tgl_shard_create(const tgl_tcsr *local, const int64_t *splits /* host [world+1] */, int32_t rank,
+                     int32_t world, const void *nccl_id /* host or NULL */, tgl_shard_group *group /* or NULL */,
+                     tgl_shard **out /* host */);
+TGL_API int tgl_shard_destroy(tgl_shard *shard);
+
+/*
+ * tgl_sample over a node-sharded T-CSR: a COLLECTIVE call -- every rank of the shard's group calls
+ * it (with its own roots, possibly none) with the same n_layers / fanouts / strategy / snapshots /
+ * seed.  The caller's blocks (capacities from tgl_sample_capacity, as for tgl_sample) receive
+ * exactly the bits tgl_sample writes on the full T-CSR for these roots with this root_key_base
+ * (R#7 keys travel with the requests, R#3 lower bounds too).  Per chain (layer 0 with its S blocks,
+ * then one per (layer, snapshot)): owner bucketing, an all-to-all of counts, the requests, local
+ * sampling on the owner's range, an all-to-all of reply sizes and the replies (grouped NCCL
+ * send / recv), un-permute -- two host synchronisations per chain (the sizes of the variable
+ * exchanges).  Stream-ordered on `stream`; the blocks' n_roots_dev / nnz_dev are written on the
+ * device.  Options of tgl_sample_ex (dedup, validity, hop-root time) are not supported here.
+ */
+TGL_API int tgl_sample_sharded(tgl_shard *shard, const int32_t *roots, const float *root_ts, int64_t n_roots,
+                       int32_t n_layers, const int32_t *fanouts /* host [L] */, tgl_strategy strategy,
+                       int32_t n_snapshots, float snapshot_len, uint64_t seed, uint64_t root_key_base,
+                       tgl_block *out /* host [L*S] */, void *stream);
+
+/* Cumulative exchange statistics of a shard: bytes sent to / received from OTHER ranks (the
+ * NVLink traffic of the protocol) and host synchronisations. */
+TGL_API int tgl_shard_stats(const tgl_shard *shard, int64_t *bytes_sent, int64_t *bytes_recv,
+                    int64_t *host_syncs);
 
 #ifdef __cplusplus
 }

@@ -26,7 +26,8 @@ from ._lib import MOST_RECENT, UNIFORM, TGLError
 _L = _lib.load()
 
 __all__ = ["TCSR", "Block", "Sampler", "build", "wrap", "aux_bytes", "sample", "gather", "check", "shard_bucket",
-           "set_node_base", "shard_unpermute", "offsets_to_counts", "block_digest",
+           "set_node_base", "shard_unpermute", "offsets_to_counts", "block_digest", "tcsr_indptr", "build_range",
+           "nccl_id", "ShardGroup", "ShardSampler",
            "MOST_RECENT", "UNIFORM", "TGLError", "lib_path"]
 
 lib_path = _lib.LIB_PATH
@@ -175,6 +176,34 @@ class Block:
         return self.offsets[: n + 1], self.nbr[:nnz], self.eid[:nnz], self.dt[:nnz], te
 
 
+def _alloc_blocks(dev, rc_, ec_, L: int, S: int, want_ts_edge_last: bool = False) -> List["Block"]:
+    """Device blocks (l, s) at index l*S + s with the capacities of tgl_sample_capacity."""
+    scal = torch.zeros(2 * L * S, dtype=torch.int64, device=dev)
+    blocks = []
+    for l in range(L):
+        for s in range(S):
+            need_ts = l < L - 1 or want_ts_edge_last
+            j = l * S + s
+            blocks.append(Block(
+                offsets=torch.empty(rc_[l] + 1, dtype=torch.int64, device=dev),
+                nbr=torch.empty(ec_[l], dtype=torch.int32, device=dev),
+                eid=torch.empty(ec_[l], dtype=torch.int32, device=dev),
+                dt=torch.empty(ec_[l], dtype=torch.float32, device=dev),
+                ts_edge=torch.empty(ec_[l], dtype=torch.float32, device=dev) if need_ts else None,
+                n_roots_dev=scal[2 * j: 2 * j + 1], nnz_dev=scal[2 * j + 1: 2 * j + 2]))
+    return blocks
+
+
+def _c_blocks(blocks, rc_, ec_, S: int):
+    arr = (_lib.Block * len(blocks))()
+    for j, b in enumerate(blocks):
+        l = j // S
+        arr[j] = _lib.Block(rc_[l], ec_[l], b.offsets.data_ptr(), b.nbr.data_ptr(), b.eid.data_ptr(),
+                            b.dt.data_ptr(), 0 if b.ts_edge is None else b.ts_edge.data_ptr(),
+                            b.n_roots_dev.data_ptr(), b.nnz_dev.data_ptr())
+    return arr
+
+
 class Sampler:
     """Preallocated outputs + workspace for repeated tgl_sample calls of up to max_roots roots."""
 
@@ -210,19 +239,7 @@ class Sampler:
         self.roots_cap, self.edges_cap = rc_, ec_
         self.workspace = torch.empty(max(wsb, 1), dtype=torch.uint8, device=dev)
         self.ws_bytes = wsb
-        scal = torch.zeros(2 * self.L * self.S, dtype=torch.int64, device=dev)
-        self.blocks: List[Block] = []
-        for l in range(self.L):
-            for s in range(self.S):
-                need_ts = l < self.L - 1 or want_ts_edge_last
-                j = l * self.S + s
-                self.blocks.append(Block(
-                    offsets=torch.empty(rc_[l] + 1, dtype=torch.int64, device=dev),
-                    nbr=torch.empty(ec_[l], dtype=torch.int32, device=dev),
-                    eid=torch.empty(ec_[l], dtype=torch.int32, device=dev),
-                    dt=torch.empty(ec_[l], dtype=torch.float32, device=dev),
-                    ts_edge=torch.empty(ec_[l], dtype=torch.float32, device=dev) if need_ts else None,
-                    n_roots_dev=scal[2 * j: 2 * j + 1], nnz_dev=scal[2 * j + 1: 2 * j + 2]))
+        self.blocks: List[Block] = _alloc_blocks(dev, rc_, ec_, self.L, self.S, want_ts_edge_last)
         self._c_dedup = None
         if dedup:
             uscal = torch.zeros(self.L * self.S, dtype=torch.int64, device=dev)
@@ -235,12 +252,7 @@ class Sampler:
                 b.n_uniq_dev = uscal[j:j + 1]
                 self._c_dedup[j] = _lib.DedupBlock(ec_[l], b.src_index.data_ptr(), b.uniq_node.data_ptr(),
                                                    b.uniq_ts.data_ptr(), b.n_uniq_dev.data_ptr())
-        self._c_blocks = (_lib.Block * len(self.blocks))()
-        for j, b in enumerate(self.blocks):
-            l = j // self.S
-            self._c_blocks[j] = _lib.Block(rc_[l], ec_[l], b.offsets.data_ptr(), b.nbr.data_ptr(), b.eid.data_ptr(),
-                                           b.dt.data_ptr(), 0 if b.ts_edge is None else b.ts_edge.data_ptr(),
-                                           b.n_roots_dev.data_ptr(), b.nnz_dev.data_ptr())
+        self._c_blocks = _c_blocks(self.blocks, rc_, ec_, self.S)
         self._fan = (ctypes.c_int32 * self.L)(*self.fanouts)
 
     def capacity(self, n_roots: int):
@@ -496,3 +508,131 @@ def shard_bucket(roots: torch.Tensor, splits: torch.Tensor, world: int, stream=N
     _rc(_L.tgl_shard_bucket(_ptr(roots), n, _ptr(splits), int(world), _ptr(perm), _ptr(counts), _ptr(ws),
                             wsb.value, _stream(stream)), "tgl_shard_bucket")
     return perm[:n], counts
+
+
+# ----------------------------------------------------------------------------- node-sharded mode
+def tcsr_indptr(src: torch.Tensor, dst: torch.Tensor, ts: torch.Tensor, *, n_nodes: int, add_reverse: bool,
+                stream=None) -> torch.Tensor:
+    """tgl_tcsr_indptr: the full graph's indptr only (validation + degree scan), e.g. to choose the
+    edge-balanced node ranges of the node-sharded mode."""
+    src = _cuda(src, torch.int32, "src")
+    dst = _cuda(dst, torch.int32, "dst")
+    ts = _cuda(ts, torch.float32, "ts")
+    indptr = torch.empty(n_nodes + 1, dtype=torch.int64, device=src.device)
+    b = ctypes.c_size_t()
+    _rc(_L.tgl_tcsr_indptr_workspace(src.numel(), int(n_nodes), ctypes.byref(b)), "tgl_tcsr_indptr_workspace")
+    ws = torch.empty(max(b.value, 1), dtype=torch.uint8, device=src.device)
+    _rc(_L.tgl_tcsr_indptr(_ptr(src), _ptr(dst), _ptr(ts), src.numel(), int(n_nodes), int(add_reverse), _ptr(indptr),
+                           _ptr(ws), b.value, _stream(stream)), "tgl_tcsr_indptr")
+    return indptr
+
+
+def build_range(src: torch.Tensor, dst: torch.Tensor, ts: torch.Tensor, eid: Optional[torch.Tensor] = None, *,
+                n_nodes: int, add_reverse: bool, node_lo: int, node_hi: int, n_local_stored: int,
+                with_index: bool = True, stream=None) -> TCSR:
+    """tgl_tcsr_build_range: the T-CSR of the nodes [node_lo, node_hi) only (node base = node_lo)."""
+    src = _cuda(src, torch.int32, "src")
+    dst = _cuda(dst, torch.int32, "dst")
+    ts = _cuda(ts, torch.float32, "ts")
+    if eid is not None:
+        eid = _cuda(eid, torch.int32, "eid")
+    dev = src.device
+    nl, es = int(node_hi) - int(node_lo), int(n_local_stored)
+    indptr = torch.empty(nl + 1, dtype=torch.int64, device=dev)
+    nbr = torch.empty(max(es, 1), dtype=torch.int32, device=dev)
+    ts_out, ts_storage = _ts_buffer(max(es, 1), dev)
+    eid_out = torch.empty(max(es, 1), dtype=torch.int32, device=dev)
+    ib = aux_bytes(es, nl) if with_index else 0
+    index = torch.empty(ib, dtype=torch.uint8, device=dev) if with_index else None
+    b = ctypes.c_size_t()
+    _rc(_L.tgl_tcsr_build_range_workspace(src.numel(), int(n_nodes), int(add_reverse), int(node_lo), int(node_hi), es,
+                                          ctypes.byref(b)), "tgl_tcsr_build_range_workspace")
+    ws = torch.empty(max(b.value, 1), dtype=torch.uint8, device=dev)
+    h = ctypes.c_void_p()
+    _rc(_L.tgl_tcsr_build_range(_ptr(src), _ptr(dst), _ptr(ts), _ptr(eid), src.numel(), int(n_nodes), int(add_reverse),
+                                int(node_lo), int(node_hi), es, _ptr(indptr), _ptr(nbr), _ptr(ts_storage),
+                                _ptr(eid_out), _ptr(index), ib, _ptr(ws), b.value, _stream(stream), ctypes.byref(h)),
+        "tgl_tcsr_build_range")
+    del ws
+    g = TCSR(indptr, nbr[:es], ts_out[:es], eid_out[:es], nl, h, index, ts_storage)
+    g.node_lo = int(node_lo)
+    return g
+
+
+def nccl_id() -> bytes:
+    """tgl_shard_nccl_id: a fresh NCCL unique id (call on one rank, broadcast to the others)."""
+    buf = (ctypes.c_char * _lib.NCCL_ID_BYTES)()
+    _rc(_L.tgl_shard_nccl_id(buf), "tgl_shard_nccl_id")
+    return bytes(buf)
+
+
+class ShardGroup:
+    """tgl_shard_group: an in-process group of ranks (threads of this process) for the node-sharded
+    sampler, exchanging by device copies (tests and single-device runs)."""
+
+    def __init__(self, world: int):
+        self.world = int(world)
+        h = ctypes.c_void_p()
+        _rc(_L.tgl_shard_group_create(self.world, ctypes.byref(h)), "tgl_shard_group_create")
+        self._h = h
+
+    def __del__(self):
+        h, self._h = getattr(self, "_h", None), None
+        if h and _L is not None:
+            _L.tgl_shard_group_destroy(h)
+
+
+class ShardSampler:
+    """One rank of the node-sharded sampler (tgl_shard_create + tgl_sample_sharded): `local` holds
+    the lists of nodes [splits[rank], splits[rank+1]) (tcsr with node base, e.g. build_range);
+    exactly one transport: `nccl_id` (bytes of nccl_id() shared by all ranks: NCCL, one process
+    per GPU) or `group` (ShardGroup: ranks on threads of this process).  run() is collective."""
+
+    def __init__(self, local: TCSR, splits: Sequence[int], rank: int, world: int, max_roots: int,
+                 fanouts: Sequence[int], strategy="most_recent", n_snapshots: int = 1,
+                 snapshot_len: float = math.inf, *, nccl_id: Optional[bytes] = None,
+                 group: Optional[ShardGroup] = None):
+        self.local, self.group = local, group
+        self.fanouts = [int(k) for k in fanouts]
+        self.L, self.S = len(self.fanouts), int(n_snapshots)
+        self.strategy = _strategy(strategy)
+        self.snapshot_len = float(snapshot_len)
+        self.max_roots = int(max_roots)
+        sp = (ctypes.c_int64 * (int(world) + 1))(*[int(x) for x in splits])
+        idb = None if nccl_id is None else ctypes.create_string_buffer(bytes(nccl_id), _lib.NCCL_ID_BYTES)
+        h = ctypes.c_void_p()
+        _rc(_L.tgl_shard_create(local.handle, sp, int(rank), int(world), idb,
+                                None if group is None else group._h, ctypes.byref(h)), "tgl_shard_create")
+        self._h = h
+        self._fan = (ctypes.c_int32 * self.L)(*self.fanouts)
+        rc_ = (ctypes.c_int64 * self.L)()
+        ec_ = (ctypes.c_int64 * self.L)()
+        wsb = ctypes.c_size_t()
+        _rc(_L.tgl_sample_capacity(self.max_roots, self.L, self._fan, self.S, self.strategy, self.snapshot_len, rc_, ec_,
+                                   ctypes.byref(wsb)), "tgl_sample_capacity")
+        self.roots_cap, self.edges_cap = list(rc_), list(ec_)
+        self.blocks = _alloc_blocks(local.nbr.device, self.roots_cap, self.edges_cap, self.L, self.S)
+        self._c_blocks = _c_blocks(self.blocks, self.roots_cap, self.edges_cap, self.S)
+
+    def run(self, roots: torch.Tensor, root_ts: torch.Tensor, *, seed: int = 0, root_key_base: int = 0,
+            stream=None) -> List[Block]:
+        roots = _cuda(roots, torch.int32, "roots")
+        root_ts = _cuda(root_ts, torch.float32, "root_ts")
+        n = roots.numel()
+        if n > self.max_roots or root_ts.numel() < n:
+            raise ValueError(f"{n} roots > max_roots {self.max_roots} or root_ts too short")
+        _rc(_L.tgl_sample_sharded(self._h, _ptr(roots), _ptr(root_ts), n, self.L, self._fan, self.strategy, self.S,
+                                  self.snapshot_len, int(seed) & 0xFFFFFFFFFFFFFFFF,
+                                  int(root_key_base) & 0xFFFFFFFFFFFFFFFF, self._c_blocks, _stream(stream)),
+            "tgl_sample_sharded")
+        return self.blocks
+
+    def stats(self):
+        a, b, c = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
+        _rc(_L.tgl_shard_stats(self._h, ctypes.byref(a), ctypes.byref(b), ctypes.byref(c)), "tgl_shard_stats")
+        return {"bytes_sent": a.value, "bytes_recv": b.value, "host_syncs": c.value}
+
+    def __del__(self):
+        h, self._h = getattr(self, "_h", None), None
+        if h and _L is not None:
+            _L.tgl_shard_destroy(h)

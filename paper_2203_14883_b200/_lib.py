@@ -14,6 +14,7 @@ LIB_PATH = os.environ.get("TGL_LIB_PATH") or os.path.join(_HERE, "libtgl.so")  #
 OK, EINVAL, ERANGE, EUNSORTED, ECAPACITY, EWORKSPACE, ECUDA, ENCCL, ENOTSUP = 0, -1, -2, -3, -4, -5, -6, -7, -8
 MOST_RECENT, UNIFORM = 0, 1
 MAX_SNAPSHOTS, MAX_FANOUT, MAX_GATHER_TABLES = 16, 1024, 8
+NCCL_ID_BYTES = 128
 
 P = ctypes.c_void_p
 i32, i64, u64, f32, sz = ctypes.c_int32, ctypes.c_int64, ctypes.c_uint64, ctypes.c_float, ctypes.c_size_t
@@ -73,6 +74,18 @@ SIGNATURES = {
     "tgl_state_write": (ctypes.c_int, [P, P, i64, i32, i32, P, P, P, i32, P, sz, P]),
     "tgl_check": (ctypes.c_int, [P, P]),
     "tgl_block_digest": (ctypes.c_int, [P, P, P, P, P, i64, P, P]),
+    "tgl_tcsr_indptr_workspace": (ctypes.c_int, [i64, i32, ctypes.POINTER(sz)]),
+    "tgl_tcsr_indptr": (ctypes.c_int, [P, P, P, i64, i32, ctypes.c_int, P, P, sz, P]),
+    "tgl_tcsr_build_range_workspace": (ctypes.c_int, [i64, i32, ctypes.c_int, i32, i32, i64, ctypes.POINTER(sz)]),
+    "tgl_tcsr_build_range": (ctypes.c_int, [P, P, P, P, i64, i32, ctypes.c_int, i32, i32, i64, P, P, P, P, P, sz, P,
+                                            sz, P, ctypes.POINTER(P)]),
+    "tgl_shard_nccl_id": (ctypes.c_int, [P]),
+    "tgl_shard_group_create": (ctypes.c_int, [i32, ctypes.POINTER(P)]),
+    "tgl_shard_group_destroy": (ctypes.c_int, [P]),
+    "tgl_shard_create": (ctypes.c_int, [P, P, i32, i32, P, P, ctypes.POINTER(P)]),
+    "tgl_shard_destroy": (ctypes.c_int, [P]),
+    "tgl_sample_sharded": (ctypes.c_int, [P, P, P, i64, i32, P, ctypes.c_int, i32, f32, u64, u64, P, P]),
+    "tgl_shard_stats": (ctypes.c_int, [P, ctypes.POINTER(i64), ctypes.POINTER(i64), ctypes.POINTER(i64)]),
     "tgl_shard_bucket_workspace": (ctypes.c_int, [i64, i32, ctypes.POINTER(sz)]),
     "tgl_shard_bucket": (ctypes.c_int, [P, i64, P, i32, P, P, P, sz, P]),
 }

@@ -27,8 +27,9 @@ namespace tgl {
 __global__ void __launch_bounds__(256) validate_hist_kernel(const int32_t* __restrict__ src,
                                                             const int32_t* __restrict__ dst,
                                                             const float* __restrict__ ts, int64_t n,
-                                                            int32_t n_nodes, int add_reverse,
-                                                            uint32_t* __restrict__ deg, int* __restrict__ err) {
+                                                            int32_t n_nodes, int add_reverse, int32_t node_lo,
+                                                            int32_t node_hi, uint32_t* __restrict__ deg,
+                                                            int* __restrict__ err) {
     int bits = 0;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i - threadIdx.x % 32 < n; i += stride) {
@@ -42,18 +43,19 @@ __global__ void __launch_bounds__(256) validate_hist_kernel(const int32_t* __res
             if (i > 0 && ts[i - 1] > t) bits |= kErrUnsorted;
             if ((uint32_t)s >= (uint32_t)n_nodes || (uint32_t)d >= (uint32_t)n_nodes) bits |= kErrRange;
         }
-        const bool ok_s = live && (uint32_t)s < (uint32_t)n_nodes;
-        const bool ok_d = live && add_reverse && (uint32_t)d < (uint32_t)n_nodes;
+        // owners counted: those in [node_lo, node_hi) (the whole graph, or one node-sharded range)
+        const bool ok_s = live && s >= node_lo && s < node_hi;
+        const bool ok_d = live && add_reverse && d >= node_lo && d < node_hi;
         // warp-aggregated histogram: one atomic per distinct owner in the warp
         {
             const int key = ok_s ? s : -1;
             const uint32_t peers = __match_any_sync(kFull, key);
-            if (ok_s && (__ffs(peers) - 1) == (int)(threadIdx.x & 31)) atomicAdd(&deg[s], __popc(peers));
+            if (ok_s && (__ffs(peers) - 1) == (int)(threadIdx.x & 31)) atomicAdd(&deg[s - node_lo], __popc(peers));
         }
         if (add_reverse) {
             const int key = ok_d ? d : -1;
             const uint32_t peers = __match_any_sync(kFull, key);
-            if (ok_d && (__ffs(peers) - 1) == (int)(threadIdx.x & 31)) atomicAdd(&deg[d], __popc(peers));
+            if (ok_d && (__ffs(peers) - 1) == (int)(threadIdx.x & 31)) atomicAdd(&deg[d - node_lo], __popc(peers));
         }
     }
     bits = __reduce_or_sync(kFull, bits);
@@ -191,8 +193,8 @@ extern "C" int tgl_tcsr_build(const int32_t* src, const int32_t* dst, const floa
         return TGL_ECUDA;
     if (n_edges > 0) {
         int64_t blocks = std::min<int64_t>((n_edges + 255) / 256, 148 * 16);
-        validate_hist_kernel<<<(unsigned)blocks, 256, 0, st>>>(src, dst, ts, n_edges, n_nodes, add_reverse, p.deg,
-                                                                p.err);
+        validate_hist_kernel<<<(unsigned)blocks, 256, 0, st>>>(src, dst, ts, n_edges, n_nodes, add_reverse, 0,
+                                                                n_nodes, p.deg, p.err);
         if (cudaGetLastError() != cudaSuccess) return TGL_ECUDA;
     }
     int herr = 0;
@@ -247,6 +249,211 @@ extern "C" int tgl_tcsr_build(const int32_t* src, const int32_t* dst, const floa
         if (rc) return rc;
     }
     return tgl_tcsr_wrap(indptr, nbr, ts_out, eid_out, aux, aux_bytes, n_nodes, (int64_t)es, out);
+}
+
+// ---------------------------------------------------------------------------- node-range build
+// Node-sharded T-CSR: a rank builds only the lists of its node range [lo, hi), so its
+// T-CSR memory is ~E_s / world.  Same method as tgl_tcsr_build, restricted to the
+// logical edges whose owner is in the range: K1 (validation of the whole stream + the range's
+// degree histogram), K2 (scan -> the local indptr), then the logical edges of the range are
+// compacted in stream order (flag -> scan -> scatter of (owner - lo, j)) and sorted by the same
+// stable LSD passes, so every list is exactly the full build's list of that node.
+namespace tgl {
+
+__global__ void range_flag_kernel(Stream s, uint64_t n, int32_t lo, int32_t hi, uint32_t* __restrict__ flag) {
+    for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (uint64_t)gridDim.x * blockDim.x) {
+        const int32_t o = (int32_t)owner_of(s, j);
+        flag[j] = o >= lo && o < hi ? 1u : 0u;
+    }
+}
+
+__global__ void range_compact_kernel(Stream s, uint64_t n, int32_t lo, const uint32_t* __restrict__ flag,
+                                     const uint32_t* __restrict__ pos, uint32_t* __restrict__ keys,
+                                     uint32_t* __restrict__ vals) {
+    for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (uint64_t)gridDim.x * blockDim.x)
+        if (flag[j]) {
+            keys[pos[j]] = owner_of(s, j) - (uint32_t)lo;
+            vals[pos[j]] = (uint32_t)j;
+        }
+}
+
+struct RangePlan {
+    uint64_t n_logical = 0, n_local = 0;
+    int bits = 0, passes = 1;
+    uint64_t ntiles = 0;
+    int* err = nullptr;
+    uint32_t* deg = nullptr;
+    uint32_t* flag = nullptr;  // [n_logical], then reused as the compaction positions
+    uint32_t* pos = nullptr;
+    uint64_t* partial = nullptr;
+    uint32_t* counts = nullptr;
+    uint32_t* kbuf[2] = {nullptr, nullptr};
+    uint32_t* vbuf[2] = {nullptr, nullptr};
+    size_t bytes = 0;
+};
+
+static RangePlan plan_range(int64_t n_edges, int32_t n_local_nodes, int64_t n_local, int add_reverse, void* ws) {
+    RangePlan p;
+    p.n_logical = (uint64_t)n_edges * (add_reverse ? 2 : 1);
+    p.n_local = (uint64_t)n_local;
+    p.bits = n_local_nodes <= 1 ? 0 : 32 - __builtin_clz((unsigned)(n_local_nodes - 1));
+    p.passes = p.bits <= 8 ? 1 : (p.bits + 7) / 8;
+    p.ntiles = (p.n_local + kRadixTile - 1) / kRadixTile;
+    Carve c(ws);
+    p.err = c.take<int>(64);
+    p.deg = c.take<uint32_t>((size_t)std::max(n_local_nodes, 1));
+    p.flag = c.take<uint32_t>((size_t)std::max<uint64_t>(p.n_logical, 1));
+    p.pos = c.take<uint32_t>((size_t)std::max<uint64_t>(p.n_logical, 1));
+    const int64_t scan_n = std::max<int64_t>(std::max<int64_t>(n_local_nodes, (int64_t)p.n_logical),
+                                             (int64_t)(kRadixBins * p.ntiles));
+    p.partial = c.take<uint64_t>(scan_workspace_bytes(scan_n) / sizeof(uint64_t));
+    p.counts = c.take<uint32_t>((size_t)kRadixBins * (p.ntiles ? p.ntiles : 1));
+    for (int b = 0; b < 2; ++b) {
+        p.kbuf[b] = c.take<uint32_t>((size_t)std::max<uint64_t>(p.n_local, 1));
+        p.vbuf[b] = c.take<uint32_t>((size_t)std::max<uint64_t>(p.n_local, 1));
+    }
+    p.bytes = c.bytes();
+    return p;
+}
+
+}  // namespace tgl
+
+extern "C" int tgl_tcsr_build_range_workspace(int64_t n_edges, int32_t n_nodes, int add_reverse, int32_t node_lo,
+                                              int32_t node_hi, int64_t n_local_stored, size_t* bytes) {
+    if (!bytes || n_edges < 0 || n_nodes < 0 || node_lo < 0 || node_hi < node_lo || node_hi > n_nodes ||
+        n_local_stored < 0)
+        return TGL_EINVAL;
+    if ((uint64_t)n_edges * (add_reverse ? 2 : 1) >= (1ull << 32)) return TGL_EINVAL;
+    *bytes = plan_range(n_edges, node_hi - node_lo, n_local_stored, add_reverse ? 1 : 0, nullptr).bytes;
+    return TGL_OK;
+}
+
+extern "C" int tgl_tcsr_build_range(const int32_t* src, const int32_t* dst, const float* ts, const int32_t* eid,
+                                    int64_t n_edges, int32_t n_nodes, int add_reverse, int32_t node_lo, int32_t node_hi,
+                                    int64_t n_local_stored, int64_t* indptr, int32_t* nbr, float* ts_out,
+                                    int32_t* eid_out, void* aux, size_t aux_bytes, void* workspace, size_t ws_bytes,
+                                    void* stream, tgl_tcsr** out) {
+    if (!out || !indptr || n_edges < 0 || n_nodes < 0 || node_lo < 0 || node_hi < node_lo || node_hi > n_nodes ||
+        n_local_stored < 0)
+        return TGL_EINVAL;
+    *out = nullptr;
+    add_reverse = add_reverse ? 1 : 0;
+    const uint64_t es = (uint64_t)n_edges * (add_reverse ? 2 : 1);
+    if (es >= (1ull << 32)) return TGL_EINVAL;
+    if (n_edges > 0 && (!src || !dst || !ts)) return TGL_EINVAL;
+    if (n_local_stored > 0 && (!nbr || !ts_out || !eid_out)) return TGL_EINVAL;
+    if (!workspace) return TGL_EINVAL;
+    int rc = check_device();
+    if (rc) return rc;
+    const int32_t nl = node_hi - node_lo;
+    RangePlan p = plan_range(n_edges, nl, n_local_stored, add_reverse, workspace);
+    if (ws_bytes < p.bytes) return TGL_EWORKSPACE;
+    cudaStream_t st = (cudaStream_t)stream;
+
+    // K1 over the whole stream (validation) with the range's histogram; K2 -> the local indptr
+    if (cudaMemsetAsync(p.err, 0, sizeof(int), st) != cudaSuccess) return TGL_ECUDA;
+    if (nl > 0 && cudaMemsetAsync(p.deg, 0, sizeof(uint32_t) * (size_t)nl, st) != cudaSuccess) return TGL_ECUDA;
+    if (n_edges > 0) {
+        const int64_t blocks = std::min<int64_t>((n_edges + 255) / 256, 148 * 16);
+        validate_hist_kernel<<<(unsigned)blocks, 256, 0, st>>>(src, dst, ts, n_edges, n_nodes, add_reverse, node_lo,
+                                                                node_hi, p.deg, p.err);
+        if (cudaGetLastError() != cudaSuccess) return TGL_ECUDA;
+    }
+    if (cuda_rc(exclusive_scan<uint32_t, int64_t>(p.deg, indptr, nl, indptr + nl, p.partial, st))) return TGL_ECUDA;
+    int herr = 0;
+    int64_t total = 0;
+    if (cudaMemcpyAsync(&herr, p.err, sizeof(int), cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+        cudaMemcpyAsync(&total, indptr + nl, sizeof(int64_t), cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+        cudaStreamSynchronize(st) != cudaSuccess)
+        return TGL_ECUDA;
+    if (herr) return err_bits_to_code(herr);
+    if (total != n_local_stored) return TGL_ECAPACITY;  // the caller's E_s of the range is wrong
+
+    // the range's logical edges in stream order, then the stable passes by (owner - lo)
+    if (p.n_local > 0) {
+        Stream s{src, dst, ts, eid, add_reverse};
+        const uint64_t n = p.n_logical;
+        const unsigned blocks = (unsigned)std::min<uint64_t>((n + 255) / 256, 148 * 16);
+        range_flag_kernel<<<blocks, 256, 0, st>>>(s, n, node_lo, node_hi, p.flag);
+        if (cuda_rc(exclusive_scan<uint32_t, uint32_t>(p.flag, p.pos, (int64_t)n, (uint32_t*)nullptr, p.partial, st)))
+            return TGL_ECUDA;
+        range_compact_kernel<<<blocks, 256, 0, st>>>(s, n, node_lo, p.flag, p.pos, p.kbuf[1], p.vbuf[1]);
+        const uint64_t m = p.n_local;
+        const unsigned grid = (unsigned)p.ntiles;
+        for (int pass = 0; pass < p.passes; ++pass) {
+            const int shift = 8 * pass;
+            const int nb = std::min(8, std::max(0, p.bits - shift));
+            const uint32_t mask = nb >= 32 ? 0xffffffffu : ((1u << nb) - 1u);
+            const bool last = pass == p.passes - 1;
+            const uint32_t* kin = p.kbuf[(pass + 1) & 1];
+            const uint32_t* vin = p.vbuf[(pass + 1) & 1];
+            uint32_t* kout = last ? nullptr : p.kbuf[pass & 1];
+            uint32_t* vout = last ? nullptr : p.vbuf[pass & 1];
+            radix_upsweep_kernel<kSrcKV><<<grid, kRadixThreads, 0, st>>>(s, kin, m, shift, mask, p.counts, p.ntiles);
+            if (cuda_rc(exclusive_scan<uint32_t, uint32_t>(p.counts, p.counts, (int64_t)kRadixBins * p.ntiles,
+                                                           (uint32_t*)nullptr, p.partial, st)))
+                return TGL_ECUDA;
+            if (last)
+                radix_downsweep_kernel<kSrcKV, kDstTCSR><<<grid, kRadixThreads, 0, st>>>(
+                    s, kin, vin, m, shift, mask, p.counts, p.ntiles, kout, vout, nbr, ts_out, eid_out, nullptr);
+            else
+                radix_downsweep_kernel<kSrcKV, kDstKV><<<grid, kRadixThreads, 0, st>>>(
+                    s, kin, vin, m, shift, mask, p.counts, p.ntiles, kout, vout, nbr, ts_out, eid_out, nullptr);
+            if (cudaGetLastError() != cudaSuccess) return TGL_ECUDA;
+        }
+    }
+    if (aux) {
+        rc = tgl_tcsr_aux_build(indptr, ts_out, nbr, eid_out, nl, n_local_stored, aux, aux_bytes, stream);
+        if (rc) return rc;
+    }
+    rc = tgl_tcsr_wrap(indptr, nbr, ts_out, eid_out, aux, aux_bytes, nl, n_local_stored, out);
+    if (rc) return rc;
+    return tgl_tcsr_set_node_base(*out, node_lo);
+}
+
+// the global indptr alone (K1 + K2: validation and the degree scan), e.g. to choose the
+// edge-balanced node ranges of the node-sharded mode before every rank builds its own range
+extern "C" int tgl_tcsr_indptr_workspace(int64_t n_edges, int32_t n_nodes, size_t* bytes) {
+    if (!bytes || n_edges < 0 || n_nodes < 0) return TGL_EINVAL;
+    Carve c(nullptr);
+    c.take<int>(64);
+    c.take<uint32_t>((size_t)std::max(n_nodes, 1));
+    c.take<uint64_t>(scan_workspace_bytes(n_nodes) / sizeof(uint64_t));
+    *bytes = c.bytes();
+    return TGL_OK;
+}
+
+extern "C" int tgl_tcsr_indptr(const int32_t* src, const int32_t* dst, const float* ts, int64_t n_edges,
+                               int32_t n_nodes, int add_reverse, int64_t* indptr, void* workspace, size_t ws_bytes,
+                               void* stream) {
+    if (!indptr || n_edges < 0 || n_nodes < 0 || !workspace) return TGL_EINVAL;
+    if (n_edges > 0 && (!src || !dst || !ts)) return TGL_EINVAL;
+    if ((uint64_t)n_edges * (add_reverse ? 2 : 1) >= (1ull << 32)) return TGL_EINVAL;
+    size_t need = 0;
+    tgl_tcsr_indptr_workspace(n_edges, n_nodes, &need);
+    if (ws_bytes < need) return TGL_EWORKSPACE;
+    int rc = check_device();
+    if (rc) return rc;
+    Carve c(workspace);
+    int* err = c.take<int>(64);
+    uint32_t* deg = c.take<uint32_t>((size_t)std::max(n_nodes, 1));
+    uint64_t* partial = c.take<uint64_t>(scan_workspace_bytes(n_nodes) / sizeof(uint64_t));
+    cudaStream_t st = (cudaStream_t)stream;
+    if (cudaMemsetAsync(err, 0, sizeof(int), st) != cudaSuccess) return TGL_ECUDA;
+    if (n_nodes > 0 && cudaMemsetAsync(deg, 0, sizeof(uint32_t) * (size_t)n_nodes, st) != cudaSuccess) return TGL_ECUDA;
+    if (n_edges > 0) {
+        const int64_t blocks = std::min<int64_t>((n_edges + 255) / 256, 148 * 16);
+        validate_hist_kernel<<<(unsigned)blocks, 256, 0, st>>>(src, dst, ts, n_edges, n_nodes, add_reverse ? 1 : 0, 0,
+                                                                n_nodes, deg, err);
+        if (cudaGetLastError() != cudaSuccess) return TGL_ECUDA;
+    }
+    if (cuda_rc(exclusive_scan<uint32_t, int64_t>(deg, indptr, n_nodes, indptr + n_nodes, partial, st)))
+        return TGL_ECUDA;
+    int herr = 0;
+    if (cudaMemcpyAsync(&herr, err, sizeof(int), cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+        cudaStreamSynchronize(st) != cudaSuccess)
+        return TGL_ECUDA;
+    return err_bits_to_code(herr);
 }
 
 // ---------------------------------------------------------------------------- K8 shard bucketing

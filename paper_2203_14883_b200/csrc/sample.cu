@@ -32,6 +32,7 @@
 #include <cstdlib>
 #include <cstring>
 
+#include "chain.cuh"
 #include "common.cuh"
 #include "scan.cuh"
 #include "tsindex.cuh"
@@ -64,6 +65,10 @@ constexpr int kSuperShift = 6;  // 64 tiles per super tile (tile bases: super to
 #define TGL_INDEX_MIN 4096  // C4 A/B: 256 73.9, 1024 74.5, 4096 75.3 G edges/s; C5 unchanged
 #endif
 constexpr uint32_t kIndexMin = TGL_INDEX_MIN;  // gaps longer than this descend the 16-ary index
+#ifndef TGL_REC_HALVES
+#define TGL_REC_HALVES 1
+#endif
+constexpr int kRecHalves = TGL_REC_HALVES;  // node records parked in shared memory in 1 or 2 rounds
 constexpr int kPicksSmemPerWarp = 8 * 1024;  // bytes of uniform picks kept in shared memory per warp
 
 struct BlockOut {
@@ -286,7 +291,7 @@ __device__ __forceinline__ uint32_t select_valid(const SampleParams& p, int64_t 
 template <int STRATEGY, bool VALID>
 __global__ void __launch_bounds__(kTile, VALID ? 6 : TGL_WINDOW_MINB) window_kernel(const __grid_constant__ SampleParams p) {
     __shared__ uint32_t s_red[TGL_MAX_SNAPSHOTS][kWarps];
-    __shared__ int4 s_rec[kTile * 4];  // the tile's 64-byte node records (16 KB)
+    __shared__ int4 s_rec[kTile * 4 / kRecHalves];  // the tile's 64-byte node records (16 KB / halves)
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int64_t n = chain_roots(p);
     const int64_t tile = (int64_t)blockIdx.x;
@@ -338,7 +343,7 @@ __global__ void __launch_bounds__(kTile, VALID ? 6 : TGL_WINDOW_MINB) window_ker
         // at chunk slot c ^ ((r >> 1) & 3): the 8 lanes of a quarter-warp then read 8 distinct
         // bank groups); then every lane counts its own root's 14 fences below each cut time with a
         // branch-free binary search over the record (fences are sorted)
-        int4* wrec = s_rec + warp * 32 * 4;
+        int4* wrec = s_rec + warp * (32 / kRecHalves) * 4;
         const int quad = lane >> 2, part = lane & 3;
         int4 ch[4];
 #pragma unroll
@@ -349,29 +354,35 @@ __global__ void __launch_bounds__(kTile, VALID ? 6 : TGL_WINDOW_MINB) window_ker
             ch[q] = okq ? __ldg(p.nodes + (size_t)vq * 4 + part)
                         : make_int4(part ? 0x7f800000 : 0, part ? 0x7f800000 : 0, 0x7f800000, 0x7f800000);
         }
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            const int src = q * 8 + quad;
-            wrec[src * 4 + (part ^ ((src >> 1) & 3))] = ch[q];
-        }
-        __syncwarp();
-        const int sw = (lane >> 1) & 3;
-        const float* rec = reinterpret_cast<const float*>(wrec + lane * 4);
-        auto word = [&](int w) { return rec[(((w >> 2) ^ sw) << 2) | (w & 3)]; };  // record word w
-        lo = __float_as_uint(word(0));
-        hi = __float_as_uint(word(1));
         uint32_t packed = 0;
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            // number of fences f[0..13] (= words 2..15) below x[j]; positions >= 14 act as +inf
-            int c = 0;
+        for (int h = 0; h < kRecHalves; ++h) {  // kRecHalves = 2: roots 0-15, then 16-31 (8 KB per CTA)
+            if (h) __syncwarp();
 #pragma unroll
-            for (int step = 8; step >= 1; step >>= 1) {
-                const int e = c + step - 1;
-                const bool below = e < kFences && word(2 + min(e, kFences - 1)) < x[j];
-                c += below ? step : 0;
+            for (int q = h * 4 / kRecHalves; q < (h + 1) * 4 / kRecHalves; ++q) {
+                const int src = q * 8 + quad;
+                wrec[(src % (32 / kRecHalves)) * 4 + (part ^ ((src >> 1) & 3))] = ch[q];
             }
-            packed |= (uint32_t)c << (8 * j);
+            __syncwarp();
+            if (lane / (32 / kRecHalves) == h) {
+                const int sw = (lane >> 1) & 3;
+                const float* rec = reinterpret_cast<const float*>(wrec + (lane % (32 / kRecHalves)) * 4);
+                auto word = [&](int w) { return rec[(((w >> 2) ^ sw) << 2) | (w & 3)]; };  // record word w
+                lo = __float_as_uint(word(0));
+                hi = __float_as_uint(word(1));
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    // number of fences f[0..13] (= words 2..15) below x[j]; positions >= 14 act as +inf
+                    int c = 0;
+#pragma unroll
+                    for (int step = 8; step >= 1; step >>= 1) {
+                        const int e = c + step - 1;
+                        const bool below = e < kFences && word(2 + min(e, kFences - 1)) < x[j];
+                        c += below ? step : 0;
+                    }
+                    packed |= (uint32_t)c << (8 * j);
+                }
+            }
         }
         const uint32_t d = hi - lo;
 #pragma unroll
@@ -977,6 +988,100 @@ static ForkStreams* fork_streams(int S) {
                            cudaEventCreateWithFlags(&f.join[s], cudaEventDisableTiming) != cudaSuccess))
             return nullptr;
     return &f;
+}
+
+// ---------------------------------------------------------------------------- one chain, explicit roots
+// The owner side of the node-sharded exchange (sharded.cu): one chain -- layer `layer`, all nsb
+// snapshot blocks of a layer-0 root (snap0 = 0) or snapshot snap0's block at l >= 1 -- over roots
+// received from other ranks, each with its explicit key (R#7) and, at l >= 1, its inherited lower
+// bound (R#3): the same two kernels and the same Philox counters as tgl_sample, so the blocks are
+// those the replicated mode writes for these roots.
+static Launch plan_chain(int64_t n, int nsb, int k, int strategy, void* ws, size_t* bytes) {
+    Carve c(ws);
+    Launch la;
+    memset(&la, 0, sizeof(la));
+    la.nsb = nsb;
+    la.roots_cap = std::max<int64_t>(1, n);
+    la.tiles_cap = (la.roots_cap + kTile - 1) / kTile;
+    la.cuts = c.take<uint32_t>((size_t)(nsb + 1) * la.roots_cap);
+    la.tile_tot = c.take<uint32_t>((size_t)nsb * la.tiles_cap);
+    la.supers_cap = (la.tiles_cap + (1 << kSuperShift) - 1) >> kSuperShift;
+    la.hypers_cap = (la.supers_cap + (1 << kSuperShift) - 1) >> kSuperShift;
+    if (strategy == TGL_UNIFORM && !picks_fit_smem(nsb, k))
+        la.picks = c.take<uint32_t>((size_t)la.tiles_cap * kTile * nsb * k);
+    la.super_tot = c.take<uint64_t>((size_t)nsb * la.supers_cap);
+    la.hyper_tot = c.take<uint64_t>((size_t)nsb * la.hypers_cap);
+    if (bytes) *bytes = c.bytes();
+    return la;
+}
+
+size_t chain_workspace_bytes(int64_t n, int nsb, int k, int strategy) {
+    size_t b = 0;
+    plan_chain(n, nsb, k, strategy, nullptr, &b);
+    return b;
+}
+
+int sample_chain(const tgl_tcsr* g, int layer, int snap0, int nsb, const int32_t* rn, const float* rt,
+                 const uint64_t* rk, const float* rlo, int64_t n, int k, int strategy, float t_s, uint64_t seed,
+                 const ChainOut* outs, void* ws, size_t ws_bytes, cudaStream_t st) {
+    if (nsb < 1 || nsb > TGL_MAX_SNAPSHOTS || k < 1 || k > TGL_MAX_FANOUT || n < 0 || !ws) return TGL_EINVAL;
+    size_t need = 0;
+    const Launch la = plan_chain(n, nsb, k, strategy, ws, &need);
+    if (ws_bytes < need) return TGL_EWORKSPACE;
+    if (la.tiles_cap > (1 << kSuperShift) &&
+        cudaMemsetAsync(la.super_tot, 0,
+                        (size_t)(reinterpret_cast<char*>(la.hyper_tot + (size_t)nsb * la.hypers_cap) -
+                                 reinterpret_cast<char*>(la.super_tot)),
+                        st) != cudaSuccess)
+        return TGL_ECUDA;
+    SampleParams sp;
+    memset(&sp, 0, sizeof(sp));
+    sp.indptr = g->indptr;
+    sp.nbr = g->nbr;
+    sp.ts = g->ts;
+    sp.eid = g->eid;
+    sp.recs = static_cast<const SlotRec*>(g->recs);
+    sp.nodes = static_cast<const int4*>(g->nodes);
+    sp.n_levels = g->index ? g->n_levels : 0;
+    for (int q = 1; q <= sp.n_levels; ++q) sp.lvl[q] = g->index + g->level_off[q];
+    sp.n_nodes = g->n_nodes;
+    sp.node_lo = g->node_lo;
+    sp.root_node = rn;
+    sp.root_ts = rt;
+    sp.root_key = rk;
+    sp.root_lo = layer > 0 ? rlo : nullptr;
+    sp.n_roots = n;
+    sp.layer = layer;
+    sp.nsb = nsb;
+    sp.snap0 = snap0;
+    sp.k = k;
+    sp.snapshot_len = t_s;
+    sp.seed_lo = (uint32_t)seed;
+    sp.seed_hi = (uint32_t)(seed >> 32);
+    sp.cuts = la.cuts;
+    sp.tile_tot = la.tile_tot;
+    sp.super_tot = la.super_tot;
+    sp.supers_cap = la.supers_cap;
+    sp.hyper_tot = la.hyper_tot;
+    sp.hypers_cap = la.hypers_cap;
+    sp.roots_cap = la.roots_cap;
+    sp.tiles_cap = la.tiles_cap;
+    sp.picks_global = la.picks;
+    sp.err = g->err_dev;
+    for (int b = 0; b < nsb; ++b) {
+        BlockOut& bo = sp.out[b];
+        bo.offsets = outs[b].offsets;
+        bo.nbr = outs[b].nbr;
+        bo.eid = outs[b].eid;
+        bo.dt = outs[b].dt;
+        bo.ts_edge = outs[b].ts_edge;
+        bo.n_roots_dev = outs[b].n_roots_dev;
+        bo.nnz_dev = outs[b].nnz_dev;
+    }
+    const int64_t tiles = std::max<int64_t>(1, (n + kTile - 1) / kTile);
+    const size_t smem = (size_t)kWarps * copy_warp_words(nsb, k, strategy == TGL_UNIFORM && la.picks == nullptr) * 4;
+    return strategy == TGL_UNIFORM ? launch_chain<TGL_UNIFORM>(sp, tiles, smem, st)
+                                   : launch_chain<TGL_MOST_RECENT>(sp, tiles, smem, st);
 }
 
 }  // namespace tgl

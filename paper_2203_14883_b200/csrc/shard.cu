@@ -6,6 +6,7 @@
 // have produced (original root order): counts scatter -> exclusive scan -> segmented copy.
 #include <algorithm>
 
+#include "chain.cuh"
 #include "common.cuh"
 #include "scan.cuh"
 
@@ -29,7 +30,8 @@ __global__ void __launch_bounds__(256) unpermute_copy_kernel(const int32_t* __re
                                                              const int32_t* __restrict__ nbr_in,
                                                              const int32_t* __restrict__ eid_in,
                                                              const float* __restrict__ dt_in, int32_t* __restrict__ nbr_out,
-                                                             int32_t* __restrict__ eid_out, float* __restrict__ dt_out) {
+                                                             int32_t* __restrict__ eid_out, float* __restrict__ dt_out,
+                                                             const float* __restrict__ ts_in, float* __restrict__ ts_out) {
     __shared__ int64_t s_in[8][33];
     __shared__ int64_t s_dst[8][32];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -51,6 +53,7 @@ __global__ void __launch_bounds__(256) unpermute_copy_kernel(const int32_t* __re
         nbr_out[d] = nbr_in[o];
         eid_out[d] = eid_in[o];
         dt_out[d] = dt_in[o];
+        if (ts_out) ts_out[d] = ts_in[o];
     }
 }
 
@@ -91,17 +94,15 @@ extern "C" int tgl_offsets_to_counts(const int64_t* offsets, int64_t n_roots, in
     return cudaGetLastError() == cudaSuccess ? TGL_OK : TGL_ECUDA;
 }
 
-extern "C" int tgl_shard_unpermute(const int32_t* perm, int64_t n_roots, const int32_t* counts_in,
-                                   const int32_t* nbr_in, const int32_t* eid_in, const float* dt_in,
-                                   int64_t* offsets_out, int32_t* nbr_out, int32_t* eid_out, float* dt_out,
-                                   void* workspace, size_t ws_bytes, void* stream) {
-    if (n_roots < 0 || n_roots >= (int64_t(1) << 31) || !offsets_out || !workspace) return TGL_EINVAL;
-    if (n_roots > 0 && (!perm || !counts_in)) return TGL_EINVAL;
-    int rc = check_device();
-    if (rc) return rc;
+namespace tgl {
+size_t unpermute_workspace_bytes(int64_t n) { return plan_unperm(n, nullptr).bytes; }
+
+int unpermute_block(const int32_t* perm, int64_t n_roots, const int32_t* counts_in, const int32_t* nbr_in,
+                    const int32_t* eid_in, const float* dt_in, const float* ts_in, int64_t* offsets_out,
+                    int32_t* nbr_out, int32_t* eid_out, float* dt_out, float* ts_out, void* workspace,
+                    size_t ws_bytes, cudaStream_t st) {
     UnpermPlan p = plan_unperm(n_roots, workspace);
     if (ws_bytes < p.bytes) return TGL_EWORKSPACE;
-    cudaStream_t st = (cudaStream_t)stream;
     if (n_roots == 0) return cuda_rc(cudaMemsetAsync(offsets_out, 0, sizeof(int64_t), st));
     const int64_t blocks = std::min<int64_t>((n_roots + 255) / 256, 148 * 8);
     // bucket-order offsets of the received block, then original-order counts and offsets
@@ -112,8 +113,21 @@ extern "C" int tgl_shard_unpermute(const int32_t* perm, int64_t n_roots, const i
         return TGL_ECUDA;
     const int64_t grid = (n_roots + 255) / 256;
     unpermute_copy_kernel<<<(unsigned)grid, 256, 0, st>>>(perm, n_roots, p.off_in, offsets_out, nbr_in, eid_in, dt_in,
-                                                          nbr_out, eid_out, dt_out);
+                                                          nbr_out, eid_out, dt_out, ts_out ? ts_in : nullptr, ts_out);
     return cudaGetLastError() == cudaSuccess ? TGL_OK : TGL_ECUDA;
+}
+}  // namespace tgl
+
+extern "C" int tgl_shard_unpermute(const int32_t* perm, int64_t n_roots, const int32_t* counts_in,
+                                   const int32_t* nbr_in, const int32_t* eid_in, const float* dt_in,
+                                   int64_t* offsets_out, int32_t* nbr_out, int32_t* eid_out, float* dt_out,
+                                   void* workspace, size_t ws_bytes, void* stream) {
+    if (n_roots < 0 || n_roots >= (int64_t(1) << 31) || !offsets_out || !workspace) return TGL_EINVAL;
+    if (n_roots > 0 && (!perm || !counts_in)) return TGL_EINVAL;
+    int rc = check_device();
+    if (rc) return rc;
+    return unpermute_block(perm, n_roots, counts_in, nbr_in, eid_in, dt_in, nullptr, offsets_out, nbr_out, eid_out,
+                           dt_out, nullptr, workspace, ws_bytes, (cudaStream_t)stream);
 }
 
 // ---------------------------------------------------------------------------- Alg. 2 schedule

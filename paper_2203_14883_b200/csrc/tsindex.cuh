@@ -51,7 +51,7 @@ inline IndexLayout index_layout(uint64_t n_stored) {
 // selected slots read the SAME lines: one DRAM row activation per list instead of one per array
 // (HBM serves ~33 G random requests/s).
 #ifndef TGL_REC_WORDS
-#define TGL_REC_WORDS 4
+#define TGL_REC_WORDS 3
 #endif
 constexpr int kRecWords = TGL_REC_WORDS;  // 4: {ts, nbr, eid, 0} (one 16-byte vector); 3: packed
 struct SlotRec {
