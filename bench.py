@@ -266,11 +266,13 @@ def setup_graph(key: str, cfg: C.Workload, dev):
 
 # ----------------------------------------------------------------------------- node-sharded mode
 def run_node_sharded(args):
-    """SURVEY 8(e) node-sharded T-CSR: each rank keeps the edge-balanced node range [splits[r],
-    splits[r+1]) (sliced from a full build, which is then freed) and samples its own root chunks
-    through the exchange protocol of paper_2203_14883_b200.sharded: owner bucketing (K8), NCCL
-    all-to-all-v of requests, tgl_sample_keyed on the shard with the roots' global keys (so the
-    bits equal the replicated mode), all-to-all-v of replies, un-permute (K8b).  1 layer (C5)."""
+    """SURVEY 8(e) node-sharded T-CSR through the C ABI: every rank computes the global degree scan
+    (tgl_tcsr_indptr), takes the edge-balanced node range [splits[r], splits[r+1]) and builds ONLY
+    that range (tgl_tcsr_build_range: ~E_s / N per rank); one NCCL communicator (tgl_shard_create,
+    id broadcast through torch.distributed); each step is one collective tgl_sample_sharded over the
+    rank's own root chunk: owner bucketing, NCCL all-to-all of counts / requests / replies, sampling
+    on the owner's range, un-permute -- blocks bit-identical to the replicated mode (checked by
+    per-batch digests against the oracle on the first timed chunk)."""
     import paper_2203_14883_b200 as tgl
     from paper_2203_14883_b200 import sharded as sh
     rank = int(os.environ.get("RANK", "0"))
@@ -283,79 +285,104 @@ def run_node_sharded(args):
         dist.init_process_group("nccl", device_id=dev)
     key = args.config
     cfg = C.CONFIGS[key]
-    if len(cfg.fanouts) != 1:
-        raise SystemExit("node-sharded mode: single-layer configs only (C1, C3, C5)")
     B = cfg.batch
+    L, S = len(cfg.fanouts), cfg.n_snapshots
     chunk = args.batches * B
     src, dst, ts, gen_s = setup_graph(key, cfg, dev)
-    g = tgl.build(src, dst, ts, n_nodes=cfg.n_nodes, add_reverse=cfg.add_reverse, with_index=False)
-    splits = sh.edge_balanced_splits(g.indptr, world)
-    lo, hi = int(splits[rank]), int(splits[rank + 1])
-    shard = sh.slice_shard(g, lo, hi)
-    del g
-    torch.cuda.empty_cache()
+    t0 = time.time()
+    indptr = tgl.tcsr_indptr(src, dst, ts, n_nodes=cfg.n_nodes, add_reverse=cfg.add_reverse)
+    splits = [int(x) for x in sh.edge_balanced_splits(indptr, world).cpu()]
+    lo, hi = splits[rank], splits[rank + 1]
+    n_local = int(indptr[hi] - indptr[lo])
+    del indptr
+    g = tgl.build_range(src, dst, ts, n_nodes=cfg.n_nodes, add_reverse=cfg.add_reverse, node_lo=lo, node_hi=hi,
+                        n_local_stored=n_local)
+    torch.cuda.synchronize(dev)
+    build_s = time.time() - t0
     n_distinct = max(1, min(args.warmup + args.steps, args.distinct))
     mine = rank_chunks(cfg.n_roots_epoch, chunk, n_distinct, world, rank, B)
     chunks = [C.roots(cfg, src, dst, ts, s0, chunk) for s0 in mine]
-    del src, dst, ts
-    torch.cuda.empty_cache()
-    ops = sh.CudaOps(shard, cfg.fanouts[0], cfg.strategy, cfg.n_snapshots, cfg.snapshot_len, world * chunk)
-    ex = sh.DistExchange() if world > 1 else _SelfExchange()
-    smp = sh.NodeShardedSampler(splits.to(dev), ex, ops, cfg.n_snapshots, cfg.sampler_seed)
+    uid = [tgl.nccl_id() if rank == 0 else None]
+    if world > 1:
+        dist.broadcast_object_list(uid, src=0)
+    smp = tgl.ShardSampler(g, splits, rank, world, chunk, cfg.fanouts, cfg.strategy, S, cfg.snapshot_len,
+                           nccl_id=uid[0])
 
     def step(j):
         r, t = chunks[j % n_distinct]
-        return smp.run(r, t, mine[j % n_distinct])
+        return smp.run(r, t, seed=cfg.sampler_seed, root_key_base=mine[j % n_distinct])
 
     for w in range(args.warmup):
         step(w)
     torch.cuda.synchronize(dev)
     if world > 1:
         dist.barrier()
+    st0 = smp.stats()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     clocks = ClockSampler(local)
-    edges = 0
     with clocks:
         e0.record()
         for j in range(args.steps):
-            blocks = step(args.warmup + j)
-            edges += sum(int(b.offsets[-1].item()) for b in blocks)
+            step(args.warmup + j)
         e1.record()
         torch.cuda.synchronize(dev)
+    st1 = smp.stats()
     if world > 1:
         dist.barrier()
     ms = e0.elapsed_time(e1)
-    tot = torch.tensor([float(edges)], dtype=torch.float64, device=dev)
+    # work (deterministic re-runs) + per-batch digests of every timed step
+    edges, digests = 0, {}
+    for j in range(args.steps):
+        blocks = step(args.warmup + j)
+        edges += sum(int(b.nnz_dev.item()) for b in blocks)
+        digests[mine[(args.warmup + j) % n_distinct]] = gpu_batch_digests(tgl, blocks, chunk, B, L, S)
+    # parity: the oracle's digests of this rank's first timed chunk
+    s0 = mine[args.warmup % n_distinct]
+    r0, t0_ = chunks[args.warmup % n_distinct]
+    go, _ = oracle_graph(cfg, src, dst, ts, [r0])
+    per_batch, _ = oracle_batches(go, cfg, r0.cpu().numpy(), t0_.cpu().numpy(), s0,
+                                  max(1, host_info()["cores_available"] // max(1, world)))
+    ok = bool(np.array_equal(oracle_batch_digests(per_batch, L * S), digests[s0]))
+    del go, per_batch
+    sent = float(st1["bytes_sent"] - st0["bytes_sent"])
+    tot = torch.tensor([float(edges), sent, 0.0 if ok else 1.0], dtype=torch.float64, device=dev)
     mx = torch.tensor([ms], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(tot)
         dist.all_reduce(mx, op=dist.ReduceOp.MAX)
-    out = {"metric": METRIC, "value": float(tot[0]) / (float(mx[0]) / 1e3), "unit": UNIT, "n_gpus": world,
-           "steps": args.steps, "warmup": args.warmup, "ms_per_step": float(mx[0]) / args.steps,
+    ms_max = float(mx[0])
+    failed = tot[2].item() > 0 or tgl.check(g) != 0
+    nv_peak = 900.0  # GB/s per direction per GPU over NVLink 5 (B200_PROFILING.md nominal)
+    nv_rate = sent / (ms / 1e3) / 1e9 if ms > 0 else 0.0
+    out = {"metric": METRIC, "value": None if failed else float(tot[0]) / (ms_max / 1e3), "unit": UNIT,
+           "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
            "config": {"workload": workload_name(key, cfg), "batch_roots": B, "batches_per_step": args.batches,
                       "roots_per_step_per_gpu": chunk,
-                      "parallelism": f"node-sharded T-CSR over {world} rank(s), edge-balanced node ranges; "
-                                     "requests/replies by all-to-all-v (NCCL)",
-                      "shard_nodes": hi - lo, "shard_edges": int(shard.n_stored),
+                      "parallelism": f"node-sharded T-CSR over {world} rank(s) (tgl_tcsr_build_range), edge-balanced "
+                                     "node ranges; tgl_sample_sharded: NCCL send/recv of counts, requests, replies",
+                      "shard_nodes": hi - lo, "shard_edges": n_local,
                       "l2": "no flush: shard and per-step roots exceed L2"},
-           "clocks": clocks.summary(), "generate_s": gen_s,
-           "note": "the timed step includes the host-synchronising count exchanges of the protocol"}
+           "exchange": {"bytes_sent_per_step_per_rank": sent / args.steps,
+                        "host_syncs_per_step": (st1["host_syncs"] - st0["host_syncs"]) / args.steps,
+                        "nvlink_GBps_per_rank": nv_rate, "nvlink_peak_GBps": nv_peak, "nvlink_frac": nv_rate / nv_peak,
+                        "note": "bytes to OTHER ranks only (none at N = 1: the exchange is a self-send)"},
+           "parity": {"bit_exact": not failed, "against": "oracle per-batch FNV-1a digests, first timed chunk of "
+                                                          "every rank", "checked_roots": chunk * world},
+           # per call: the root keys + per chain bucketing (owner, upsweep, 3 scan, downsweep, counts), pack,
+           # window + copy, reply counts; per block offsets->counts, un-permute (2 x 3 scan + counts + copy),
+           # block sizes; per deeper chain the child keys (NCCL's own kernels not counted)
+           "gpu_launches": args.steps * (1 + (11 + 10 * S) + (L - 1) * S * (11 + 10 + 1)),
+           "clocks": clocks.summary(), "generate_s": gen_s, "build_s": build_s,
+           "note": "the timed step includes the protocol's 2 host synchronisations per chain"}
+    if failed:
+        out["error"] = "parity failure or device error: no throughput reported"
     if rank == 0:
         print(json.dumps(out), flush=True)
     if world > 1:
         dist.destroy_process_group()
-
-
-class _SelfExchange:
-    """world = 1: the all-to-all-v of one rank is the identity."""
-    world, rank = 1, 0
-
-    def splits(self, send_counts):
-        return send_counts.clone()
-
-    def exchange(self, t, send_splits, recv_splits):
-        return t
+    if failed:
+        sys.exit(1)
 
 
 # ----------------------------------------------------------------------------- parity (oracle side)
