@@ -471,6 +471,29 @@ TGL_API int tgl_sample_sharded(tgl_shard *shard, const int32_t *roots, const flo
                        int32_t n_snapshots, float snapshot_len, uint64_t seed, uint64_t root_key_base,
                        tgl_block *out /* host [L*S] */, void *stream);
 
+/*
+ * Sharded node state: node memory / mailbox tables split
+ * by the shard's node ranges -- rank r holds the rows of global nodes [splits[r], splits[r+1]).
+ * COLLECTIVE calls (every rank of the shard calls them, with its own ids, possibly none).
+ *
+ * tgl_shard_gather (Fig. 2 step 2 across ranks): for every table j, out_j[i] = the row of global
+ *   node ids[i] (wherever it lives), i < n, in request order.  tables[j].table = this rank's LOCAL
+ *   rows, tables[j].n_rows = splits[rank+1] - splits[rank], tables[j].row_bytes = bytes per node
+ *   (a K-slot ring is one K * slot-bytes row), tables[j].out = device [n * row_bytes].
+ *   id == -1 gives a zero row.  One host synchronisation (the request counts).
+ * tgl_shard_state_write (Fig. 2 step 6 across ranks, R#25): the events (ids[i], ts[i], rows_j[i])
+ *   of all ranks are applied, in (rank, event index) order, to the owners' LOCAL tables exactly as
+ *   tgl_state_write applies a batch: tables[j].rows = device [n * row_bytes], tables[j].table =
+ *   LOCAL [n_local * K * row_bytes]; pos (int32 [n_local], required for K > 1) and ts_table
+ *   (float [n_local * K], may be NULL) are LOCAL too.  At most TGL_MAX_GATHER_TABLES - 2 tables.
+ *   One host synchronisation.  Device-detected errors go to tgl_check(NULL, ...).
+ */
+TGL_API int tgl_shard_gather(tgl_shard *shard, const int32_t *ids, int64_t n,
+                     const tgl_gather_table *tables /* host [n_tables] */, int32_t n_tables, void *stream);
+TGL_API int tgl_shard_state_write(tgl_shard *shard, const int32_t *ids, const float *ts, int64_t n, int32_t K,
+                          int32_t *pos, float *ts_table, const tgl_state_table *tables /* host [n_tables] */,
+                          int32_t n_tables, void *stream);
+
 /* Cumulative exchange statistics of a shard: bytes sent to / received from OTHER ranks (the
  * NVLink traffic of the protocol) and host synchronisations. */
 TGL_API int tgl_shard_stats(const tgl_shard *shard, int64_t *bytes_sent, int64_t *bytes_recv,

@@ -627,6 +627,44 @@ class ShardSampler:
             "tgl_sample_sharded")
         return self.blocks
 
+    def gather(self, ids: torch.Tensor, local_tables: Sequence[torch.Tensor],
+               outs: Optional[Sequence[torch.Tensor]] = None, stream=None) -> List[torch.Tensor]:
+        """tgl_shard_gather (collective): rows of global nodes `ids` from tables sharded like the
+        T-CSR; local_tables[j] = this rank's rows [n_local, ...] (a K-slot ring: [n_local, K, ...])."""
+        ids = _cuda(ids, torch.int32, "ids")
+        n = ids.numel()
+        arr, res = (_lib.GatherTable * len(local_tables))(), []
+        for j, t in enumerate(local_tables):
+            if not (t.is_cuda and t.is_contiguous()):
+                raise TypeError("local tables must be contiguous CUDA tensors")
+            rb = t.element_size() * int(np.prod(t.shape[1:], dtype=np.int64))
+            o = outs[j] if outs is not None else torch.empty((n,) + tuple(t.shape[1:]), dtype=t.dtype, device=t.device)
+            res.append(o)
+            arr[j] = _lib.GatherTable(t.data_ptr(), t.shape[0], rb, o.data_ptr())
+        _rc(_L.tgl_shard_gather(self._h, _ptr(ids), n, arr, len(local_tables), _stream(stream)), "tgl_shard_gather")
+        return res
+
+    def state_write(self, ids: torch.Tensor, ts: Optional[torch.Tensor], pairs, *, K: int = 1,
+                    pos: Optional[torch.Tensor] = None, ts_table: Optional[torch.Tensor] = None, stream=None) -> None:
+        """tgl_shard_state_write (collective): pairs = [(rows [n, ...], local table [n_local * K, ...])];
+        pos / ts_table: this rank's local cursors [n_local] / times [n_local * K]."""
+        ids = _cuda(ids, torch.int32, "ids")
+        n = ids.numel()
+        if ts is not None:
+            ts = _cuda(ts, torch.float32, "ts")
+        arr = (_lib.StateTable * max(len(pairs), 1))()
+        for j, (rows, table) in enumerate(pairs):
+            if not (rows.is_cuda and table.is_cuda and rows.is_contiguous() and table.is_contiguous()):
+                raise TypeError("state rows / tables must be contiguous CUDA tensors")
+            rb = rows.element_size() * int(np.prod(rows.shape[1:], dtype=np.int64))
+            arr[j] = _lib.StateTable(rows.data_ptr() if n else None, rb, table.data_ptr())
+        if pos is not None:
+            pos = _cuda(pos, torch.int32, "pos")
+        if ts_table is not None:
+            ts_table = _cuda(ts_table, torch.float32, "ts_table")
+        _rc(_L.tgl_shard_state_write(self._h, _ptr(ids), _ptr(ts), n, int(K), _ptr(pos), _ptr(ts_table), arr, len(pairs),
+                                     _stream(stream)), "tgl_shard_state_write")
+
     def stats(self):
         a, b, c = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
         _rc(_L.tgl_shard_stats(self._h, ctypes.byref(a), ctypes.byref(b), ctypes.byref(c)), "tgl_shard_stats")

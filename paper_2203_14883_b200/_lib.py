@@ -85,6 +85,8 @@ SIGNATURES = {
     "tgl_shard_create": (ctypes.c_int, [P, P, i32, i32, P, P, ctypes.POINTER(P)]),
     "tgl_shard_destroy": (ctypes.c_int, [P]),
     "tgl_sample_sharded": (ctypes.c_int, [P, P, P, i64, i32, P, ctypes.c_int, i32, f32, u64, u64, P, P]),
+    "tgl_shard_gather": (ctypes.c_int, [P, P, i64, P, i32, P]),
+    "tgl_shard_state_write": (ctypes.c_int, [P, P, P, i64, i32, P, P, P, i32, P]),
     "tgl_shard_stats": (ctypes.c_int, [P, ctypes.POINTER(i64), ctypes.POINTER(i64), ctypes.POINTER(i64)]),
     "tgl_shard_bucket_workspace": (ctypes.c_int, [i64, i32, ctypes.POINTER(sz)]),
     "tgl_shard_bucket": (ctypes.c_int, [P, i64, P, i32, P, P, P, sz, P]),

@@ -604,3 +604,142 @@ extern "C" int tgl_sample_sharded(tgl_shard* sh, const int32_t* roots, const flo
     }
     return TGL_OK;
 }
+
+// ---------------------------------------------------------------------------- sharded node state
+// Node memory / mailbox sharded by the same node ranges (MAG's 121 M x (100 +
+// K x 428) fp32 state does not fit one GPU -- the paper's APAN-on-MAG OOM).  Fig. 2 step
+// 2 (gather) and step 6 (state write) across ranks, with the shard's transport:
+//   gather       bucket the ids by owner (K8), X1 counts (sync), X2 ids, local tgl_gather on the
+//                owner's rows, X3 rows back (sizes already known), request order restored through
+//                the inverse permutation (tgl_perm_invert + tgl_gather);
+//   state write  bucket the events by owner (stable: each owner receives them in (source rank,
+//                batch index) order, the global event order of R#25), X1 counts (sync), X2 ids,
+//                times and rows, local tgl_state_write on the owner's tables.
+namespace tgl {
+
+struct Route {
+    int32_t* perm = nullptr;
+    std::vector<int64_t> scnt, rcnt;
+    int64_t m = 0;
+};
+
+static int route(tgl_shard* sh, const int32_t* ids, int64_t n, cudaStream_t st, Route& R) {
+    const int W = sh->world;
+    int rc = TGL_OK;
+    size_t bws = 0;
+    if ((rc = tgl_shard_bucket_workspace(n, W, &bws))) return rc;
+    void* bw = sh->b_bucket.get<char>(bws, &rc);
+    R.perm = sh->b_perm.get<int32_t>(std::max<int64_t>(n, 1), &rc);
+    int64_t* cnt = sh->b_cnt.get<int64_t>(2 * 256 + 2 * 256 * TGL_MAX_SNAPSHOTS, &rc);
+    if (rc) return rc;
+    if ((rc = tgl_shard_bucket(ids, n, static_cast<const int64_t*>(sh->b_splits.p), W, R.perm, cnt, bw, bws, st)))
+        return rc;
+    std::vector<int64_t> ones(W, 1);
+    Field f{cnt, cnt + 256, sizeof(int64_t), ones.data(), ones.data()};
+    if ((rc = sh->tr->exchange(&f, 1, st))) return rc;
+    int64_t* h = sh->h_cnt;
+    if (cudaMemcpyAsync(h, cnt, sizeof(int64_t) * 512, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+        cudaStreamSynchronize(st) != cudaSuccess)
+        return TGL_ECUDA;
+    ++sh->host_syncs;
+    R.scnt.assign(h, h + W);
+    R.rcnt.assign(h + 256, h + 256 + W);
+    R.m = 0;
+    for (int p = 0; p < W; ++p) R.m += R.rcnt[p];
+    return TGL_OK;
+}
+
+}  // namespace tgl
+
+extern "C" int tgl_shard_gather(tgl_shard* sh, const int32_t* ids, int64_t n, const tgl_gather_table* tables,
+                                int32_t n_tables, void* stream) {
+    if (!sh || n < 0 || (n > 0 && !ids) || n_tables < 1 || n_tables > TGL_MAX_GATHER_TABLES || !tables)
+        return TGL_EINVAL;
+    const int64_t lo = sh->splits[sh->rank], hi = sh->splits[sh->rank + 1];
+    for (int j = 0; j < n_tables; ++j)
+        if (tables[j].row_bytes <= 0 || tables[j].n_rows != hi - lo || (hi > lo && !tables[j].table) ||
+            (n > 0 && !tables[j].out))
+            return TGL_EINVAL;
+    int rc = check_device();
+    if (rc) return rc;
+    cudaStream_t st = (cudaStream_t)stream;
+    Route R;
+    if ((rc = route(sh, ids, n, st, R))) return rc;
+    // X2: the ids to their owners (bucket order)
+    int32_t* qids = sh->b_qn.get<int32_t>(n, &rc);
+    int32_t* rids = sh->b_rn.get<int32_t>(R.m, &rc);
+    if (rc) return rc;
+    tgl_gather_table pk{ids, n, 4, qids};
+    if (n > 0 && (rc = tgl_gather(R.perm, n, nullptr, &pk, 1, stream))) return rc;
+    {
+        Field f{qids, rids, 4, R.scnt.data(), R.rcnt.data()};
+        if ((rc = sh->tr->exchange(&f, 1, st))) return rc;
+    }
+    // local rows (global ids: table bases offset by -lo rows), then X3 back to the requesters
+    tgl_gather_table loc[TGL_MAX_GATHER_TABLES], back[TGL_MAX_GATHER_TABLES];
+    Field f[TGL_MAX_GATHER_TABLES];
+    for (int j = 0; j < n_tables; ++j) {
+        const int64_t rb = tables[j].row_bytes;
+        char* lrows = sh->b_lnbr[j].get<char>((size_t)std::max<int64_t>(R.m, 1) * rb, &rc);
+        char* brows = sh->b_pnbr[j].get<char>((size_t)std::max<int64_t>(n, 1) * rb, &rc);
+        if (rc) return rc;
+        loc[j] = {static_cast<const char*>(tables[j].table) - lo * rb, hi, rb, lrows};
+        back[j] = {brows, n, rb, tables[j].out};
+        f[j] = {lrows, brows, (size_t)rb, R.rcnt.data(), R.scnt.data()};
+    }
+    if (R.m > 0 && (rc = tgl_gather(rids, R.m, nullptr, loc, n_tables, stream))) return rc;
+    if ((rc = sh->tr->exchange(f, n_tables, st))) return rc;
+    // request order: out[perm[j]] = back[j]  <=>  out[i] = back[inv[i]]
+    int32_t* inv = sh->b_qk.get<int32_t>(std::max<int64_t>(n, 1), &rc);
+    if (rc) return rc;
+    if (n > 0 && ((rc = tgl_perm_invert(R.perm, n, inv, stream)) || (rc = tgl_gather(inv, n, nullptr, back, n_tables, stream))))
+        return rc;
+    return TGL_OK;
+}
+
+extern "C" int tgl_shard_state_write(tgl_shard* sh, const int32_t* ids, const float* ts, int64_t n, int32_t K,
+                                     int32_t* pos, float* ts_table, const tgl_state_table* tables, int32_t n_tables,
+                                     void* stream) {
+    if (!sh || n < 0 || (n > 0 && !ids) || K < 1 || (K > 1 && !pos) || n_tables < 0 ||
+        n_tables > TGL_MAX_GATHER_TABLES - 2 || (n_tables > 0 && !tables) || (ts_table && !ts))
+        return TGL_EINVAL;
+    const int64_t lo = sh->splits[sh->rank], hi = sh->splits[sh->rank + 1];
+    for (int j = 0; j < n_tables; ++j)
+        if (tables[j].row_bytes <= 0 || (n > 0 && !tables[j].rows) || (hi > lo && !tables[j].table)) return TGL_EINVAL;
+    int rc = check_device();
+    if (rc) return rc;
+    cudaStream_t st = (cudaStream_t)stream;
+    Route R;
+    if ((rc = route(sh, ids, n, st, R))) return rc;
+    // pack (ids, times, rows) in bucket order, X2 to the owners
+    const int nf = 1 + (ts ? 1 : 0) + n_tables;
+    tgl_gather_table pk[TGL_MAX_GATHER_TABLES];
+    Field f[TGL_MAX_GATHER_TABLES];
+    char* recv[TGL_MAX_GATHER_TABLES];
+    int q = 0;
+    auto add = [&](const void* src, int64_t rb) {
+        char* packed = sh->b_pnbr[q].get<char>((size_t)std::max<int64_t>(n, 1) * rb, &rc);
+        recv[q] = sh->b_lnbr[q].get<char>((size_t)std::max<int64_t>(R.m, 1) * rb, &rc);
+        pk[q] = {src, n, rb, packed};
+        f[q] = {packed, recv[q], (size_t)rb, R.scnt.data(), R.rcnt.data()};
+        ++q;
+    };
+    add(ids, 4);
+    if (ts) add(ts, 4);
+    for (int j = 0; j < n_tables; ++j) add(tables[j].rows, tables[j].row_bytes);
+    if (rc) return rc;
+    if (n > 0 && (rc = tgl_gather(R.perm, n, nullptr, pk, nf, stream))) return rc;
+    if ((rc = sh->tr->exchange(f, nf, st))) return rc;
+    // apply on the owner: global ids, local tables (bases offset by -lo nodes)
+    tgl_state_table loc[TGL_MAX_GATHER_TABLES];
+    for (int j = 0; j < n_tables; ++j)
+        loc[j] = {recv[(ts ? 2 : 1) + j], tables[j].row_bytes,
+                  static_cast<char*>(tables[j].table) - lo * (int64_t)K * tables[j].row_bytes};
+    size_t wsb = 0;
+    if ((rc = tgl_state_write_workspace(R.m, (int32_t)hi, &wsb))) return rc;
+    void* ws = sh->b_unperm.get<char>(wsb, &rc);
+    if (rc) return rc;
+    return tgl_state_write(reinterpret_cast<const int32_t*>(recv[0]), ts ? reinterpret_cast<const float*>(recv[1]) : nullptr,
+                           R.m, (int32_t)hi, K, pos ? pos - lo : nullptr, ts_table ? ts_table - lo * K : nullptr, loc,
+                           n_tables, ws, wsb, stream);
+}

@@ -167,3 +167,73 @@ def test_sharded_against_oracle_and_nccl(tgl):
         np.testing.assert_array_equal(off, want_np[b][0])
         for j in (1, 2, 3):
             np.testing.assert_array_equal(np.concatenate([got[i][b][j] for i in range(W)]), want_np[b][j])
+
+
+@pytest.mark.parametrize("world", [1, 2, 3])
+def test_sharded_node_state(tgl, world):
+    """tgl_shard_gather / tgl_shard_state_write over W ranks on threads: the
+    gathered rows equal the full tables' rows, and the owners' local tables after the write equal
+    the oracle's sequential write (R#25) of all ranks' events in (rank, index) order."""
+    V, E, K, dm, dmail = 500, 20000, 3, 7, 5
+    src, dst, ts, _ = random_graph(31, V, E, with_eid=False, integer_times=True)
+    s, d, t = (torch.as_tensor(x).cuda() for x in (src, dst, ts))
+    _, sp, shards = build_ranges(tgl, s, d, t, V, True, world)
+    grp = tgl.ShardGroup(world)
+    smps = [tgl.ShardSampler(shards[r], sp, r, world, 1, [1], group=grp) for r in range(world)]
+    rng = np.random.default_rng(5)
+    mem = torch.as_tensor(rng.standard_normal((V, dm)).astype(np.float32)).cuda()
+    mail = torch.as_tensor(rng.standard_normal((V, K, dmail)).astype(np.float32)).cuda()
+    pos = torch.as_tensor(rng.integers(0, K, V).astype(np.int32)).cuda()
+    mts = torch.zeros(V * K, dtype=torch.float32, device="cuda")
+    loc = [dict(mem=mem[sp[r]:sp[r + 1]].clone(), mail=mail[sp[r]:sp[r + 1]].clone(), pos=pos[sp[r]:sp[r + 1]].clone(),
+                mts=mts[sp[r] * K:sp[r + 1] * K].clone()) for r in range(world)]
+    ids = [torch.as_tensor(np.where(rng.random(n) < 0.1, -1, rng.integers(0, V, n)).astype(np.int32)).cuda()
+           for n in (900, 0, 1500)[:world]]
+    ev = [torch.as_tensor(rng.integers(0, V, n).astype(np.int32)).cuda() for n in (800, 1200, 0)[:world]]
+    ev_t = [torch.sort(torch.as_tensor(rng.random(x.numel()).astype(np.float32) * 100).cuda())[0] for x in ev]
+    ev_mem = [torch.as_tensor(rng.standard_normal((x.numel(), dm)).astype(np.float32)).cuda() for x in ev]
+    ev_mail = [torch.as_tensor(rng.standard_normal((x.numel(), dmail)).astype(np.float32)).cuda() for x in ev]
+    got, errs = [None] * world, []
+
+    def work(r):
+        try:
+            st = torch.cuda.Stream()
+            with torch.cuda.stream(st):
+                g_mem, g_mail = smps[r].gather(ids[r], [loc[r]["mem"], loc[r]["mail"]])
+                st.synchronize()
+                got[r] = (g_mem.cpu().numpy(), g_mail.cpu().numpy())
+                smps[r].state_write(ev[r], ev_t[r], [(ev_mem[r], loc[r]["mem"])], K=1)
+                smps[r].state_write(ev[r], ev_t[r], [(ev_mail[r], loc[r]["mail"])], K=K, pos=loc[r]["pos"],
+                                    ts_table=loc[r]["mts"])
+                st.synchronize()
+        except Exception as e:  # noqa: BLE001
+            errs.append(e)
+    th = [threading.Thread(target=work, args=(r,)) for r in range(world)]
+    for x in th:
+        x.start()
+    for x in th:
+        x.join(timeout=600)
+    assert not errs, errs
+    assert tgl.check(None) == 0
+    full_mem, full_mail = mem.cpu().numpy(), mail.cpu().numpy()
+    for r in range(world):
+        idn = ids[r].cpu().numpy()
+        want_mem = np.where((idn >= 0)[:, None], full_mem[np.maximum(idn, 0)], 0)
+        want_mail = np.where((idn >= 0)[:, None, None], full_mail[np.maximum(idn, 0)], 0)
+        np.testing.assert_array_equal(got[r][0], want_mem)
+        np.testing.assert_array_equal(got[r][1], want_mail)
+    # oracle: all events in (rank, index) order on the full tables
+    all_ids = np.concatenate([x.cpu().numpy() for x in ev])
+    all_t = np.concatenate([x.cpu().numpy() for x in ev_t])
+    w_mem = full_mem.copy()
+    w_mail = full_mail.reshape(V * K, dmail).copy()
+    w_pos, w_ts = pos.cpu().numpy().copy(), mts.cpu().numpy().copy()
+    oracle.state_write(all_ids, all_t, n_nodes=V, K=1, tables=[(np.concatenate([x.cpu().numpy() for x in ev_mem]), w_mem)])
+    oracle.state_write(all_ids, all_t, n_nodes=V, K=K, tables=[(np.concatenate([x.cpu().numpy() for x in ev_mail]),
+                                                                w_mail)], pos=w_pos, ts_table=w_ts)
+    for r in range(world):
+        lo, hi = sp[r], sp[r + 1]
+        np.testing.assert_array_equal(loc[r]["mem"].cpu().numpy(), w_mem[lo:hi])
+        np.testing.assert_array_equal(loc[r]["mail"].cpu().numpy().reshape(-1, dmail), w_mail[lo * K:hi * K])
+        np.testing.assert_array_equal(loc[r]["pos"].cpu().numpy(), w_pos[lo:hi])
+        np.testing.assert_array_equal(loc[r]["mts"].cpu().numpy(), w_ts[lo * K:hi * K])
