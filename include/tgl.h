@@ -483,7 +483,8 @@ TGL_API int tgl_sample_sharded(tgl_shard *shard, const int32_t *roots, const flo
  *   id == -1 gives a zero row.  One host synchronisation (the request counts).
  * tgl_shard_state_write (Fig. 2 step 6 across ranks, R#25): the events (ids[i], ts[i], rows_j[i])
  *   of all ranks are applied, in (rank, event index) order, to the owners' LOCAL tables exactly as
- *   tgl_state_write applies a batch: tables[j].rows = device [n * row_bytes], tables[j].table =
+ *   tgl_state_write applies a batch (ts: device float [n], required when n > 0, the same fields
+ *   travel from every rank): tables[j].rows = device [n * row_bytes], tables[j].table =
  *   LOCAL [n_local * K * row_bytes]; pos (int32 [n_local], required for K > 1) and ts_table
  *   (float [n_local * K], may be NULL) are LOCAL too.  At most TGL_MAX_GATHER_TABLES - 2 tables.
  *   One host synchronisation.  Device-detected errors go to tgl_check(NULL, ...).

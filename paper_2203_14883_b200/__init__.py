@@ -644,14 +644,13 @@ class ShardSampler:
         _rc(_L.tgl_shard_gather(self._h, _ptr(ids), n, arr, len(local_tables), _stream(stream)), "tgl_shard_gather")
         return res
 
-    def state_write(self, ids: torch.Tensor, ts: Optional[torch.Tensor], pairs, *, K: int = 1,
+    def state_write(self, ids: torch.Tensor, ts: torch.Tensor, pairs, *, K: int = 1,
                     pos: Optional[torch.Tensor] = None, ts_table: Optional[torch.Tensor] = None, stream=None) -> None:
         """tgl_shard_state_write (collective): pairs = [(rows [n, ...], local table [n_local * K, ...])];
         pos / ts_table: this rank's local cursors [n_local] / times [n_local * K]."""
         ids = _cuda(ids, torch.int32, "ids")
         n = ids.numel()
-        if ts is not None:
-            ts = _cuda(ts, torch.float32, "ts")
+        ts = _cuda(ts, torch.float32, "ts")
         arr = (_lib.StateTable * max(len(pairs), 1))()
         for j, (rows, table) in enumerate(pairs):
             if not (rows.is_cuda and table.is_cuda and rows.is_contiguous() and table.is_contiguous()):

@@ -160,6 +160,8 @@ struct LocalTransport : Transport {
         if (cudaEventRecord(me.ready, st) != cudaSuccess) return TGL_ECUDA;
         grp->barrier();  // every rank's send buffers are posted (and produced once `ready` fires)
         int rc = TGL_OK;
+        for (int p = 0; p < world; ++p)  // every rank must post the same fields (else: no copies)
+            if ((int)grp->post[p].f.size() != nf) rc = TGL_EINVAL;
         for (int p = 0; p < world && !rc; ++p) {
             auto& peer = grp->post[p];
             if (cudaStreamWaitEvent(st, peer.ready, 0) != cudaSuccess) rc = TGL_ECUDA;
@@ -700,8 +702,9 @@ extern "C" int tgl_shard_gather(tgl_shard* sh, const int32_t* ids, int64_t n, co
 extern "C" int tgl_shard_state_write(tgl_shard* sh, const int32_t* ids, const float* ts, int64_t n, int32_t K,
                                      int32_t* pos, float* ts_table, const tgl_state_table* tables, int32_t n_tables,
                                      void* stream) {
-    if (!sh || n < 0 || (n > 0 && !ids) || K < 1 || (K > 1 && !pos) || n_tables < 0 ||
-        n_tables > TGL_MAX_GATHER_TABLES - 2 || (n_tables > 0 && !tables) || (ts_table && !ts))
+    // every rank exchanges the same fields (ids, times, rows): times are required whenever n > 0
+    if (!sh || n < 0 || (n > 0 && (!ids || !ts)) || K < 1 || (K > 1 && !pos) || n_tables < 0 ||
+        n_tables > TGL_MAX_GATHER_TABLES - 2 || (n_tables > 0 && !tables))
         return TGL_EINVAL;
     const int64_t lo = sh->splits[sh->rank], hi = sh->splits[sh->rank + 1];
     for (int j = 0; j < n_tables; ++j)
@@ -712,7 +715,7 @@ extern "C" int tgl_shard_state_write(tgl_shard* sh, const int32_t* ids, const fl
     Route R;
     if ((rc = route(sh, ids, n, st, R))) return rc;
     // pack (ids, times, rows) in bucket order, X2 to the owners
-    const int nf = 1 + (ts ? 1 : 0) + n_tables;
+    const int nf = 2 + n_tables;
     tgl_gather_table pk[TGL_MAX_GATHER_TABLES];
     Field f[TGL_MAX_GATHER_TABLES];
     char* recv[TGL_MAX_GATHER_TABLES];
@@ -725,7 +728,7 @@ extern "C" int tgl_shard_state_write(tgl_shard* sh, const int32_t* ids, const fl
         ++q;
     };
     add(ids, 4);
-    if (ts) add(ts, 4);
+    add(ts, 4);
     for (int j = 0; j < n_tables; ++j) add(tables[j].rows, tables[j].row_bytes);
     if (rc) return rc;
     if (n > 0 && (rc = tgl_gather(R.perm, n, nullptr, pk, nf, stream))) return rc;
@@ -733,13 +736,13 @@ extern "C" int tgl_shard_state_write(tgl_shard* sh, const int32_t* ids, const fl
     // apply on the owner: global ids, local tables (bases offset by -lo nodes)
     tgl_state_table loc[TGL_MAX_GATHER_TABLES];
     for (int j = 0; j < n_tables; ++j)
-        loc[j] = {recv[(ts ? 2 : 1) + j], tables[j].row_bytes,
+        loc[j] = {recv[2 + j], tables[j].row_bytes,
                   static_cast<char*>(tables[j].table) - lo * (int64_t)K * tables[j].row_bytes};
     size_t wsb = 0;
     if ((rc = tgl_state_write_workspace(R.m, (int32_t)hi, &wsb))) return rc;
     void* ws = sh->b_unperm.get<char>(wsb, &rc);
     if (rc) return rc;
-    return tgl_state_write(reinterpret_cast<const int32_t*>(recv[0]), ts ? reinterpret_cast<const float*>(recv[1]) : nullptr,
+    return tgl_state_write(reinterpret_cast<const int32_t*>(recv[0]), reinterpret_cast<const float*>(recv[1]),
                            R.m, (int32_t)hi, K, pos ? pos - lo : nullptr, ts_table ? ts_table - lo * K : nullptr, loc,
                            n_tables, ws, wsb, stream);
 }
