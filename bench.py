@@ -505,11 +505,19 @@ def run_ours(args):
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+    # more ranks than GPUs (a launcher test on a 1-GPU box): ranks share the devices and the
+    # reporting collectives run over gloo; the line says so ("oversubscribed") -- not a scaling number
+    n_dev = max(1, torch.cuda.device_count())
+    oversub = world > n_dev
+    torch.cuda.set_device(local % n_dev)
+    dev = torch.device("cuda", local % n_dev)
+    cdev = torch.device("cpu") if oversub else dev  # device of the reporting collectives
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=dev)
+        if oversub:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
     key = args.config
     cfg = C.CONFIGS[key]
     B = cfg.batch
@@ -608,7 +616,7 @@ def run_ours(args):
     rerun_same = bool(np.array_equal(digests_by_start[mine[args.warmup + args.steps - 1]], timed_last_digests))
     err = tgl.check(g)
 
-    edges_all, bytes_all, total_ms_max = reduce_report(edges_total, bytes_total, total_ms, world, dev)
+    edges_all, bytes_all, total_ms_max = reduce_report(edges_total, bytes_total, total_ms, world, cdev)
 
     value = edges_all / (total_ms_max / 1e3)
     tcsr_bytes = g.indptr.numel() * 8 + g.n_stored * 12
@@ -651,19 +659,21 @@ def run_ours(args):
         "build_ms": build_ms, "generate_s": gen_s,
         "edges_per_step": edges_total / args.steps, "roots_per_step": roots_total / args.steps,
         "device_error": int(err),
+        **({"oversubscribed": f"{world} ranks on {n_dev} GPU(s): launcher test, not a scaling number"}
+           if oversub else {}),
     }
 
     # per-batch mode (SURVEY 8(d) mode 1): one tgl_sample call per batch, replayed as a CUDA graph
     if not args.no_per_batch:
         mid = n_distinct // 2  # a chunk from the middle of the epoch (early batches have short histories)
-        out["per_batch"] = per_batch(args, tgl, g, cfg, chunks[mid], mine[mid], dev, world)
+        out["per_batch"] = per_batch(args, tgl, g, cfg, chunks[mid], mine[mid], dev, world, cdev=cdev)
 
     # end to end through the public API with host buffers (rank-local), copies inside the region
     if not args.no_e2e:
         gf = (lambda smp: make_gather(tgl, cfg, smp, dev)) if gather is not None else None
-        out["e2e"] = e2e(args, tgl, sampler, chunks, mine, cfg, dev, world, gather_factory=gf,
+        out["e2e"] = e2e(args, tgl, sampler, chunks, mine, cfg, dev, world, gather_factory=gf, cdev=cdev,
                          events=events if gather is not None else None)
-        out["e2e_full_d2h"] = e2e(args, tgl, sampler, chunks, mine, cfg, dev, world, full_d2h=True)
+        out["e2e_full_d2h"] = e2e(args, tgl, sampler, chunks, mine, cfg, dev, world, full_d2h=True, cdev=cdev)
 
     # parity gate (every rank, its own timed chunks) + CPU oracle baseline (rank 0, N = 1 only)
     out["parity"], cpu = parity_gate(args, cfg, tgl, sampler, src, dst, ts, chunks, mine, digests_by_start,
@@ -672,7 +682,7 @@ def run_ours(args):
         out["cpu_baseline"] = cpu
     failed = not out["parity"]["bit_exact"] or err != 0
     if world > 1:
-        flag = torch.tensor([1.0 if failed else 0.0], device=dev)
+        flag = torch.tensor([1.0 if failed else 0.0], device=cdev)
         torch.distributed.all_reduce(flag, op=torch.distributed.ReduceOp.MAX)
         failed = bool(flag.item())
     if failed:  # a run whose outputs do not match the oracle reports no throughput
@@ -686,7 +696,7 @@ def run_ours(args):
         sys.exit(1)
 
 
-def per_batch(args, tgl, g, cfg, chunk, key0, dev, world, n_graph=64, reps=10):
+def per_batch(args, tgl, g, cfg, chunk, key0, dev, world, n_graph=64, reps=10, cdev=None):
     """Latency mode: n_graph consecutive batches, one tgl_sample call each (batch b's roots, key base
     = its global root index), captured once as a CUDA graph and replayed; device time per batch =
     replay time / n_graph (CUDA events, max over ranks).  Edges counted from an eager re-run."""
@@ -726,7 +736,7 @@ def per_batch(args, tgl, g, cfg, chunk, key0, dev, world, n_graph=64, reps=10):
     e1.record()
     torch.cuda.synchronize(dev)
     ms = e0.elapsed_time(e1)
-    edges_all, _, ms_max = reduce_report(edges * reps, 0.0, ms, world, dev)
+    edges_all, _, ms_max = reduce_report(edges * reps, 0.0, ms, world, cdev or dev)
     launches = 2 * (1 + (L - 1) * S)
     return {"batch_roots": B, "batches_per_graph": n_graph, "replays": reps, "graph": True,
             "latency_us_per_batch": ms_max * 1e3 / (reps * n_graph),
@@ -735,7 +745,8 @@ def per_batch(args, tgl, g, cfg, chunk, key0, dev, world, n_graph=64, reps=10):
                     "launch-latency bound; the headline value is epoch mode"}
 
 
-def e2e(args, tgl, sampler, chunks, mine, cfg, dev, world, full_d2h=False, gather_factory=None, events=None):
+def e2e(args, tgl, sampler, chunks, mine, cfg, dev, world, full_d2h=False, gather_factory=None, events=None,
+        cdev=None):
     """End to end through the public API with host buffers, copies inside the timed region.
 
     Per step: pinned host roots -> H2D (copy stream) -> tgl_sample (compute stream) -> D2H of the
@@ -846,7 +857,7 @@ def e2e(args, tgl, sampler, chunks, mine, cfg, dev, world, full_d2h=False, gathe
     e.record(comp)
     torch.cuda.synchronize(dev)
     ms = s.elapsed_time(e)
-    edges, _, ms_max = reduce_report(stats["edges"], 0.0, ms, world, dev)
+    edges, _, ms_max = reduce_report(stats["edges"], 0.0, ms, world, cdev or dev)
     what = ("pinned host roots -> H2D -> tgl_sample -> D2H of every block (offsets, nbr, eid, dt)" if full_d2h else
             "pinned host roots -> H2D -> tgl_sample -> D2H of the step's metric (per-block n_roots, nnz); "
             "blocks stay on the GPU for the consumer")

@@ -174,6 +174,7 @@ extern "C" int tgl_tcsr_build(const int32_t* src, const int32_t* dst, const floa
                               int64_t n_edges, int32_t n_nodes, int add_reverse, int64_t* indptr, int32_t* nbr,
                               float* ts_out, int32_t* eid_out, void* aux, size_t aux_bytes, void* workspace,
                               size_t ws_bytes, void* stream, tgl_tcsr** out) {
+    NvtxRange nvtx_("tgl_tcsr_build");
     if (!out || !indptr || n_edges < 0 || n_nodes < 0) return TGL_EINVAL;
     *out = nullptr;
     add_reverse = add_reverse ? 1 : 0;
@@ -333,6 +334,7 @@ extern "C" int tgl_tcsr_build_range(const int32_t* src, const int32_t* dst, cons
                                     int64_t n_local_stored, int64_t* indptr, int32_t* nbr, float* ts_out,
                                     int32_t* eid_out, void* aux, size_t aux_bytes, void* workspace, size_t ws_bytes,
                                     void* stream, tgl_tcsr** out) {
+    NvtxRange nvtx_("tgl_tcsr_build_range");
     if (!out || !indptr || n_edges < 0 || n_nodes < 0 || node_lo < 0 || node_hi < node_lo || node_hi > n_nodes ||
         n_local_stored < 0)
         return TGL_EINVAL;

@@ -104,6 +104,7 @@ using namespace tgl;
 
 extern "C" int tgl_gather(const int32_t* ids, int64_t n_ids_cap, const int64_t* n_ids_dev,
                           const tgl_gather_table* tables, int32_t n_tables, void* stream) {
+    NvtxRange nvtx_("tgl_gather");
     if (n_tables < 0 || n_tables > TGL_MAX_GATHER_TABLES || n_ids_cap < 0) return TGL_EINVAL;
     if (n_tables > 0 && !tables) return TGL_EINVAL;
     if (n_ids_cap > 0 && !ids) return TGL_EINVAL;

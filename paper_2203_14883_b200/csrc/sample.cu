@@ -1108,6 +1108,7 @@ static int sample_impl(const tgl_tcsr* g, const int32_t* roots, const float* roo
                        int32_t n_snapshots, float snapshot_len, uint64_t seed, uint64_t root_key_base,
                        const tgl_sample_options* opts, tgl_block* out, const tgl_dedup_block* dd,
                        void* workspace, size_t ws_bytes, void* stream) {
+    NvtxRange nvtx_("tgl_sample");
     if (!g || !out || !workspace) return TGL_EINVAL;
     tgl_sample_options o;
     memset(&o, 0, sizeof(o));

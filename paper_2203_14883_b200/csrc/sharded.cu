@@ -101,6 +101,7 @@ struct NcclTransport : Transport {
         if (comm) nccl().CommDestroy(comm);
     }
     int exchange(const Field* f, int nf, cudaStream_t st) override {
+    NvtxRange nvtx_("exchange (NCCL)");
         NcclApi& A = nccl();
         count(f, nf);
         if (A.GroupStart() != ncclSuccess) return TGL_ENCCL;
@@ -397,6 +398,7 @@ static unsigned grid_for(int64_t n) { return (unsigned)std::max<int64_t>(1, std:
 static int shard_chain(tgl_shard* sh, int l, int s0, int nsb, const int32_t* rn, const float* rt, const uint64_t* rk,
                        const float* rlo, int64_t n, int k, int strategy, float t_s, uint64_t seed, bool want_ts,
                        const tgl_block* const* out, int64_t* nnz_host, cudaStream_t st) {
+    NvtxRange nvtx_("shard_chain");
     const int W = sh->world;
     int rc = TGL_OK;
     // K8: bucket by owner
@@ -541,6 +543,7 @@ extern "C" int tgl_sample_sharded(tgl_shard* sh, const int32_t* roots, const flo
                                   int32_t n_layers, const int32_t* fanouts, tgl_strategy strategy, int32_t n_snapshots,
                                   float snapshot_len, uint64_t seed, uint64_t root_key_base, tgl_block* out,
                                   void* stream) {
+    NvtxRange nvtx_("tgl_sample_sharded");
     if (!sh || !out || !fanouts || n_roots < 0 || (n_roots > 0 && (!roots || !root_ts))) return TGL_EINVAL;
     const int L = n_layers, S = n_snapshots;
     int64_t roots_cap[64], edges_cap[64];
@@ -655,6 +658,7 @@ static int route(tgl_shard* sh, const int32_t* ids, int64_t n, cudaStream_t st, 
 
 extern "C" int tgl_shard_gather(tgl_shard* sh, const int32_t* ids, int64_t n, const tgl_gather_table* tables,
                                 int32_t n_tables, void* stream) {
+    NvtxRange nvtx_("tgl_shard_gather");
     if (!sh || n < 0 || (n > 0 && !ids) || n_tables < 1 || n_tables > TGL_MAX_GATHER_TABLES || !tables)
         return TGL_EINVAL;
     const int64_t lo = sh->splits[sh->rank], hi = sh->splits[sh->rank + 1];
@@ -702,6 +706,7 @@ extern "C" int tgl_shard_gather(tgl_shard* sh, const int32_t* ids, int64_t n, co
 extern "C" int tgl_shard_state_write(tgl_shard* sh, const int32_t* ids, const float* ts, int64_t n, int32_t K,
                                      int32_t* pos, float* ts_table, const tgl_state_table* tables, int32_t n_tables,
                                      void* stream) {
+    NvtxRange nvtx_("tgl_shard_state_write");
     // every rank exchanges the same fields (ids, times, rows): times are required whenever n > 0
     if (!sh || n < 0 || (n > 0 && (!ids || !ts)) || K < 1 || (K > 1 && !pos) || n_tables < 0 ||
         n_tables > TGL_MAX_GATHER_TABLES - 2 || (n_tables > 0 && !tables))

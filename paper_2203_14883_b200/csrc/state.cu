@@ -191,6 +191,7 @@ extern "C" int tgl_state_write_workspace(int64_t n_events, int32_t n_nodes, size
 extern "C" int tgl_state_write(const int32_t* ids, const float* ts, int64_t n_events, int32_t n_nodes, int32_t K,
                                int32_t* pos, float* ts_table, const tgl_state_table* tables, int32_t n_tables,
                                void* workspace, size_t ws_bytes, void* stream) {
+    NvtxRange nvtx_("tgl_state_write");
     if (n_events < 0 || n_nodes < 0 || n_events >= (int64_t(1) << 31) || K < 1) return TGL_EINVAL;
     if (n_tables < 0 || n_tables > TGL_MAX_GATHER_TABLES || (n_tables > 0 && !tables)) return TGL_EINVAL;
     if (K > 1 && !pos) return TGL_EINVAL;
