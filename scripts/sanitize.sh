@@ -4,7 +4,7 @@ tag=${1:-r02}
 out=gpurun_out/$tag/sanitizer; mkdir -p $out
 CS=/usr/local/cuda/bin/compute-sanitizer
 for tool in memcheck racecheck synccheck initcheck; do
-  timeout 1500 $CS --tool $tool --kernel-name regex:tgl --error-exitcode 9 --print-limit 50 \
+  timeout 1500 $CS --tool $tool --kernel-name kns=3tgl --error-exitcode 9 --print-limit 50 \
       python tools/sanitize_run.py > $out/$tool.log 2>&1
   echo "$tool rc=$?" | tee -a $out/summary.txt
   tail -3 $out/$tool.log
