@@ -287,6 +287,11 @@ __device__ __forceinline__ uint32_t select_valid(const SampleParams& p, int64_t 
     return take;
 }
 
+// word w of a node record parked in shared memory with its 16-byte chunks swizzled by sw
+__device__ __forceinline__ float rec_word(const float* rec, int sw, int w) {
+    return rec[(((w >> 2) ^ sw) << 2) | (w & 3)];
+}
+
 // ---------------------------------------------------------------------------- K4a windows
 template <int STRATEGY, bool VALID>
 __global__ void __launch_bounds__(kTile, VALID ? 6 : TGL_WINDOW_MINB) window_kernel(const __grid_constant__ SampleParams p) {
@@ -367,18 +372,17 @@ __global__ void __launch_bounds__(kTile, VALID ? 6 : TGL_WINDOW_MINB) window_ker
             if (lane / (32 / kRecHalves) == h) {
                 const int sw = (lane >> 1) & 3;
                 const float* rec = reinterpret_cast<const float*>(wrec + (lane % (32 / kRecHalves)) * 4);
-                auto word = [&](int w) { return rec[(((w >> 2) ^ sw) << 2) | (w & 3)]; };  // record word w
-                lo = __float_as_uint(word(0));
-                hi = __float_as_uint(word(1));
+                lo = __float_as_uint(rec_word(rec, sw, 0));
+                hi = __float_as_uint(rec_word(rec, sw, 1));
 #pragma unroll
                 for (int j = 0; j < 4; ++j) {
                     // number of fences f[0..13] (= words 2..15) below x[j]; positions >= 14 act as +inf
                     int c = 0;
 #pragma unroll
                     for (int step = 8; step >= 1; step >>= 1) {
-                        const int e = c + step - 1;
-                        const bool below = e < kFences && word(2 + min(e, kFences - 1)) < x[j];
-                        c += below ? step : 0;
+                        const int e = min(c + step - 1, kFences);
+                        const float f = rec_word(rec, sw, 2 + min(e, kFences - 1));
+                        c += (e < kFences && f < x[j]) ? step : 0;
                     }
                     packed |= (uint32_t)c << (8 * j);
                 }

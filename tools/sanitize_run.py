@@ -22,13 +22,14 @@ from synth.tiny import random_graph, random_roots  # noqa: E402
 
 
 def main():
-    V, E = 3000, 60000
+    small = os.environ.get("SANITIZE_SMALL") == "1"  # racecheck: fewer tiles (it is slow)
+    V, E = (800, 12000) if small else (3000, 60000)
     src, dst, ts, eid = random_graph(11, V, E, with_eid=True, integer_times=True)
     s, d, t, e = (torch.as_tensor(x).cuda() for x in (src, dst, ts, eid))
     g = tgl.build(s, d, t, e, n_nodes=V, add_reverse=True)
     go = oracle.build(src, dst, ts, eid, n_nodes=V, add_reverse=True)
     assert np.array_equal(g.indptr.cpu().numpy(), go["indptr"])
-    roots, rts = random_roots(5, V, 70_000)   # 274 tiles: super / hyper tile bases
+    roots, rts = random_roots(5, V, 20_000 if small else 70_000)   # 274 tiles: super tile bases
     r, rt = torch.as_tensor(roots).cuda(), torch.as_tensor(rts).cuda()
     for fan, strat, S, tsl, kw in (([10], "most_recent", 3, 5.0, {}), ([10, 5], "uniform", 1, math.inf, {}),
                                    ([4, 3], "uniform", 2, 20.0, {}), ([6], "uniform", 1, math.inf, {"replacement": True}),
@@ -40,7 +41,7 @@ def main():
         for b, o in zip(blocks, bo):
             off, nbr, _, dt, _ = b.trimmed()
             assert np.array_equal(off.cpu().numpy(), o["offsets"]) and np.array_equal(nbr.cpu().numpy(), o["nbr"])
-        bounds = torch.arange(0, r.numel() + 1, 7000, dtype=torch.int64, device="cuda")
+        bounds = torch.tensor(list(range(0, r.numel() + 1, 5000)), dtype=torch.int64, device="cuda")
         tgl.block_digest(blocks[0], bounds)
     valid = torch.full(((E + 31) // 32,), -1, dtype=torch.int32, device="cuda")
     tgl.edge_valid_set(valid, torch.arange(0, E, 3, dtype=torch.int32, device="cuda"), False, n_bits=E)
