@@ -472,12 +472,16 @@ __global__ void __launch_bounds__(kTile, VALID ? 6 : TGL_WINDOW_MINB) window_ker
 #pragma unroll
         for (int w = 0; w < kWarps; ++w) s += s_red[threadIdx.x][w];
         p.tile_tot[(size_t)threadIdx.x * p.tiles_cap + tile] = s;
-        atomicAdd(reinterpret_cast<unsigned long long*>(p.super_tot + (size_t)threadIdx.x * p.supers_cap +
-                                                        (tile >> kSuperShift)),
-                  (unsigned long long)s);
-        atomicAdd(reinterpret_cast<unsigned long long*>(p.hyper_tot + (size_t)threadIdx.x * p.hypers_cap +
-                                                        (tile >> (2 * kSuperShift))),
-                  (unsigned long long)s);
+        // super / hyper totals are read only for super tiles BEFORE a copy CTA's own: a grid of one
+        // super tile (per-batch calls) neither zeroes nor accumulates them
+        if (gridDim.x > (1u << kSuperShift)) {
+            atomicAdd(reinterpret_cast<unsigned long long*>(p.super_tot + (size_t)threadIdx.x * p.supers_cap +
+                                                            (tile >> kSuperShift)),
+                      (unsigned long long)s);
+            atomicAdd(reinterpret_cast<unsigned long long*>(p.hyper_tot + (size_t)threadIdx.x * p.hypers_cap +
+                                                            (tile >> (2 * kSuperShift))),
+                      (unsigned long long)s);
+        }
     }
     // programmatic dependent launch: the copy kernel may be scheduled once every window CTA got
     // here (its griddepcontrol.wait still waits for this grid's completion and memory flush)

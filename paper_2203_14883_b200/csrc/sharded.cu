@@ -429,7 +429,8 @@ static int shard_chain(tgl_shard* sh, int l, int s0, int nsb, const int32_t* rn,
         if ((rc = sh->tr->exchange(&f, 1, st))) return rc;
     }
     int64_t* h = sh->h_cnt;
-    if (cudaMemcpyAsync(h, cnt, sizeof(int64_t) * 512, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+    if (cudaMemcpyAsync(h, cnt, sizeof(int64_t) * W, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+        cudaMemcpyAsync(h + 256, cnt + 256, sizeof(int64_t) * W, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
         cudaStreamSynchronize(st) != cudaSuccess)
         return TGL_ECUDA;
     ++sh->host_syncs;
@@ -487,8 +488,9 @@ static int shard_chain(tgl_shard* sh, int l, int s0, int nsb, const int32_t* rn,
         Field f{esend_d, erecv_d, sizeof(int64_t), nsbv.data(), nsbv.data()};
         if ((rc = sh->tr->exchange(&f, 1, st))) return rc;
     }
-    if (cudaMemcpyAsync(h, cnt, sizeof(int64_t) * (512 + 2 * 256 * TGL_MAX_SNAPSHOTS), cudaMemcpyDeviceToHost, st) !=
-            cudaSuccess ||
+    if (cudaMemcpyAsync(h + 512, esend_d, sizeof(int64_t) * W * nsb, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+        cudaMemcpyAsync(h + 512 + 256 * TGL_MAX_SNAPSHOTS, erecv_d, sizeof(int64_t) * W * nsb, cudaMemcpyDeviceToHost,
+                        st) != cudaSuccess ||
         cudaStreamSynchronize(st) != cudaSuccess)
         return TGL_ECUDA;
     ++sh->host_syncs;
@@ -643,7 +645,8 @@ static int route(tgl_shard* sh, const int32_t* ids, int64_t n, cudaStream_t st, 
     Field f{cnt, cnt + 256, sizeof(int64_t), ones.data(), ones.data()};
     if ((rc = sh->tr->exchange(&f, 1, st))) return rc;
     int64_t* h = sh->h_cnt;
-    if (cudaMemcpyAsync(h, cnt, sizeof(int64_t) * 512, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+    if (cudaMemcpyAsync(h, cnt, sizeof(int64_t) * W, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+        cudaMemcpyAsync(h + 256, cnt + 256, sizeof(int64_t) * W, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
         cudaStreamSynchronize(st) != cudaSuccess)
         return TGL_ECUDA;
     ++sh->host_syncs;
