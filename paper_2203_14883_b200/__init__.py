@@ -169,6 +169,15 @@ class Block:
     uniq_ts: Optional[torch.Tensor] = None
     n_uniq_dev: Optional[torch.Tensor] = None
 
+    def batch(self, r0: int, r1: int):
+        """Views of roots [r0, r1) of this block -- e.g. one mini-batch of a many-batch (epoch-mode)
+        call: (offsets rebased to the batch, nbr, eid, dt[, ts_edge]).  Host-synchronising (reads
+        two offsets); no copies of the edge arrays."""
+        o = self.offsets[r0:r1 + 1]
+        e0, e1 = int(o[0].item()), int(o[-1].item())
+        te = None if self.ts_edge is None else self.ts_edge[e0:e1]
+        return o - e0, self.nbr[e0:e1], self.eid[e0:e1], self.dt[e0:e1], te
+
     def trimmed(self):
         """Host-synchronising view: (offsets[:n+1], nbr[:nnz], eid[:nnz], dt[:nnz], ts_edge[:nnz])."""
         n, nnz = int(self.n_roots_dev.item()), int(self.nnz_dev.item())

@@ -173,3 +173,36 @@ def test_c5_mag_full_size(tgl):
         assert hi - lo == ghi - glo
         np.testing.assert_array_equal(g.eid[glo:ghi].cpu().numpy(), go["eid"][lo:hi])
     _compare_call(tgl, cfg, g, go, src, dst, ts, batches)
+
+
+def test_c5_tcsr_full_digest(tgl):
+    """The WHOLE C5 T-CSR (121 M lists, 2.6 B slots) against the oracle's build, by digest: the
+    node range is cut into 8 parts; per part the oracle builds the lists of its nodes with its own
+    count / fill passes over the stream sub-selected to them (build_restricted), and 64 sub-ranges
+    per part are compared through tgl_block_digest over (indptr, nbr, eid, ts) -- FNV-1a of every
+    list element, so any difference anywhere in the 31 GB of lists fails."""
+    cfg = C.CONFIGS["C5"]
+    src, dst, ts = C.edges("C5", cfg, device="cuda")
+    g = tgl.build(src, dst, ts, n_nodes=cfg.n_nodes, add_reverse=True)
+    as_block = tgl.Block(offsets=g.indptr, nbr=g.nbr, eid=g.eid, dt=g.ts, ts_edge=None, n_roots_dev=None,
+                         nnz_dev=None)
+    V, parts, sub = cfg.n_nodes, 8, 64
+    for p in range(parts):
+        lo, hi = V * p // parts, V * (p + 1) // parts
+        nodes = torch.arange(lo, hi, dtype=torch.int32, device="cuda")
+        s_np, d_np, t_np, e_np, keep = C.relevant_substream(src, dst, ts, nodes, V, True)
+        go = oracle.build_restricted(lambda: iter([(s_np, d_np, t_np, e_np, 0)]), n_nodes=V, add_reverse=True, keep=keep)
+        del s_np, d_np, t_np, e_np
+        bounds = [lo + (hi - lo) * q // sub for q in range(sub + 1)]
+        gd = tgl.block_digest(as_block, torch.tensor(bounds, dtype=torch.int64, device="cuda")).cpu().numpy()
+        ip = go["indptr"]
+        od = []
+        for q in range(sub):
+            a, b = bounds[q], bounds[q + 1]
+            e0, e1 = int(ip[a]), int(ip[b])
+            od.append(oracle.block_digest({"offsets": ip[a:b + 1], "nbr": go["nbr"][e0:e1], "eid": go["eid"][e0:e1],
+                                           "dt": go["ts"][e0:e1]}))
+        np.testing.assert_array_equal(gd.view(np.uint64), np.array(od, dtype=np.uint64), err_msg=f"part {p}")
+        # the restricted oracle's indptr differences equal the GPU degrees on this part
+        np.testing.assert_array_equal(np.diff(ip[lo:hi + 1]), torch.diff(g.indptr[lo:hi + 1]).cpu().numpy())
+        del go

@@ -61,3 +61,21 @@ def test_c5_bench_call(tgl):
     for s0, (r, t) in zip(starts, rts):
         assert (r.numel() + 255) // 256 == 32000
         _check_call(tgl, cfg, g, go, r, t, s0)
+
+
+def test_batch_views_equal_per_batch_calls(tgl):
+    """A training loop samples many batches per call (epoch mode) and consumes per-batch views
+    (Block.batch): each view equals the per-batch call of that batch (R#7 keys)."""
+    cfg = C.CONFIGS["C1"]
+    src, dst, ts = C.edges("C1", cfg, device="cuda")
+    g = tgl.build(src, dst, ts, n_nodes=cfg.n_nodes, add_reverse=True)
+    B, M, s0 = cfg.batch, 50, 600 * 100
+    r, t = C.roots(cfg, src, dst, ts, s0, M * B)
+    many = tgl.Sampler(g, M * B, cfg.fanouts).run(r, t, seed=cfg.sampler_seed, root_key_base=s0)[0]
+    one = tgl.Sampler(g, B, cfg.fanouts)
+    for b in (0, 17, M - 1):
+        got = many.batch(b * B, (b + 1) * B)
+        want = one.run(r[b * B:(b + 1) * B], t[b * B:(b + 1) * B], seed=cfg.sampler_seed,
+                       root_key_base=s0 + b * B)[0].trimmed()
+        for x, y in zip(got[:4], want[:4]):
+            assert torch.equal(x, y)
