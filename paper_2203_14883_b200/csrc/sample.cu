@@ -130,6 +130,42 @@ __device__ __forceinline__ int64_t chain_roots(const SampleParams& p) {
     return n > 0 ? n : 0;
 }
 
+// Scattered reads of the sampler with an explicit L2 fill size: by default a B200 L2 miss fills
+// the whole 128-byte line (4 sectors); the ".L2::64B" qualifier fills 64 bytes (tools/granule.cu:
+// 127.7 -> 63.8 DRAM bytes per scattered 4-byte read, same request rate).  Node records are 64
+// bytes, cut probes 4 bytes and a root's selected slot records a run of <= k x 12 bytes.
+#ifndef TGL_L2_FILL64
+#define TGL_L2_FILL64 1
+#endif
+__device__ __forceinline__ float ld_rand_f32(const float* p) {
+#if TGL_L2_FILL64
+    float v;
+    asm("ld.global.nc.L2::64B.f32 %0, [%1];" : "=f"(v) : "l"(p));
+    return v;
+#else
+    return __ldg(p);
+#endif
+}
+__device__ __forceinline__ int32_t ld_rand_s32(const int32_t* p) {
+#if TGL_L2_FILL64
+    int32_t v;
+    asm("ld.global.nc.L2::64B.s32 %0, [%1];" : "=r"(v) : "l"(p));
+    return v;
+#else
+    return __ldg(p);
+#endif
+}
+__device__ __forceinline__ int4 ld_rand_v4(const int4* p) {
+#if TGL_L2_FILL64
+    int4 v;
+    asm("ld.global.nc.L2::64B.v4.s32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
+    return v;
+#else
+    return __ldg(p);
+#endif
+}
+
 // ---------------------------------------------------------------------------- cut search
 // first slot in [a, b) with ts >= x, else b (R#2).  Long lists first descend the 16-ary index
 // (tsindex.cuh): per level a binary search over <= 16 consecutive index entries (one 64-byte
@@ -164,7 +200,7 @@ __device__ __forceinline__ uint32_t lower_bound_ts(const SampleParams& p, uint32
     uint32_t lo = (uint32_t)A, hi = (uint32_t)B;
     while (lo < hi) {
         const uint32_t mid = lo + ((hi - lo) >> 1);
-        if (__ldg(p.ts + mid) < x)
+        if (ld_rand_f32(p.ts + mid) < x)
             lo = mid + 1;
         else
             hi = mid;
@@ -194,7 +230,7 @@ __device__ __forceinline__ void lower_bound_multi(const SampleParams& p, uint32_
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
             mid[j] = a[j] + ((b[j] - a[j]) >> 1);
-            v[j] = a[j] < b[j] ? __ldg(p.ts + mid[j]) : 0.0f;
+            v[j] = a[j] < b[j] ? ld_rand_f32(p.ts + mid[j]) : 0.0f;
         }
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
@@ -356,7 +392,7 @@ __global__ void __launch_bounds__(kTile, VALID ? 6 : TGL_WINDOW_MINB) window_ker
             const int src = q * 8 + quad;
             const int vq = __shfl_sync(kFull, v, src);
             const bool okq = __shfl_sync(kFull, ok, src);
-            ch[q] = okq ? __ldg(p.nodes + (size_t)vq * 4 + part)
+            ch[q] = okq ? ld_rand_v4(p.nodes + (size_t)vq * 4 + part)
                         : make_int4(part ? 0x7f800000 : 0, part ? 0x7f800000 : 0, 0x7f800000, 0x7f800000);
         }
         uint32_t packed = 0;
@@ -452,7 +488,7 @@ __global__ void __launch_bounds__(kTile, VALID ? 6 : TGL_WINDOW_MINB) window_ker
                 if (b == 0)                      // the first lower bound's fence gap (x[1] = xb)
                     a = min(lower_bound_ts(p, min(ga[1], bcur), min(gb[1], bcur), xb), bcur);
                 else
-                    a = __ldg(p.ts + bcur - 1) < xb ? bcur : lower_bound_ts(p, lo, bcur - 1, xb);
+                    a = ld_rand_f32(p.ts + bcur - 1) < xb ? bcur : lower_bound_ts(p, lo, bcur - 1, xb);
             }
             const uint32_t c = bcur - a;
             const uint32_t take = VALID ? (valid ? select_valid<STRATEGY>(p, i, b, a, bcur, rk0) : 0u)
@@ -701,10 +737,10 @@ __global__ void __launch_bounds__(kTile, STRATEGY == TGL_MOST_RECENT ? TGL_COPY_
             if (act[u]) {
                 if (p.recs) {
 #if TGL_REC_WORDS == 4
-                    rec[u] = __ldg(reinterpret_cast<const int4*>(p.recs) + pos[u]);
+                    rec[u] = ld_rand_v4(reinterpret_cast<const int4*>(p.recs) + pos[u]);
 #else
                     const int* w = reinterpret_cast<const int*>(p.recs + pos[u]);
-                    rec[u] = make_int4(__ldg(w), __ldg(w + 1), __ldg(w + 2), 0);
+                    rec[u] = make_int4(ld_rand_s32(w), ld_rand_s32(w + 1), ld_rand_s32(w + 2), 0);
 #endif
                 } else {
                     rec[u] = make_int4(__float_as_int(__ldg(p.ts + pos[u])), __ldg(p.nbr + pos[u]),
