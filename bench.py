@@ -185,15 +185,26 @@ def make_gather(tgl, cfg, sampler, dev):
     new_mail = torch.randn((cap_r, tabs["mailbox"].shape[1]), generator=gen, device=dev)
     writer = tgl.StateWriter(cfg.n_nodes, cap_r, device=dev)
 
-    def run(roots, block, events=None):
+    marks = []  # (gather start, gather end / state start, state end) events of timed steps
+
+    def run(roots, block, events=None, mark=False):
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)] if mark else None
+        if mark:
+            ev[0].record()
         tgl.gather(roots, node_tabs, outs=out_r)
         tgl.gather(block.nbr, node_tabs, n_ids_dev=block.nnz_dev, outs=out_n)
         tgl.gather(block.eid, [tabs["edge_feat"]], n_ids_dev=block.nnz_dev, outs=out_e)
+        if mark:
+            ev[1].record()
         if events is not None:
             ids, ets = events
             n = ids.numel()
             writer(ids, ets, [(new_mem[:n], tabs["memory"]), (new_mail[:n], tabs["mailbox"]), (ets, tabs["mail_ts"])],
                    K=1, ts_table=tabs["mem_ts"])
+        if mark:
+            ev[2].record()
+            marks.append(ev)
+    run.marks = marks
     return run
 
 
@@ -554,11 +565,11 @@ def run_ours(args):
             if id(r) not in events:
                 events[id(r)] = chunk_events(s0, r, t)
 
-    def step(j):
+    def step(j, mark=False):
         r, t = chunks[j]
         blocks = sampler.run(r, t, seed=cfg.sampler_seed, root_key_base=mine[j])
         if gather is not None:
-            gather(r, blocks[0], events[id(r)])
+            gather(r, blocks[0], events[id(r)], mark=mark)
         return blocks
 
     for w in range(args.warmup):
@@ -583,7 +594,7 @@ def run_ours(args):
             if flush:
                 flush_buf.fill_(j & 0xFF)
             ev[j][0].record()
-            step(args.warmup + j)
+            step(args.warmup + j, mark=True)
             ev[j][1].record()
         t_end.record()
         torch.cuda.synchronize(dev)
@@ -662,6 +673,21 @@ def run_ours(args):
         **({"oversubscribed": f"{world} ranks on {n_dev} GPU(s): launcher test, not a scaling number"}
            if oversub else {}),
     }
+
+    if gather is not None and gather.marks:
+        # Fig. 2 step 2 alone: the three gathers (node tables by roots and by sampled neighbours, edge
+        # features by sampled eids) against the HBM peak, and the state write (step 6) beside it
+        g_ms = sum(a.elapsed_time(b) for a, b, _ in gather.marks) / len(gather.marks)
+        s_ms = sum(b.elapsed_time(c) for _, b, c in gather.marks) / len(gather.marks)
+        gb = gather_bytes(cfg, roots_total // args.steps, int(edges_total // args.steps))
+        sb = state_bytes(cfg, int(np.mean([events[id(chunks[args.warmup + j][0])][0].numel() for j in range(args.steps)])))
+        out["gather_roofline"] = {"bound": "hbm", "bytes_per_step": gb, "ms_per_step": g_ms,
+                                  "achieved": gb / (g_ms / 1e3) / 1e9, "peak": peak, "unit": "GB/s",
+                                  "frac": gb / (g_ms / 1e3) / 1e9 / peak,
+                                  "note": "tgl_gather x 3 (node tables by roots and by nbr, 660 MB edge-feature table "
+                                          "by eid), CUDA events around the three launches of each timed step; bytes = "
+                                          "read + write of every gathered row (the node tables themselves are L2-resident)"}
+        out["state_write"] = {"bytes_per_step": sb, "ms_per_step": s_ms, "GBps": sb / (s_ms / 1e3) / 1e9}
 
     # per-batch mode (SURVEY 8(d) mode 1): one tgl_sample call per batch, replayed as a CUDA graph
     if not args.no_per_batch:

@@ -146,14 +146,20 @@ __device__ __forceinline__ float ld_rand_f32(const float* p) {
     return __ldg(p);
 #endif
 }
-__device__ __forceinline__ int32_t ld_rand_s32(const int32_t* p) {
-#if TGL_L2_FILL64
-    int32_t v;
-    asm("ld.global.nc.L2::64B.s32 %0, [%1];" : "=r"(v) : "l"(p));
-    return v;
-#else
-    return __ldg(p);
+// slot records (copy kernel): TGL_REC_FILL = the L2 fill of a record load (64, 128 or 256 bytes)
+#ifndef TGL_REC_FILL
+#define TGL_REC_FILL 128
 #endif
+__device__ __forceinline__ int32_t ld_rand_s32(const int32_t* p) {
+    int32_t v;
+#if TGL_REC_FILL == 64
+    asm("ld.global.nc.L2::64B.s32 %0, [%1];" : "=r"(v) : "l"(p));
+#elif TGL_REC_FILL == 256
+    asm("ld.global.nc.L2::256B.s32 %0, [%1];" : "=r"(v) : "l"(p));
+#else
+    asm("ld.global.nc.L2::128B.s32 %0, [%1];" : "=r"(v) : "l"(p));
+#endif
+    return v;
 }
 __device__ __forceinline__ int4 ld_rand_v4(const int4* p) {
 #if TGL_L2_FILL64
