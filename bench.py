@@ -236,6 +236,31 @@ def measured_traffic(key: str, roots_per_step: float):
     return d["bytes_per_root"] * roots_per_step, src
 
 
+def measured_random_access(key: str, roots_per_step: float, kern_ms: float):
+    """The sampler's binding resource on HBM-scale graphs: scattered DRAM requests (L2 misses).
+    Requests per root from the committed ncu capture (lts__t_requests_srcunit_tex_lookup_miss of
+    the sampler kernels), the peak request rate from tools/granule.cu in the same profiles dir."""
+    import glob
+    path = os.environ.get("TGL_TRAFFIC_JSON")
+    if not path:
+        cands = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*", "traffic.json")))
+        path = cands[-1] if cands else None
+    if not path or not os.path.exists(path):
+        return None
+    d = json.load(open(path)).get(key) or {}
+    pk = os.path.join(os.path.dirname(path), "granule_peak.json")
+    if "l2_miss_requests_per_root" not in d or not os.path.exists(pk):
+        return None
+    peak = json.load(open(pk))["peak_l2_miss_Greq_per_s"]
+    rpr = d["l2_miss_requests_per_root"]
+    achieved = rpr * roots_per_step / (kern_ms / 1e3) / 1e9
+    return {"bound": "dram_random_requests", "requests_per_root": rpr, "achieved": achieved, "peak": peak,
+            "unit": "G L2-miss requests/s", "frac": achieved / peak,
+            "source": f"{os.path.relpath(path, ROOT)} (ncu lts__t_requests_srcunit_tex_lookup_miss of the sampler "
+                      f"kernels) / {os.path.relpath(pk, ROOT)} (tools/granule.cu: 4-byte reads at random lines of "
+                      "32 GB)"}
+
+
 def measured_shares(key: str):
     """Per-kernel DRAM bytes per root and share of the sampler kernels' time in the committed ncu
     capture (same file as measured_traffic) -- for comparing with the live step time."""
@@ -653,6 +678,8 @@ def run_ours(args):
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic, "traffic_source": traffic_src, "peak_source": peak_src,
                      "kernels_ncu": measured_shares(key) if gather is None else None,
+                     "random_access": measured_random_access(key, roots_total / args.steps, kern_ms)
+                     if gather is None else None,
                      "kernel": (f"tgl_sample ({cfg.strategy}): window_kernel + copy_kernel"
                                 + (" + tgl_gather (3 launches) + tgl_state_write" if gather is not None else "")
                                 + ", timed together"),
