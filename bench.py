@@ -249,14 +249,14 @@ def measured_random_access(key: str, roots_per_step: float, kern_ms: float):
         return None
     d = json.load(open(path)).get(key) or {}
     pk = os.path.join(os.path.dirname(path), "granule_peak.json")
-    if "l2_miss_requests_per_root" not in d or not os.path.exists(pk):
+    if "l2_read_miss_requests_per_root" not in d or not os.path.exists(pk):
         return None
-    peak = json.load(open(pk))["peak_l2_miss_Greq_per_s"]
-    rpr = d["l2_miss_requests_per_root"]
+    peak = json.load(open(pk))["peak_l2_read_miss_Greq_per_s"]
+    rpr = d["l2_read_miss_requests_per_root"]
     achieved = rpr * roots_per_step / (kern_ms / 1e3) / 1e9
     return {"bound": "dram_random_requests", "requests_per_root": rpr, "achieved": achieved, "peak": peak,
-            "unit": "G L2-miss requests/s", "frac": achieved / peak,
-            "source": f"{os.path.relpath(path, ROOT)} (ncu lts__t_requests_srcunit_tex_lookup_miss of the sampler "
+            "unit": "G L2-missing read requests/s", "frac": achieved / peak,
+            "source": f"{os.path.relpath(path, ROOT)} (ncu lts__t_requests_srcunit_tex_op_read_lookup_miss of the sampler "
                       f"kernels) / {os.path.relpath(pk, ROOT)} (tools/granule.cu: 4-byte reads at random lines of "
                       "32 GB)"}
 
