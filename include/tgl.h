@@ -47,7 +47,7 @@ extern "C" {
 #define TGL_API
 #endif
 
-#define TGL_ABI_VERSION 1
+#define TGL_ABI_VERSION 2
 
 enum {
     TGL_OK = 0,
@@ -231,7 +231,32 @@ typedef struct {
     const uint32_t *edge_valid; /* device bitmask over edge ids (bit e of word e/32; R#28) or NULL:
                                    an edge whose bit is 0 is not a candidate ("invalid edges could
                                    be simply ignored"); maintained by tgl_edge_valid_set */
+    const struct tgl_fused_gather *gather; /* host pointer or NULL: fused gather of the last layer's
+                                   outputs (see tgl_fused_gather below; ABI version 2) */
 } tgl_sample_options;
+
+/*
+ * Fused gather (Fig. 2 step 2): while the copy kernel writes the
+ * last layer's block, it also fills, for every output i of that block, out_t[i] = table_t[id] with
+ * id = the output's source node (nbr[i]; node memory, mailbox, their timestamps) or its edge id
+ * (eid[i]; edge features) -- the rows of tgl_gather without a second pass over the block.  Rows
+ * that are a multiple of 16 bytes (and 16-byte aligned) are copied by a warp per row, narrower
+ * ones lane per row (4-byte multiples).  An id outside [0, n_rows) gives a zero row and, unless -1,
+ * the sticky ERANGE of the handle.  Supported when the last layer has ONE block (n_snapshots == 1)
+ * and without edge validity or dedup (TGL_EINVAL otherwise); out_t needs >= edges_cap[L-1] rows.
+ */
+#define TGL_MAX_FUSED_GATHER 4
+typedef struct {
+    const void *table; /* device [n_rows * row_bytes] */
+    int64_t n_rows;
+    int64_t row_bytes; /* > 0, a multiple of 4 */
+    void *out;         /* device [edges_cap * row_bytes], row i = output i of the block */
+    int32_t by_edge;   /* 0: rows of the source node (nbr), 1: rows of the edge (eid) */
+} tgl_fused_table;
+typedef struct tgl_fused_gather {
+    int32_t n_tables;  /* 1 .. TGL_MAX_FUSED_GATHER */
+    tgl_fused_table tables[TGL_MAX_FUSED_GATHER];
+} tgl_fused_gather;
 
 /*
  * dedup = 1 (R#27, SPEC's message-flow-graph node lists): for every block (l, s) the library also

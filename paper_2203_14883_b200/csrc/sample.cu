@@ -84,6 +84,24 @@ struct BlockOut {
     int64_t* nnz_dev;
 };
 
+// Fused gather (Fig. 2 step 2): the copy kernel also copies, for every output
+// it writes, the row of its source node (node memory / mailbox / their times) or of its edge (edge
+// features) from caller tables into caller outputs at the output's index.  Rows that are whole
+// 16-byte chunks are copied by the whole warp per output; narrower rows lane per output.
+constexpr int kMaxFused = TGL_MAX_FUSED_GATHER;
+struct FusedTable {
+    const void* table;
+    void* out;
+    int64_t n_rows;
+    uint32_t chunks16;  // row_bytes / 16 when rows are 16-byte chunks (and aligned), else 0
+    uint32_t words;     // row_bytes / 4 otherwise
+    int32_t by_edge;    // 0: indexed by the output's source node (nbr), 1: by its edge id (eid)
+};
+struct FusedGather {
+    int32_t n;
+    FusedTable t[kMaxFused];
+};
+
 struct SampleParams {
     const int64_t* indptr;
     const int32_t* nbr;
@@ -118,6 +136,7 @@ struct SampleParams {
     int64_t roots_cap, tiles_cap;
     uint32_t* picks_global;  // null -> picks in shared memory; else [tiles_cap * 8 warps][nsb*k][32]
     int* err;
+    FusedGather fg;  // optional row gather of the outputs (last layer, one block)
     BlockOut out[TGL_MAX_SNAPSHOTS];
 };
 
@@ -530,6 +549,34 @@ __global__ void __launch_bounds__(kTile, VALID ? 6 : TGL_WINDOW_MINB) window_ker
     asm volatile("griddepcontrol.launch_dependents;");
 }
 
+// the fused gather of one group of (up to 32) outputs held one per lane
+__device__ __forceinline__ void fused_gather_rows(const SampleParams& p, bool act, int64_t gi, int32_t nbr,
+                                                  int32_t eid, int lane) {
+    for (int j = 0; j < p.fg.n; ++j) {
+        const FusedTable& T = p.fg.t[j];
+        const int32_t id = T.by_edge ? eid : nbr;
+        const bool inr = id >= 0 && (int64_t)id < T.n_rows;
+        if (act && !inr && id != -1) atomicOr(p.err, kErrRange);  // as tgl_gather: zero row + ERANGE
+        if (T.chunks16) {  // whole warp per output row, 16-byte chunks
+            uint32_t m = __ballot_sync(kFull, act);
+            while (m) {
+                const int q = __ffs(m) - 1;
+                m &= m - 1;
+                const int32_t idq = __shfl_sync(kFull, id, q);
+                const int64_t gq = __shfl_sync(kFull, gi, q);
+                const bool okq = __shfl_sync(kFull, inr, q);
+                const int4* src = reinterpret_cast<const int4*>(T.table) + (int64_t)idq * T.chunks16;
+                int4* dst = reinterpret_cast<int4*>(T.out) + gq * T.chunks16;
+                for (uint32_t c = lane; c < T.chunks16; c += 32) dst[c] = okq ? __ldg(src + c) : make_int4(0, 0, 0, 0);
+            }
+        } else if (act) {  // narrow rows (e.g. one timestamp): lane per output
+            const int32_t* src = reinterpret_cast<const int32_t*>(T.table) + (int64_t)id * T.words;
+            int32_t* dst = reinterpret_cast<int32_t*>(T.out) + gi * T.words;
+            for (uint32_t w = 0; w < T.words; ++w) dst[w] = inr ? __ldg(src + w) : 0;
+        }
+    }
+}
+
 // ---------------------------------------------------------------------------- K4b copy
 // Per warp shared memory (words): inclusive counts [nsb][32]; segment list [nsb*32] of uint2
 // {start << 9 | b << 5 | r, first slot} (the warp's non-empty (block, root) windows in output
@@ -541,8 +588,10 @@ __host__ __device__ inline int copy_warp_words(int nsb, int k, bool picks_in_sme
 
 // PSMEM: uniform picks in shared memory (known at compile time, so LDS/STS instead of generic
 // 64-bit accesses); else in the global workspace
-template <int STRATEGY, bool VALID, bool EXTRA, bool PSMEM>
-__global__ void __launch_bounds__(kTile, STRATEGY == TGL_MOST_RECENT ? TGL_COPY_MINB_MR : TGL_COPY_MINB) copy_kernel(const __grid_constant__ SampleParams p) {
+template <int STRATEGY, bool VALID, int OUTX, bool PSMEM>
+__global__ void __launch_bounds__(kTile, OUTX == 2 ? 6 : (STRATEGY == TGL_MOST_RECENT ? TGL_COPY_MINB_MR : TGL_COPY_MINB)) copy_kernel(const __grid_constant__ SampleParams p) {
+    constexpr bool EXTRA = OUTX == 1;   // per-output data for a following layer / dedup
+    constexpr bool GATHER = OUTX == 2;  // fused row gather of the last layer's outputs
     extern __shared__ __align__(16) uint32_t smem[];
     __shared__ uint32_t s_wsum[TGL_MAX_SNAPSHOTS][kWarps];
     __shared__ uint64_t s_tbase[TGL_MAX_SNAPSHOTS];
@@ -784,6 +833,17 @@ __global__ void __launch_bounds__(kTile, STRATEGY == TGL_MOST_RECENT ? TGL_COPY_
                                                   : p.root_lo[warp_root0 + r];
             }
         }
+        if (GATHER) {
+#pragma unroll
+            for (int u = 0; u < kCopyUnroll; ++u) {
+                int64_t gi = 0;
+                if (act[u]) {
+                    const uint32_t b = (info[u] >> 5) & 15u;
+                    gi = (int64_t)((reinterpret_cast<int32_t*>(wptr[b * 4]) + oo[u]) - p.out[b].nbr);
+                }
+                fused_gather_rows(p, act[u], gi, rec[u].y, rec[u].z, lane);
+            }
+        }
     }
 }
 
@@ -959,16 +1019,16 @@ static int plan_sample(int64_t n_roots, int L, const int32_t* fanouts, int S, in
     return TGL_OK;
 }
 
-template <int STRATEGY, bool VALID, bool EXTRA, bool PSMEM>
+template <int STRATEGY, bool VALID, int OUTX, bool PSMEM>
 static void launch_copy_ps(const SampleParams& sp, int64_t grid, size_t smem, cudaStream_t st) {
     if (smem + 1024 > 48 * 1024)  // the dynamic part plus ~640 B of static shared memory
-        cudaFuncSetAttribute(copy_kernel<STRATEGY, VALID, EXTRA, PSMEM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaFuncSetAttribute(copy_kernel<STRATEGY, VALID, OUTX, PSMEM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)smem);
     // programmatic dependent launch (PDL): the copy grid is launched while the window grid's last
     // CTAs finish and waits in griddepcontrol.wait -- hides the launch gap between the two
     static const bool no_pdl = getenv("TGL_NO_PDL") != nullptr;  // A/B knob
     if (no_pdl) {
-        copy_kernel<STRATEGY, VALID, EXTRA, PSMEM><<<(unsigned)grid, kTile, smem, st>>>(sp);
+        copy_kernel<STRATEGY, VALID, OUTX, PSMEM><<<(unsigned)grid, kTile, smem, st>>>(sp);
         return;
     }
     cudaLaunchConfig_t cfg = {};
@@ -981,15 +1041,15 @@ static void launch_copy_ps(const SampleParams& sp, int64_t grid, size_t smem, cu
     at[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    cudaLaunchKernelEx(&cfg, copy_kernel<STRATEGY, VALID, EXTRA, PSMEM>, sp);
+    cudaLaunchKernelEx(&cfg, copy_kernel<STRATEGY, VALID, OUTX, PSMEM>, sp);
 }
 
-template <int STRATEGY, bool VALID, bool EXTRA>
+template <int STRATEGY, bool VALID, int OUTX>
 static void launch_copy(const SampleParams& sp, int64_t grid, size_t smem, cudaStream_t st) {
     if (STRATEGY == TGL_UNIFORM && sp.picks_global == nullptr)
-        launch_copy_ps<STRATEGY, VALID, EXTRA, true>(sp, grid, smem, st);
+        launch_copy_ps<STRATEGY, VALID, OUTX, true>(sp, grid, smem, st);
     else
-        launch_copy_ps<STRATEGY, VALID, EXTRA, false>(sp, grid, smem, st);
+        launch_copy_ps<STRATEGY, VALID, OUTX, false>(sp, grid, smem, st);
 }
 
 // EXTRA: the chain writes per-output data for a following layer or the dedup (ts_edge, child
@@ -1001,9 +1061,11 @@ static int launch_pair(const SampleParams& sp, int64_t grid, size_t smem, cudaSt
     for (int b = 0; b < sp.nsb; ++b)
         extra |= sp.out[b].ts_edge || sp.out[b].child_key || sp.out[b].child_t || sp.out[b].child_lo;
     if (extra)
-        launch_copy<STRATEGY, VALID, true>(sp, grid, smem, st);
+        launch_copy<STRATEGY, VALID, 1>(sp, grid, smem, st);
+    else if (!VALID && sp.fg.n > 0)  // fused gather: last-layer chains only (never with extra data)
+        launch_copy<STRATEGY, false, 2>(sp, grid, smem, st);
     else
-        launch_copy<STRATEGY, VALID, false>(sp, grid, smem, st);
+        launch_copy<STRATEGY, VALID, 0>(sp, grid, smem, st);
     return cudaGetLastError() == cudaSuccess ? TGL_OK : TGL_ECUDA;
 }
 
@@ -1170,6 +1232,23 @@ static int sample_impl(const tgl_tcsr* g, const int32_t* roots, const float* roo
         if (o.reserved[q]) return TGL_EINVAL;
     const bool hop_root = o.hop_time == TGL_HOP_ROOT_TIME;
     const bool dedup = o.dedup == 1;
+    FusedGather fg;
+    memset(&fg, 0, sizeof(fg));
+    if (o.gather) {  // fused gather of the last layer's block
+        const tgl_fused_gather& G = *o.gather;
+        if (G.n_tables < 1 || G.n_tables > TGL_MAX_FUSED_GATHER || n_snapshots != 1 || dedup || o.edge_valid)
+            return TGL_EINVAL;
+        fg.n = G.n_tables;
+        for (int j = 0; j < G.n_tables; ++j) {
+            const tgl_fused_table& t = G.tables[j];
+            if (!t.out || t.row_bytes <= 0 || (t.row_bytes & 3) || t.n_rows < 0 || (t.n_rows > 0 && !t.table) ||
+                (t.by_edge != 0 && t.by_edge != 1))
+                return TGL_EINVAL;
+            const bool v16 = (t.row_bytes % 16) == 0 && ((uintptr_t)t.table % 16) == 0 && ((uintptr_t)t.out % 16) == 0;
+            fg.t[j] = FusedTable{t.table, t.out, t.n_rows, v16 ? (uint32_t)(t.row_bytes / 16) : 0u,
+                                 (uint32_t)(t.row_bytes / 4), t.by_edge};
+        }
+    }
     if (n_roots > 0 && (!roots || !root_ts)) return TGL_EINVAL;
     static thread_local SamplePlan P;
     int rc = plan_sample(n_roots, n_layers, fanouts, n_snapshots, (int)strategy, snapshot_len, dedup, hop_root,
@@ -1278,6 +1357,7 @@ static int sample_impl(const tgl_tcsr* g, const int32_t* roots, const float* roo
         sp.tiles_cap = la.tiles_cap;
         sp.picks_global = la.picks;
         sp.err = g->err_dev;
+        if (l == L - 1) sp.fg = fg;  // the fused gather rides on the last layer's copy kernel
         for (int b = 0; b < la.nsb; ++b) {
             const int bs = l == 0 ? b : s;  // snapshot of output b
             const tgl_block& ob = out[l * S + bs];
