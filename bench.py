@@ -167,13 +167,19 @@ def state_write_launches(tgl, cfg, K: int = 1) -> int:
     return 1 + 5 * max(1, (bits + 7) // 8) + 2 + (1 if K > 1 else 0)
 
 
-def make_gather(tgl, cfg, sampler, dev):
+def fused_spec(tabs):
+    """Fused gather (tgl_fused_gather): the copy kernel writes each sampled edge's node rows (memory,
+    mem_ts, mailbox) and edge-feature row; mail_ts stays with the roots' separate gather."""
+    return [(tabs["memory"], "node"), (tabs["mem_ts"], "node"), (tabs["mailbox"], "node"), (tabs["edge_feat"], "edge")]
+
+
+def make_gather(tgl, cfg, sampler, dev, tabs=None, fused=False):
     """C3 data path of Fig. 2: step 2 -- memory, mem_ts, mailbox, mail_ts for the roots
     and sampled neighbours, edge features for the sampled eids (preallocated outputs, device-side
     counts) -- and step 6 -- the batch's events write their new memory (mem_ts) and mail (mail_ts)
     into the node tables (tgl_state_write, K = 1, R#25).  The new rows are the memory updater's /
     mail builder's outputs (model code, out of scope): resident synthetic rows stand in."""
-    tabs = C.tables(cfg, device=dev)
+    tabs = C.tables(cfg, device=dev) if tabs is None else tabs
     node_tabs = [tabs[k] for k in ("memory", "mem_ts", "mailbox", "mail_ts")]
     cap_r, cap_e = sampler.roots_cap[0], sampler.edges_cap[0]
     out_r = [torch.empty((cap_r,) + tuple(t.shape[1:]), dtype=t.dtype, device=dev) for t in node_tabs]
@@ -192,8 +198,11 @@ def make_gather(tgl, cfg, sampler, dev):
         if mark:
             ev[0].record()
         tgl.gather(roots, node_tabs, outs=out_r)
-        tgl.gather(block.nbr, node_tabs, n_ids_dev=block.nnz_dev, outs=out_n)
-        tgl.gather(block.eid, [tabs["edge_feat"]], n_ids_dev=block.nnz_dev, outs=out_e)
+        if fused:  # the sampler's copy kernel wrote memory / mem_ts / mailbox / edge rows; mail_ts here
+            tgl.gather(block.nbr, [tabs["mail_ts"]], n_ids_dev=block.nnz_dev, outs=[out_n[3]])
+        else:
+            tgl.gather(block.nbr, node_tabs, n_ids_dev=block.nnz_dev, outs=out_n)
+            tgl.gather(block.eid, [tabs["edge_feat"]], n_ids_dev=block.nnz_dev, outs=out_e)
         if mark:
             ev[1].record()
         if events is not None:
@@ -578,14 +587,17 @@ def run_ours(args):
     chunks = [C.roots(cfg, src, dst, ts, s0, chunk) for s0 in mine]
     mine = [mine[j % n_distinct] for j in range(args.warmup + args.steps)]
     chunks = [chunks[j % n_distinct] for j in range(args.warmup + args.steps)]
-    sampler = tgl.Sampler(g, chunk, cfg.fanouts, cfg.strategy, cfg.n_snapshots, cfg.snapshot_len)
+    fused = bool(args.fused_gather and cfg.tables)
+    tabs = C.tables(cfg, device=dev) if fused else None
+    sampler = tgl.Sampler(g, chunk, cfg.fanouts, cfg.strategy, cfg.n_snapshots, cfg.snapshot_len,
+                          fused_gather=fused_spec(tabs) if fused else None)
     L, S = len(cfg.fanouts), cfg.n_snapshots
     launches_per_step = 2 * (1 + (L - 1) * S)  # window + copy kernel per chain (+1 memset, not ours)
-    gather = make_gather(tgl, cfg, sampler, dev) if cfg.tables else None
+    gather = make_gather(tgl, cfg, sampler, dev, tabs=tabs, fused=fused) if cfg.tables else None
     events = {}
     if gather is not None:
-        # node tables by roots, node tables by nbr, edge features by eid; the state write
-        launches_per_step += 3 + state_write_launches(tgl, cfg)
+        # node tables by roots, node tables by nbr, edge features by eid (fused: roots + mail_ts); state write
+        launches_per_step += (2 if fused else 3) + state_write_launches(tgl, cfg)
         for (r, t), s0 in zip(chunks, mine):
             if id(r) not in events:
                 events[id(r)] = chunk_events(s0, r, t)
@@ -669,6 +681,7 @@ def run_ours(args):
         "config": {"workload": workload_name(key, cfg),
                    "batch_roots": B, "batches_per_step": M, "roots_per_step_per_gpu": chunk,
                    "parallelism": f"root-sharded dp{world}, replicated T-CSR",
+                   **({"fused_gather": "tgl_fused_gather: edge rows written by the copy kernel"} if fused else {}),
                    "l2": (f"flushed: T-CSR + aux ({graph_bytes / 2**20:.0f} MiB) fit L2, so a {4 * l2_bytes >> 20} MiB "
                           "buffer is written between timed steps; time = sum of the per-step CUDA-event "
                           "intervals (flush excluded); the e2e leg is a host-fed pipeline, not flushed"
@@ -701,7 +714,7 @@ def run_ours(args):
            if oversub else {}),
     }
 
-    if gather is not None and gather.marks:
+    if gather is not None and gather.marks and not fused:
         # Fig. 2 step 2 alone: the three gathers (node tables by roots and by sampled neighbours, edge
         # features by sampled eids) against the HBM peak, and the state write (step 6) beside it
         g_ms = sum(a.elapsed_time(b) for a, b, _ in gather.marks) / len(gather.marks)
@@ -1106,6 +1119,8 @@ def main():
     ap.add_argument("--sharding", default="root", choices=["root", "node"],
                     help="root: replicated T-CSR, roots sharded (default); node: node-sharded T-CSR (SURVEY 8(e))")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--fused-gather", action="store_true",
+                    help="configs with tables (C3): the copy kernel writes the sampled edges' rows (tgl_fused_gather)")
     ap.add_argument("--dry-run", action="store_true", help=argparse.SUPPRESS)  # host logic only (gloo, no GPU)
     args = ap.parse_args()
     world_env = os.environ.get("WORLD_SIZE")

@@ -219,7 +219,7 @@ class Sampler:
     def __init__(self, g: TCSR, max_roots: int, fanouts: Sequence[int], strategy="most_recent",
                  n_snapshots: int = 1, snapshot_len: float = math.inf, device=None, want_ts_edge_last=False,
                  hop_time: str = "edge", replacement: bool = False, dedup: bool = False,
-                 edge_valid: Optional[torch.Tensor] = None):
+                 edge_valid: Optional[torch.Tensor] = None, fused_gather=None):
         """hop_time: "edge" (R#4) or "root" (R#23, hop roots carry the root time); replacement:
         uniform with replacement (R#24); dedup: per-block distinct (node, hop time) lists feeding
         the next layer (R#27); edge_valid: int32/uint32 CUDA bitmask over edge ids (R#28), invalid
@@ -234,7 +234,18 @@ class Sampler:
             if not (edge_valid.is_cuda and edge_valid.dtype in (torch.int32, torch.uint32) and edge_valid.is_contiguous()):
                 raise TypeError("edge_valid must be a contiguous CUDA int32/uint32 bitmask")
             self._opts.edge_valid = edge_valid.data_ptr()
-        self._default_opts = hop_time == "edge" and not replacement and not dedup and edge_valid is None
+        self.fused_outs = []
+        if fused_gather:
+            # tgl_fused_gather: [(table, "node" | "edge")] -> rows of the last layer's outputs, written by the
+            # copy kernel into self.fused_outs[j] ([edges_cap, ...], row i = output i of the last block)
+            if len(fused_gather) > _lib.MAX_FUSED_GATHER:
+                raise ValueError("too many fused gather tables")
+            self._fg = _lib.FusedGather()
+            self._fg.n_tables = len(fused_gather)
+            self._fused_spec = list(fused_gather)
+            self._opts.gather = ctypes.pointer(self._fg)
+        self._default_opts = hop_time == "edge" and not replacement and not dedup and edge_valid is None \
+            and not fused_gather
         self.dedup = bool(dedup)
         if dedup and hop_time == "edge":
             want_ts_edge_last = True
@@ -262,6 +273,14 @@ class Sampler:
                 self._c_dedup[j] = _lib.DedupBlock(ec_[l], b.src_index.data_ptr(), b.uniq_node.data_ptr(),
                                                    b.uniq_ts.data_ptr(), b.n_uniq_dev.data_ptr())
         self._c_blocks = _c_blocks(self.blocks, rc_, ec_, self.S)
+        if fused_gather:
+            for j, (t, by) in enumerate(self._fused_spec):
+                if by not in ("node", "edge") or not (t.is_cuda and t.is_contiguous()):
+                    raise ValueError("fused gather: (contiguous CUDA table, 'node' | 'edge')")
+                rb = t.element_size() * int(np.prod(t.shape[1:], dtype=np.int64))
+                o = torch.empty((ec_[-1],) + tuple(t.shape[1:]), dtype=t.dtype, device=dev)
+                self.fused_outs.append(o)
+                self._fg.tables[j] = _lib.FusedTable(t.data_ptr(), t.shape[0], rb, o.data_ptr(), 1 if by == "edge" else 0)
         self._fan = (ctypes.c_int32 * self.L)(*self.fanouts)
 
     def capacity(self, n_roots: int):

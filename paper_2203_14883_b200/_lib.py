@@ -26,9 +26,23 @@ class Block(ctypes.Structure):
                 ("ts_edge", P), ("n_roots_dev", P), ("nnz_dev", P)]
 
 
+MAX_FUSED_GATHER = 4
+
+
+class FusedTable(ctypes.Structure):
+    """tgl_fused_table (include/tgl.h)."""
+    _fields_ = [("table", P), ("n_rows", i64), ("row_bytes", i64), ("out", P), ("by_edge", i32)]
+
+
+class FusedGather(ctypes.Structure):
+    """tgl_fused_gather (include/tgl.h)."""
+    _fields_ = [("n_tables", i32), ("tables", FusedTable * MAX_FUSED_GATHER)]
+
+
 class SampleOptions(ctypes.Structure):
     _fields_ = [("hop_time", ctypes.c_int32), ("replacement", ctypes.c_int32), ("dedup", ctypes.c_int32),
-                ("reserved", ctypes.c_int32 * 5), ("edge_valid", ctypes.c_void_p)]
+                ("reserved", ctypes.c_int32 * 5), ("edge_valid", ctypes.c_void_p),
+                ("gather", ctypes.POINTER(FusedGather))]
 
 
 class DedupBlock(ctypes.Structure):
