@@ -587,7 +587,7 @@ def run_ours(args):
     chunks = [C.roots(cfg, src, dst, ts, s0, chunk) for s0 in mine]
     mine = [mine[j % n_distinct] for j in range(args.warmup + args.steps)]
     chunks = [chunks[j % n_distinct] for j in range(args.warmup + args.steps)]
-    fused = bool(args.fused_gather and cfg.tables)
+    fused = bool(cfg.tables) and not args.separate_gather
     tabs = C.tables(cfg, device=dev) if fused else None
     sampler = tgl.Sampler(g, chunk, cfg.fanouts, cfg.strategy, cfg.n_snapshots, cfg.snapshot_len,
                           fused_gather=fused_spec(tabs) if fused else None)
@@ -720,10 +720,18 @@ def run_ours(args):
         g_ms = sum(a.elapsed_time(b) for a, b, _ in gather.marks) / len(gather.marks)
         s_ms = sum(b.elapsed_time(c) for _, b, c in gather.marks) / len(gather.marks)
         gb = gather_bytes(cfg, roots_total // args.steps, int(edges_total // args.steps))
+        node_row = sum(4 * cols for name, (rows, cols) in cfg.tables.items() if name != "edge_feat")
+        edge_row = 4 * cfg.tables["edge_feat"][1]
+        # HBM floor: every gathered row is written; of the reads only the edge features come from HBM
+        # (the 4 MB node tables stay in L2)
+        floor = (roots_total // args.steps + int(edges_total // args.steps)) * node_row \
+            + 2 * int(edges_total // args.steps) * edge_row
         sb = state_bytes(cfg, int(np.mean([events[id(chunks[args.warmup + j][0])][0].numel() for j in range(args.steps)])))
         out["gather_roofline"] = {"bound": "hbm", "bytes_per_step": gb, "ms_per_step": g_ms,
                                   "achieved": gb / (g_ms / 1e3) / 1e9, "peak": peak, "unit": "GB/s",
                                   "frac": gb / (g_ms / 1e3) / 1e9 / peak,
+                                  "hbm_floor_bytes_per_step": floor,
+                                  "frac_of_hbm_floor": floor / (g_ms / 1e3) / 1e9 / peak,
                                   "note": "tgl_gather x 3 (node tables by roots and by nbr, 660 MB edge-feature table "
                                           "by eid), CUDA events around the three launches of each timed step; bytes = "
                                           "read + write of every gathered row (the node tables themselves are L2-resident)"}
@@ -1119,8 +1127,9 @@ def main():
     ap.add_argument("--sharding", default="root", choices=["root", "node"],
                     help="root: replicated T-CSR, roots sharded (default); node: node-sharded T-CSR (SURVEY 8(e))")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--fused-gather", action="store_true",
-                    help="configs with tables (C3): the copy kernel writes the sampled edges' rows (tgl_fused_gather)")
+    ap.add_argument("--separate-gather", action="store_true",
+                    help="configs with tables (C3): gather the sampled edges' rows with separate tgl_gather launches "
+                         "instead of the copy kernel's fused gather (tgl_fused_gather, default)")
     ap.add_argument("--dry-run", action="store_true", help=argparse.SUPPRESS)  # host logic only (gloo, no GPU)
     args = ap.parse_args()
     world_env = os.environ.get("WORLD_SIZE")
