@@ -169,8 +169,9 @@ def state_write_launches(tgl, cfg, K: int = 1) -> int:
 
 def fused_spec(tabs):
     """Fused gather (tgl_fused_gather): the copy kernel writes each sampled edge's node rows (memory,
-    mem_ts, mailbox) and edge-feature row; mail_ts stays with the roots' separate gather."""
-    return [(tabs["memory"], "node"), (tabs["mem_ts"], "node"), (tabs["mailbox"], "node"), (tabs["edge_feat"], "edge")]
+    mem_ts, mailbox, mail_ts) and edge-feature row; only the roots' rows take a separate gather."""
+    return [(tabs["memory"], "node"), (tabs["mem_ts"], "node"), (tabs["mailbox"], "node"), (tabs["mail_ts"], "node"),
+            (tabs["edge_feat"], "edge")]
 
 
 def make_gather(tgl, cfg, sampler, dev, tabs=None, fused=False):
@@ -183,8 +184,8 @@ def make_gather(tgl, cfg, sampler, dev, tabs=None, fused=False):
     node_tabs = [tabs[k] for k in ("memory", "mem_ts", "mailbox", "mail_ts")]
     cap_r, cap_e = sampler.roots_cap[0], sampler.edges_cap[0]
     out_r = [torch.empty((cap_r,) + tuple(t.shape[1:]), dtype=t.dtype, device=dev) for t in node_tabs]
-    out_n = [torch.empty((cap_e,) + tuple(t.shape[1:]), dtype=t.dtype, device=dev) for t in node_tabs]
-    out_e = [torch.empty((cap_e, tabs["edge_feat"].shape[1]), dtype=torch.float32, device=dev)]
+    out_n = [] if fused else [torch.empty((cap_e,) + tuple(t.shape[1:]), dtype=t.dtype, device=dev) for t in node_tabs]
+    out_e = [] if fused else [torch.empty((cap_e, tabs["edge_feat"].shape[1]), dtype=torch.float32, device=dev)]
     gen = torch.Generator(device=dev)
     gen.manual_seed(cfg.seed)
     new_mem = torch.randn((cap_r, tabs["memory"].shape[1]), generator=gen, device=dev)
@@ -198,9 +199,7 @@ def make_gather(tgl, cfg, sampler, dev, tabs=None, fused=False):
         if mark:
             ev[0].record()
         tgl.gather(roots, node_tabs, outs=out_r)
-        if fused:  # the sampler's copy kernel wrote memory / mem_ts / mailbox / edge rows; mail_ts here
-            tgl.gather(block.nbr, [tabs["mail_ts"]], n_ids_dev=block.nnz_dev, outs=[out_n[3]])
-        else:
+        if not fused:  # (fused: the sampler's copy kernel wrote the sampled edges' rows)
             tgl.gather(block.nbr, node_tabs, n_ids_dev=block.nnz_dev, outs=out_n)
             tgl.gather(block.eid, [tabs["edge_feat"]], n_ids_dev=block.nnz_dev, outs=out_e)
         if mark:
@@ -597,7 +596,7 @@ def run_ours(args):
     events = {}
     if gather is not None:
         # node tables by roots, node tables by nbr, edge features by eid (fused: roots + mail_ts); state write
-        launches_per_step += (2 if fused else 3) + state_write_launches(tgl, cfg)
+        launches_per_step += (1 if fused else 3) + state_write_launches(tgl, cfg)
         for (r, t), s0 in zip(chunks, mine):
             if id(r) not in events:
                 events[id(r)] = chunk_events(s0, r, t)

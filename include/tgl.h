@@ -245,7 +245,7 @@ typedef struct {
  * the sticky ERANGE of the handle.  Supported when the last layer has ONE block (n_snapshots == 1)
  * and without edge validity or dedup (TGL_EINVAL otherwise); out_t needs >= edges_cap[L-1] rows.
  */
-#define TGL_MAX_FUSED_GATHER 4
+#define TGL_MAX_FUSED_GATHER 8
 typedef struct {
     const void *table; /* device [n_rows * row_bytes] */
     int64_t n_rows;

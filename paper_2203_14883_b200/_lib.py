@@ -26,7 +26,7 @@ class Block(ctypes.Structure):
                 ("ts_edge", P), ("n_roots_dev", P), ("nnz_dev", P)]
 
 
-MAX_FUSED_GATHER = 4
+MAX_FUSED_GATHER = 8
 
 
 class FusedTable(ctypes.Structure):
