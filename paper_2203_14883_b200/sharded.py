@@ -1,4 +1,13 @@
-"""Node-sharded sampling: the T-CSR split by node ranges over the ranks.
+"""Node-sharded sampling: the PROTOCOL MODEL in Python over torch.distributed.
+
+The product node-sharded path is behind the C ABI (include/tgl.h: tgl_tcsr_build_range,
+tgl_shard_create, tgl_sample_sharded, tgl_shard_gather, tgl_shard_state_write; Python:
+`ShardSampler`): NCCL send/recv groups inside the library, any number of layers.  This module keeps
+the same exchange written against torch.distributed all-to-all (pluggable ops / exchange), which
+runs with gloo on CPU (tests/test_sharded_gloo.py, world 2) -- the host-side model of the protocol
+-- and `edge_balanced_splits`, shared by both.
+
+Node-sharded sampling: the T-CSR split by node ranges over the ranks.
 
 For graphs larger than one GPU's HBM the T-CSR is split into contiguous node ranges balanced by
 edges; the node v is owned by shard r with splits[r] <= v < splits[r+1].  One sampling call:
