@@ -23,9 +23,9 @@ edges; the node v is owned by shard r with splits[r] <= v < splits[r+1].  One sa
 Steps 1, 2, 4, 6 are the library's kernels; 3 and 5 are the collective (the path's real exchange
 step).  The exchange object is pluggable: `DistExchange` (torch.distributed all_to_all_single:
 NCCL on GPUs, gloo on CPU tests) or a test double.  `ops` is pluggable the same way so the
-exchange protocol can be exercised on CPU with world_size 2 (tests/test_sharded_gloo.py); the
-product default is `CudaOps`, which only calls libtgl.so.  Single layer (the C5 configuration);
-multi-layer node-sharded sampling is NEXT in DESIGN.md.
+exchange protocol can be exercised on CPU with world_size 2 (tests/test_sharded_gloo.py); on a GPU
+`CudaOps` calls only libtgl.so.  Single layer (the C5 configuration); the multi-layer node-sharded
+sampler is the C-ABI one (`tgl_sample_sharded`).
 """
 from __future__ import annotations
 
