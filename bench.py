@@ -958,7 +958,8 @@ def parity_gate(args, cfg, tgl, sampler, src, dst, ts, chunks, mine, digests_by_
     n_thr = max(1, host_info()["cores_available"] // max(1, world))
     timed = [mine[args.warmup + j] for j in range(args.steps)]
     distinct = list(dict.fromkeys(timed))
-    n_chk = max(1, min(args.parity_chunks, len(distinct)))
+    # every rank checks its own chunks on the shared host: one chunk each at N > 1 (host RAM / cores)
+    n_chk = max(1, min(args.parity_chunks if world == 1 else 1, len(distinct)))
     pick = [distinct[(len(distinct) - 1) * c // max(1, n_chk - 1)] if n_chk > 1 else distinct[0] for c in range(n_chk)]
     pick = list(dict.fromkeys(pick))
     by_start = {s0: chunks[args.warmup + timed.index(s0)] for s0 in pick}
