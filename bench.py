@@ -743,7 +743,7 @@ def run_ours(args):
 
     # end to end through the public API with host buffers (rank-local), copies inside the region
     if not args.no_e2e:
-        gf = (lambda smp: make_gather(tgl, cfg, smp, dev)) if gather is not None else None
+        gf = (lambda smp: make_gather(tgl, cfg, smp, dev, tabs=tabs, fused=fused)) if gather is not None else None
         out["e2e"] = e2e(args, tgl, sampler, chunks, mine, cfg, dev, world, gather_factory=gf, cdev=cdev,
                          events=events if gather is not None else None)
         out["e2e_full_d2h"] = e2e(args, tgl, sampler, chunks, mine, cfg, dev, world, full_d2h=True, cdev=cdev)
@@ -842,7 +842,8 @@ def e2e(args, tgl, sampler, chunks, mine, cfg, dev, world, full_d2h=False, gathe
     d_ev = [(torch.empty(cap_r, dtype=torch.int32, device=dev), torch.empty(cap_r, dtype=torch.float32, device=dev))
             for _ in range(2)] if events is not None else None
     nb = L * S
-    smps = [sampler, tgl.Sampler(sampler.g, cap_r, cfg.fanouts, cfg.strategy, S, cfg.snapshot_len)]
+    smps = [sampler, tgl.Sampler(sampler.g, cap_r, cfg.fanouts, cfg.strategy, S, cfg.snapshot_len,
+                                 fused_gather=getattr(sampler, "_fused_spec", None) if sampler.fused_outs else None)]
     gathers = [gather_factory(smp) for smp in smps] if gather_factory is not None else None
     d_roots = [(torch.empty(cap_r, dtype=torch.int32, device=dev), torch.empty(cap_r, dtype=torch.float32, device=dev))
                for _ in range(2)]
