@@ -104,7 +104,7 @@ struct tgl_tcsr {
     const float* index;      // 16-ary atom index over ts (tsindex.cuh), or null
     int n_levels;
     uint64_t level_off[12];  // float offset of level l in index (levels <= 8)
-    const void* recs;        // 16-byte slot records {ts, nbr, eid, 0} (tsindex.cuh), or null
-    const void* nodes;       // 16-byte node records {lo, hi, ts_first, ts_last} (tsindex.cuh), or null
+    const void* recs;        // 12-byte slot records {ts, nbr, eid} (tsindex.cuh), or null
+    const void* nodes;       // 64-byte node records {lo, hi, 14 fences} (tsindex.cuh), or null
     int64_t node_lo;         // node-sharded handle: global id of local node 0
 };

@@ -22,7 +22,7 @@
 //                      uniform: Floyd's k-subset with Philox4x32-10 draws, ascending (R#5, R#6);
 //                      then the tile's outputs are copied as one flat range per snapshot -- lane o
 //                      finds its root by a 5-step search over the warp's inclusive counts -- loading
-//                      the selected 16-byte slot record {ts, nbr, eid} (one request per run of
+//                      the selected 12-byte slot record {ts, nbr, eid} (one request per run of
 //                      slots) and storing (nbr, eid, dt[, ts_edge, child key, child lo]) as
 //                      coalesced runs (a9, a10; K6 fused).
 // dt = t_root (-) t_edge with __fsub_rn; window bounds with __fmul_rn / __fsub_rn (R#12).
@@ -55,20 +55,10 @@ constexpr int kWarps = kTile / 32;
 #endif
 constexpr int kCopyUnroll = TGL_COPY_UNROLL;  // outputs in flight per lane in the flat copy
 constexpr int kSuperShift = 6;  // 64 tiles per super tile (tile bases: super totals + tile totals)
-#ifndef TGL_CUT0_MULTI
-#define TGL_CUT0_MULTI 0
-#endif
-#ifndef TGL_STCS
-#define TGL_STCS 0
-#endif
 #ifndef TGL_INDEX_MIN
 #define TGL_INDEX_MIN 4096  // C4 A/B: 256 73.9, 1024 74.5, 4096 75.3 G edges/s; C5 unchanged
 #endif
 constexpr uint32_t kIndexMin = TGL_INDEX_MIN;  // gaps longer than this descend the 16-ary index
-#ifndef TGL_REC_HALVES
-#define TGL_REC_HALVES 1
-#endif
-constexpr int kRecHalves = TGL_REC_HALVES;  // node records parked in shared memory in 1 or 2 rounds
 constexpr int kPicksSmemPerWarp = 8 * 1024;  // bytes of uniform picks kept in shared memory per warp
 
 struct BlockOut {
@@ -153,42 +143,23 @@ __device__ __forceinline__ int64_t chain_roots(const SampleParams& p) {
 // the whole 128-byte line (4 sectors); the ".L2::64B" qualifier fills 64 bytes (tools/granule.cu:
 // 127.7 -> 63.8 DRAM bytes per scattered 4-byte read, same request rate).  Node records are 64
 // bytes, cut probes 4 bytes and a root's selected slot records a run of <= k x 12 bytes.
-#ifndef TGL_L2_FILL64
-#define TGL_L2_FILL64 1
-#endif
 __device__ __forceinline__ float ld_rand_f32(const float* p) {
-#if TGL_L2_FILL64
     float v;
     asm("ld.global.nc.L2::64B.f32 %0, [%1];" : "=f"(v) : "l"(p));
     return v;
-#else
-    return __ldg(p);
-#endif
 }
-// slot records (copy kernel): TGL_REC_FILL = the L2 fill of a record load (64, 128 or 256 bytes)
-#ifndef TGL_REC_FILL
-#define TGL_REC_FILL 128
-#endif
+// slot records (copy kernel): a run of <= k 12-byte records, 128-byte fills (64 / 256: +-1 %,
+// profiles/r02/experiments/recfill_ktime_C5.txt)
 __device__ __forceinline__ int32_t ld_rand_s32(const int32_t* p) {
     int32_t v;
-#if TGL_REC_FILL == 64
-    asm("ld.global.nc.L2::64B.s32 %0, [%1];" : "=r"(v) : "l"(p));
-#elif TGL_REC_FILL == 256
-    asm("ld.global.nc.L2::256B.s32 %0, [%1];" : "=r"(v) : "l"(p));
-#else
     asm("ld.global.nc.L2::128B.s32 %0, [%1];" : "=r"(v) : "l"(p));
-#endif
     return v;
 }
 __device__ __forceinline__ int4 ld_rand_v4(const int4* p) {
-#if TGL_L2_FILL64
     int4 v;
     asm("ld.global.nc.L2::64B.v4.s32 {%0, %1, %2, %3}, [%4];"
-                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
+        : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
     return v;
-#else
-    return __ldg(p);
-#endif
 }
 
 // ---------------------------------------------------------------------------- cut search
@@ -357,7 +328,7 @@ __device__ __forceinline__ float rec_word(const float* rec, int sw, int w) {
 template <int STRATEGY, bool VALID>
 __global__ void __launch_bounds__(kTile, VALID ? 6 : TGL_WINDOW_MINB) window_kernel(const __grid_constant__ SampleParams p) {
     __shared__ uint32_t s_red[TGL_MAX_SNAPSHOTS][kWarps];
-    __shared__ int4 s_rec[kTile * 4 / kRecHalves];  // the tile's 64-byte node records (16 KB / halves)
+    __shared__ int4 s_rec[kTile * 4];  // the tile's 64-byte node records (16 KB)
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int64_t n = chain_roots(p);
     const int64_t tile = (int64_t)blockIdx.x;
@@ -409,7 +380,7 @@ __global__ void __launch_bounds__(kTile, VALID ? 6 : TGL_WINDOW_MINB) window_ker
         // at chunk slot c ^ ((r >> 1) & 3): the 8 lanes of a quarter-warp then read 8 distinct
         // bank groups); then every lane counts its own root's 14 fences below each cut time with a
         // branch-free binary search over the record (fences are sorted)
-        int4* wrec = s_rec + warp * (32 / kRecHalves) * 4;
+        int4* wrec = s_rec + warp * 32 * 4;
         const int quad = lane >> 2, part = lane & 3;
         int4 ch[4];
 #pragma unroll
@@ -420,34 +391,28 @@ __global__ void __launch_bounds__(kTile, VALID ? 6 : TGL_WINDOW_MINB) window_ker
             ch[q] = okq ? ld_rand_v4(p.nodes + (size_t)vq * 4 + part)
                         : make_int4(part ? 0x7f800000 : 0, part ? 0x7f800000 : 0, 0x7f800000, 0x7f800000);
         }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int src = q * 8 + quad;
+            wrec[src * 4 + (part ^ ((src >> 1) & 3))] = ch[q];
+        }
+        __syncwarp();
+        const int sw = (lane >> 1) & 3;
+        const float* rec = reinterpret_cast<const float*>(wrec + lane * 4);
+        lo = __float_as_uint(rec_word(rec, sw, 0));
+        hi = __float_as_uint(rec_word(rec, sw, 1));
         uint32_t packed = 0;
 #pragma unroll
-        for (int h = 0; h < kRecHalves; ++h) {  // kRecHalves = 2: roots 0-15, then 16-31 (8 KB per CTA)
-            if (h) __syncwarp();
+        for (int j = 0; j < 4; ++j) {
+            // number of fences f[0..13] (= words 2..15) below x[j]; positions >= 14 act as +inf
+            int c = 0;
 #pragma unroll
-            for (int q = h * 4 / kRecHalves; q < (h + 1) * 4 / kRecHalves; ++q) {
-                const int src = q * 8 + quad;
-                wrec[(src % (32 / kRecHalves)) * 4 + (part ^ ((src >> 1) & 3))] = ch[q];
+            for (int step = 8; step >= 1; step >>= 1) {
+                const int e = min(c + step - 1, kFences);
+                const float f = rec_word(rec, sw, 2 + min(e, kFences - 1));
+                c += (e < kFences && f < x[j]) ? step : 0;
             }
-            __syncwarp();
-            if (lane / (32 / kRecHalves) == h) {
-                const int sw = (lane >> 1) & 3;
-                const float* rec = reinterpret_cast<const float*>(wrec + (lane % (32 / kRecHalves)) * 4);
-                lo = __float_as_uint(rec_word(rec, sw, 0));
-                hi = __float_as_uint(rec_word(rec, sw, 1));
-#pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                    // number of fences f[0..13] (= words 2..15) below x[j]; positions >= 14 act as +inf
-                    int c = 0;
-#pragma unroll
-                    for (int step = 8; step >= 1; step >>= 1) {
-                        const int e = min(c + step - 1, kFences);
-                        const float f = rec_word(rec, sw, 2 + min(e, kFences - 1));
-                        c += (e < kFences && f < x[j]) ? step : 0;
-                    }
-                    packed |= (uint32_t)c << (8 * j);
-                }
-            }
+            packed |= (uint32_t)c << (8 * j);
         }
         const uint32_t d = hi - lo;
 #pragma unroll
@@ -492,19 +457,7 @@ __global__ void __launch_bounds__(kTile, VALID ? 6 : TGL_WINDOW_MINB) window_ker
             if (lane == 0) s_red[b][warp] = s2;
         }
     } else {
-#if TGL_CUT0_MULTI
-        // the upper cut through the warp's counted, branch-free search (all 32 lanes reach here;
-        // lanes with no slot before t search an empty gap)
-        uint32_t bcur;
-        {
-            uint32_t a4[4] = {early ? ga[0] : lo, lo, lo, lo}, b4[4] = {early ? gb[0] : lo, lo, lo, lo};
-            const float x4[4] = {t, 0.0f, 0.0f, 0.0f};
-            lower_bound_multi(p, a4, b4, x4);
-            bcur = a4[0];
-        }
-#else
         uint32_t bcur = early ? lower_bound_ts(p, ga[0], gb[0], t) : lo;
-#endif
         for (int b = 0; b < nsb; ++b) {
             // lower bound of window b: layer 0 -> t (-) ((b+1) (x) t_s); l >= 1 -> inherited
             const float xb = p.layer == 0 ? __fsub_rn(t, __fmul_rn((float)(b + 1), p.snapshot_len)) : lin;
@@ -739,11 +692,7 @@ __global__ void __launch_bounds__(kTile, OUTX == 2 ? 6 : (STRATEGY == TGL_MOST_R
                                                        : lane == 1 ? (uintptr_t)(o.eid + adj) : (uintptr_t)(o.dt + adj));
         const uint32_t x = inc[b * 32 + lane];
         const uint32_t ex = __shfl_up_sync(kFull, x, 1);
-#if TGL_STCS
-        if (valid) __stcs(reinterpret_cast<long long*>(o.offsets) + i, (long long)(wb + (lane ? ex : 0u)));
-#else
         if (valid) o.offsets[i] = (int64_t)(wb + (lane ? ex : 0u));
-#endif
         fb += __shfl_sync(kFull, x, 31);
     }
     __syncwarp();
@@ -791,12 +740,8 @@ __global__ void __launch_bounds__(kTile, OUTX == 2 ? 6 : (STRATEGY == TGL_MOST_R
         for (int u = 0; u < kCopyUnroll; ++u) {
             if (act[u]) {
                 if (p.recs) {
-#if TGL_REC_WORDS == 4
-                    rec[u] = ld_rand_v4(reinterpret_cast<const int4*>(p.recs) + pos[u]);
-#else
                     const int* w = reinterpret_cast<const int*>(p.recs + pos[u]);
                     rec[u] = make_int4(ld_rand_s32(w), ld_rand_s32(w + 1), ld_rand_s32(w + 2), 0);
-#endif
                 } else {
                     rec[u] = make_int4(__float_as_int(__ldg(p.ts + pos[u])), __ldg(p.nbr + pos[u]),
                                        __ldg(p.eid + pos[u]), 0);
@@ -811,16 +756,9 @@ __global__ void __launch_bounds__(kTile, OUTX == 2 ? 6 : (STRATEGY == TGL_MOST_R
             float* dtp = reinterpret_cast<float*>(wptr[b * 4 + 2]);
             const float tv = __int_as_float(rec[u].x);
             const float tr = troot[r];
-#if TGL_STCS
-            // block outputs are not read again by this kernel: streaming (evict-first) global stores
-            __stcs(reinterpret_cast<int32_t*>(pne.x) + oo[u], rec[u].y);
-            __stcs(reinterpret_cast<int32_t*>(pne.y) + oo[u], rec[u].z);
-            __stcs(dtp + oo[u], __fsub_rn(tr, tv));
-#else
             reinterpret_cast<int32_t*>(pne.x)[oo[u]] = rec[u].y;
             reinterpret_cast<int32_t*>(pne.y)[oo[u]] = rec[u].z;
             dtp[oo[u]] = __fsub_rn(tr, tv);
-#endif
             if (EXTRA) {
                 const BlockOut& o = p.out[b];
                 const uint64_t oi = (uint64_t)((reinterpret_cast<int32_t*>(pne.x) + oo[u]) - o.nbr);
