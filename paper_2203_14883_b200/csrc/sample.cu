@@ -502,6 +502,44 @@ __global__ void __launch_bounds__(kTile, VALID ? 6 : TGL_WINDOW_MINB) window_ker
     asm volatile("griddepcontrol.launch_dependents;");
 }
 
+// Floyd's k-subset for k <= kFloydRegs with the picks in registers (R#5, R#6): draw j is word j
+// mod 4 of Philox4x32-10 at counter (j / 4, ctr1, rk); r_j = floor(x_j (m_j + 1) / 2^32),
+// m_j = c - k + j; pick j = r_j unless an earlier pick equals it, else m_j (> every earlier pick).
+// The picks are kept ascending (R#13) by a compare-exchange chain after each draw (static register
+// indices) and stored to the lane's column of picks (stride 32).  Same set and order as the
+// shared-memory insertion below -- which ran each draw's shift loop at the warp's slowest lane.
+constexpr int kFloydRegs = 16;
+__device__ __forceinline__ void floyd_in_registers(uint32_t* pk, uint32_t len, int k, uint32_t ctr1, uint64_t rk,
+                                                   uint32_t seed_lo, uint32_t seed_hi) {
+    uint32_t a[kFloydRegs];
+    uint4 rnd = make_uint4(0u, 0u, 0u, 0u);
+#pragma unroll
+    for (int j = 0; j < kFloydRegs; ++j) {
+        a[j] = 0xffffffffu;
+        if (j < k) {
+            if ((j & 3) == 0)
+                rnd = philox4x32_10(make_uint4((uint32_t)j >> 2, ctr1, (uint32_t)rk, (uint32_t)(rk >> 32)), seed_lo,
+                                    seed_hi);
+            const uint32_t m = len - (uint32_t)k + (uint32_t)j;
+            const uint32_t r = __umulhi(draw_word(rnd, (uint32_t)j), m + 1u);
+            bool taken = false;
+#pragma unroll
+            for (int i = 0; i < j; ++i) taken |= a[i] == r;
+            a[j] = taken ? m : r;
+            // keep a[0..j] ascending: one compare-exchange chain bubbles the new pick into place
+#pragma unroll
+            for (int i = j - 1; i >= 0; --i) {
+                const uint32_t lo = min(a[i], a[i + 1]), hi = max(a[i], a[i + 1]);
+                a[i] = lo;
+                a[i + 1] = hi;
+            }
+        }
+    }
+#pragma unroll
+    for (int j = 0; j < kFloydRegs; ++j)
+        if (j < k) pk[j * 32] = a[j];
+}
+
 // the fused gather of one group of (up to 32) outputs held one per lane
 __device__ __forceinline__ void fused_gather_rows(const SampleParams& p, bool act, int64_t gi, int32_t nbr,
                                                   int32_t eid, int lane) {
@@ -631,6 +669,10 @@ __global__ void __launch_bounds__(kTile, OUTX == 2 ? 6 : (STRATEGY == TGL_MOST_R
                     }
                     pk[(q + 1) * 32] = xj;
                 }
+            } else if (k <= kFloydRegs) {
+                // Floyd (R#5, R#6) with the picks in registers: the k draws and their membership
+                // tests fully unrolled (k is warp-uniform: no divergence), then a sorting network
+                floyd_in_registers(pk, len, k, ctr1, rk, p.seed_lo, p.seed_hi);
             } else {
                 // Floyd: for m = c-k .. c-1, r uniform in [0, m]; take r unless taken, else m
                 for (int j = 0; j < k; ++j) {
