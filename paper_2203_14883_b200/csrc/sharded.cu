@@ -573,9 +573,13 @@ extern "C" int tgl_sample_sharded(tgl_shard* sh, const int32_t* roots, const flo
     int64_t nnz[64][TGL_MAX_SNAPSHOTS];
     {
         const tgl_block* ob[TGL_MAX_SNAPSHOTS];
-        for (int s = 0; s < S; ++s) ob[s] = &out[s];
+        bool ts0 = L > 1;  // ts_edge travels with the replies when a layer follows or the caller asked for it
+        for (int s = 0; s < S; ++s) {
+            ob[s] = &out[s];
+            ts0 |= out[s].ts_edge != nullptr;
+        }
         if ((rc = shard_chain(sh, 0, 0, S, roots, root_ts, k0, nullptr, n_roots, fanouts[0], strategy, snapshot_len,
-                              seed, L > 1, ob, nnz[0], st)))
+                              seed, ts0, ob, nnz[0], st)))
             return rc;
     }
     // layer l >= 1: chain (l, s) over block (l-1, s)'s outputs (R#3, R#4), keys parent * k + j (R#7)
@@ -601,7 +605,7 @@ extern "C" int tgl_sample_sharded(tgl_shard* sh, const int32_t* roots, const flo
                                                               snapshot_len, fanouts[l - 1], ck, clo);
             const tgl_block* ob[1] = {&out[l * S + s]};
             if ((rc = shard_chain(sh, l, s, 1, par.nbr, par.ts_edge, ck, clo, m, fanouts[l], strategy, snapshot_len,
-                                  seed, l < L - 1, ob, &nnz[l][s], st)))
+                                  seed, l < L - 1 || out[l * S + s].ts_edge != nullptr, ob, &nnz[l][s], st)))
                 return rc;
             pkey[s] = ck;
             plo[s] = clo;
