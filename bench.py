@@ -744,9 +744,19 @@ def run_ours(args):
     # end to end through the public API with host buffers (rank-local), copies inside the region
     if not args.no_e2e:
         gf = (lambda smp: make_gather(tgl, cfg, smp, dev, tabs=tabs, fused=fused)) if gather is not None else None
+        # the mini-batches as TGL feeds them: positive edges + negatives (host), roots staged on the device
+        by_start = {}
+        for (r, _), s0 in zip(chunks, mine):
+            if s0 not in by_start:
+                by_start[s0] = C.batch_edges(cfg, src, dst, ts, s0, r.numel())
+        bedges = [by_start[s0] for s0 in mine]
         out["e2e"] = e2e(args, tgl, sampler, chunks, mine, cfg, dev, world, gather_factory=gf, cdev=cdev,
-                         events=events if gather is not None else None)
-        out["e2e_full_d2h"] = e2e(args, tgl, sampler, chunks, mine, cfg, dev, world, full_d2h=True, cdev=cdev)
+                         events=events if gather is not None else None, batch_edges=bedges)
+        out["e2e_root_arrays"] = e2e(args, tgl, sampler, chunks, mine, cfg, dev, world, gather_factory=gf, cdev=cdev,
+                                     events=events if gather is not None else None)
+        out["e2e_full_d2h"] = e2e(args, tgl, sampler, chunks, mine, cfg, dev, world, full_d2h=True, cdev=cdev,
+                                  batch_edges=bedges)
+        del by_start, bedges
 
     # parity gate (every rank, its own timed chunks) + CPU oracle baseline (rank 0, N = 1 only)
     out["parity"], cpu = parity_gate(args, cfg, tgl, sampler, src, dst, ts, chunks, mine, digests_by_start,
@@ -819,21 +829,30 @@ def per_batch(args, tgl, g, cfg, chunk, key0, dev, world, n_graph=64, reps=10, c
 
 
 def e2e(args, tgl, sampler, chunks, mine, cfg, dev, world, full_d2h=False, gather_factory=None, events=None,
-        cdev=None):
+        cdev=None, batch_edges=None):
     """End to end through the public API with host buffers, copies inside the timed region.
 
-    Per step: pinned host roots -> H2D (copy stream) -> tgl_sample (compute stream) -> D2H of the
-    step's result.  full_d2h=False: the result read back is the step's metric, the per-block
+    Per step: pinned host inputs -> H2D (copy stream) -> tgl_sample (compute stream) -> D2H of the
+    step's result.  Inputs: with `batch_edges` (per chunk (e0, src, dst, neg, ts) of C.batch_edges) the
+    mini-batch in TGL's own form -- the positive edges and their negatives, 16 bytes per 3 roots --
+    expanded into roots on the device by tgl_batch_roots (R#16); else the root arrays themselves
+    (8 bytes per root).  full_d2h=False: the result read back is the step's metric, the per-block
     (n_roots, nnz) counts (the blocks stay on the GPU for the consumer, as in TGL's training step);
     full_d2h=True: every block (offsets + nbr/eid/dt trimmed to nnz) is copied to pinned host memory.
     Double-buffered: the H2D of step j+1 and the D2H of step j overlap the sampling of j+1 / j+1.
     """
     L, S = len(cfg.fanouts), cfg.n_snapshots
     pinned = {}  # one pinned copy per distinct chunk (the step list cycles over them)
-    for r, t in chunks:
+    for j, (r, t) in enumerate(chunks):
         if id(r) not in pinned:
-            pinned[id(r)] = (r.cpu().pin_memory(), t.cpu().pin_memory())
+            pinned[id(r)] = tuple(x.cpu().pin_memory() for x in batch_edges[j][1:]) if batch_edges is not None else \
+                (r.cpu().pin_memory(), t.cpu().pin_memory())
     host = [pinned[id(r)] for r, _ in chunks]
+    d_edges = None
+    if batch_edges is not None:
+        cap_e = max(x[1].numel() for x in batch_edges)
+        d_edges = [tuple(torch.empty(cap_e, dtype=x.dtype, device=dev) for x in batch_edges[0][1:])
+                   for _ in range(2)]
     host_ev = None
     if events is not None:  # step-6 events travel with their roots
         pin_ev = {k: (a.cpu().pin_memory(), b.cpu().pin_memory()) for k, (a, b) in events.items()}
@@ -865,13 +884,19 @@ def e2e(args, tgl, sampler, chunks, mine, cfg, dev, world, full_d2h=False, gathe
         pending = None  # (slot, event) whose counts / payload are still to be read
         for j in js:
             slot = j % 2
-            r, t = host[j]
             dr, dt_ = d_roots[slot]
+            n_r = chunks[j][0].numel()
             with torch.cuda.stream(copy_s):
                 if roots_free[slot] is not None:
                     copy_s.wait_event(roots_free[slot])
-                dr.copy_(r, non_blocking=True)
-                dt_.copy_(t, non_blocking=True)
+                if d_edges is not None:  # the batch's edges + negatives
+                    for dst_, src_ in zip(d_edges[slot], host[j]):
+                        dst_[:src_.numel()].copy_(src_, non_blocking=True)
+                    stats["h2d"] += sum(x.numel() * x.element_size() for x in host[j])
+                else:
+                    dr.copy_(host[j][0], non_blocking=True)
+                    dt_.copy_(host[j][1], non_blocking=True)
+                    stats["h2d"] += n_r * 8
                 if host_ev is not None:
                     ne = host_ev[j][0].numel()
                     d_ev[slot][0][:ne].copy_(host_ev[j][0], non_blocking=True)
@@ -882,7 +907,9 @@ def e2e(args, tgl, sampler, chunks, mine, cfg, dev, world, full_d2h=False, gathe
             comp.wait_event(h2d_done)
             if outs_free[slot] is not None:
                 comp.wait_event(outs_free[slot])
-            blocks = smps[slot].run(dr, dt_, seed=cfg.sampler_seed, root_key_base=mine[j])
+            if d_edges is not None:
+                tgl.batch_roots(*d_edges[slot], first_root=mine[j], n_roots=n_r, out=(dr, dt_))
+            blocks = smps[slot].run(dr[:n_r], dt_[:n_r], seed=cfg.sampler_seed, root_key_base=mine[j])
             if gathers is not None:
                 ev = None
                 if host_ev is not None:
@@ -895,7 +922,6 @@ def e2e(args, tgl, sampler, chunks, mine, cfg, dev, world, full_d2h=False, gathe
             done = torch.cuda.Event()
             done.record(comp)
             roots_free[slot] = done
-            stats["h2d"] += r.numel() * 8
             stats["d2h"] += 16 * nb
             if pending is not None:
                 finish(*pending)
@@ -932,8 +958,10 @@ def e2e(args, tgl, sampler, chunks, mine, cfg, dev, world, full_d2h=False, gathe
     torch.cuda.synchronize(dev)
     ms = s.elapsed_time(e)
     edges, _, ms_max = reduce_report(stats["edges"], 0.0, ms, world, cdev or dev)
-    what = ("pinned host roots -> H2D -> tgl_sample -> D2H of every block (offsets, nbr, eid, dt)" if full_d2h else
-            "pinned host roots -> H2D -> tgl_sample -> D2H of the step's metric (per-block n_roots, nnz); "
+    src_what = ("pinned host mini-batch (positive edges src, dst, ts + negatives: 16 B per 3 roots) -> H2D -> "
+                "tgl_batch_roots" if batch_edges is not None else "pinned host roots -> H2D")
+    what = (f"{src_what} -> tgl_sample -> D2H of every block (offsets, nbr, eid, dt)" if full_d2h else
+            f"{src_what} -> tgl_sample -> D2H of the step's metric (per-block n_roots, nnz); "
             "blocks stay on the GPU for the consumer")
     return {"value": edges / (ms_max / 1e3), "unit": UNIT, "h2d_bytes_per_step": stats["h2d"] // args.steps,
             "d2h_bytes_per_step": stats["d2h"] // args.steps,

@@ -365,6 +365,20 @@ TGL_API int tgl_state_write(const int32_t *ids, const float *ts, int64_t n_event
 TGL_API int tgl_chunk_schedule(int64_t n_edges, int64_t batch_size, int64_t chunk_size, uint64_t epoch,
                        uint64_t seed, int64_t *first_edge, int64_t cap, int64_t *n_batches, void *stream);
 
+/* ------------------------------------------------------------------ root staging */
+
+/*
+ * The roots of a mini-batch given in TGL's own form -- positive edges (src_i, dst_i, ts_i) and one
+ * negative destination neg_i per edge ("600 positive and 600 negative edges") --
+ * reading R#16: root 3i = src_i, 3i+1 = dst_i, 3i+2 = neg_i, each at time ts_i.  Writes roots
+ * [first_root, first_root + n_roots) of that stream into roots / root_ts (device int32 / float32
+ * [n_roots]); the input arrays (device, or mapped pinned host memory) hold the edges
+ * first_root / 3 .. (first_root + n_roots - 1) / 3 (index 0 = edge first_root / 3).  Errors:
+ * TGL_EINVAL for negative sizes or NULL pointers with n_roots > 0.
+ */
+TGL_API int tgl_batch_roots(const int32_t *src, const int32_t *dst, const int32_t *neg, const float *ts,
+                    int64_t first_root, int64_t n_roots, int32_t *roots, float *root_ts, void *stream);
+
 /* ------------------------------------------------------------------ verification */
 
 /*

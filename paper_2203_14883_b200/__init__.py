@@ -26,7 +26,7 @@ from ._lib import MOST_RECENT, UNIFORM, TGLError
 _L = _lib.load()
 
 __all__ = ["TCSR", "Block", "Sampler", "build", "wrap", "aux_bytes", "sample", "gather", "check", "shard_bucket",
-           "set_node_base", "shard_unpermute", "offsets_to_counts", "block_digest", "tcsr_indptr", "build_range",
+           "set_node_base", "shard_unpermute", "offsets_to_counts", "block_digest", "tcsr_indptr", "build_range", "batch_roots",
            "nccl_id", "ShardGroup", "ShardSampler",
            "MOST_RECENT", "UNIFORM", "TGLError", "lib_path"]
 
@@ -480,6 +480,25 @@ def block_digest(block: Block, bounds: torch.Tensor, stream=None) -> torch.Tenso
     _rc(_L.tgl_block_digest(_ptr(block.offsets), _ptr(block.nbr), _ptr(block.eid), _ptr(block.dt), _ptr(bounds), nb,
                             _ptr(out), _stream(stream)), "tgl_block_digest")
     return out
+
+
+def batch_roots(src: torch.Tensor, dst: torch.Tensor, neg: torch.Tensor, ts: torch.Tensor, first_root: int,
+                n_roots: int, out: Optional[tuple] = None, stream=None):
+    """tgl_batch_roots: roots [first_root, first_root + n_roots) of a mini-batch of positive edges +
+    negatives (R#16: src_i, dst_i, neg_i at ts_i); the arrays start at edge first_root // 3."""
+    src = _cuda(src, torch.int32, "src")
+    dst = _cuda(dst, torch.int32, "dst")
+    neg = _cuda(neg, torch.int32, "neg")
+    ts = _cuda(ts, torch.float32, "ts")
+    n = int(n_roots)
+    need = (int(first_root) + n - 1) // 3 + 1 - int(first_root) // 3 if n else 0
+    if min(src.numel(), dst.numel(), neg.numel(), ts.numel()) < need:
+        raise ValueError(f"the edge arrays must hold {need} edges")
+    r, t = out if out is not None else (torch.empty(n, dtype=torch.int32, device=src.device),
+                                        torch.empty(n, dtype=torch.float32, device=src.device))
+    _rc(_L.tgl_batch_roots(_ptr(src), _ptr(dst), _ptr(neg), _ptr(ts), int(first_root), n, _ptr(r), _ptr(t),
+                           _stream(stream)), "tgl_batch_roots")
+    return r, t
 
 
 def check(g: Optional[TCSR] = None, stream=None) -> int:

@@ -88,6 +88,7 @@ SIGNATURES = {
     "tgl_state_write": (ctypes.c_int, [P, P, i64, i32, i32, P, P, P, i32, P, sz, P]),
     "tgl_check": (ctypes.c_int, [P, P]),
     "tgl_block_digest": (ctypes.c_int, [P, P, P, P, P, i64, P, P]),
+    "tgl_batch_roots": (ctypes.c_int, [P, P, P, P, i64, i64, P, P, P]),
     "tgl_tcsr_indptr_workspace": (ctypes.c_int, [i64, i32, ctypes.POINTER(sz)]),
     "tgl_tcsr_indptr": (ctypes.c_int, [P, P, P, i64, i32, ctypes.c_int, P, P, sz, P]),
     "tgl_tcsr_build_range_workspace": (ctypes.c_int, [i64, i32, ctypes.c_int, i32, i32, i64, ctypes.POINTER(sz)]),

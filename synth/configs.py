@@ -272,6 +272,22 @@ def roots(cfg: Workload, src: torch.Tensor, dst: torch.Tensor, ts: torch.Tensor,
     return node.to(torch.int32), ts[le].clone()
 
 
+def batch_edges(cfg: Workload, src: torch.Tensor, dst: torch.Tensor, ts: torch.Tensor, first_root: int,
+                n_roots: int):
+    """The mini-batch in TGL's own form ("600 positive and 600 negative edges"): the positive
+    edges (src_i, dst_i, ts_i) covering roots [first_root, first_root + n_roots) of the root stream
+    and their negative destinations neg_i (R#17) -- e0 = first_root // 3 and int32 / float32 arrays
+    of the edges e0 .. (first_root + n_roots - 1) // 3.  roots() of the same range = their expansion."""
+    e0, e1 = first_root // 3, (first_root + n_roots - 1) // 3 + 1
+    e = torch.arange(e0, e1, dtype=torch.int64, device=src.device)
+    if cfg.bipartite_split is not None:
+        lo, n = cfg.bipartite_split, cfg.n_nodes - cfg.bipartite_split
+    else:
+        lo, n = 0, cfg.n_nodes
+    neg = (lo + uniform_int(e, cfg.seed, 9, n)).to(torch.int32)
+    return e0, src[e0:e1].clone(), dst[e0:e1].clone(), neg, ts[e0:e1].clone()
+
+
 def tables(cfg: Workload, device="cpu") -> Dict[str, torch.Tensor]:
     """Gather sources for C3: node memory, mem_ts, mailbox (K=1, 428 wide, R#18), mail_ts, edge
     features (128-d, random as the paper does for LastFM, L428).  Exact float32 values."""

@@ -79,3 +79,15 @@ def test_batch_views_equal_per_batch_calls(tgl):
                        root_key_base=s0 + b * B)[0].trimmed()
         for x, y in zip(got[:4], want[:4]):
             assert torch.equal(x, y)
+
+
+def test_batch_roots_equals_root_stream(tgl):
+    """tgl_batch_roots (a5 root staging from positive edges + negatives, R#16) reproduces the root
+    stream, for ranges starting at every position of an edge triple."""
+    cfg = C.CONFIGS["C2"]
+    src, dst, ts = C.edges("C2", cfg, device="cuda")
+    for s0, n in ((0, 600), (3001, 4000), (3002, 1), (12345, 7777), (5, 0)):
+        e0, s, d, ng, t = C.batch_edges(cfg, src, dst, ts, s0, max(n, 1))
+        r, rt = tgl.batch_roots(s, d, ng, t, first_root=s0, n_roots=n)
+        wr, wt = C.roots(cfg, src, dst, ts, s0, n)
+        assert torch.equal(r, wr) and torch.equal(rt, wt)
