@@ -32,16 +32,12 @@
 #include <cstdlib>
 #include <cstring>
 
-#include <cooperative_groups.h>
-
 #include "chain.cuh"
 #include "common.cuh"
 #include "scan.cuh"
 #include "tsindex.cuh"
 
 namespace tgl {
-
-namespace cg = cooperative_groups;
 
 #ifndef TGL_WINDOW_MINB
 #define TGL_WINDOW_MINB 8
@@ -330,7 +326,7 @@ __device__ __forceinline__ float rec_word(const float* rec, int sw, int w) {
 
 // ---------------------------------------------------------------------------- K4a windows
 template <int STRATEGY, bool VALID>
-__device__ __forceinline__ void window_tile(const SampleParams& p) {
+__global__ void __launch_bounds__(kTile, VALID ? 6 : TGL_WINDOW_MINB) window_kernel(const __grid_constant__ SampleParams p) {
     __shared__ uint32_t s_red[TGL_MAX_SNAPSHOTS][kWarps];
     __shared__ int4 s_rec[kTile * 4];  // the tile's 64-byte node records (16 KB)
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -506,11 +502,6 @@ __device__ __forceinline__ void window_tile(const SampleParams& p) {
     asm volatile("griddepcontrol.launch_dependents;");
 }
 
-template <int STRATEGY, bool VALID>
-__global__ void __launch_bounds__(kTile, VALID ? 6 : TGL_WINDOW_MINB) window_kernel(const __grid_constant__ SampleParams p) {
-    window_tile<STRATEGY, VALID>(p);
-}
-
 // Floyd's k-subset for k <= kFloydRegs with the picks in registers (R#5, R#6): draw j is word j
 // mod 4 of Philox4x32-10 at counter (j / 4, ctr1, rk); r_j = floor(x_j (m_j + 1) / 2^32),
 // m_j = c - k + j; pick j = r_j unless an earlier pick equals it, else m_j (> every earlier pick).
@@ -589,7 +580,7 @@ __host__ __device__ inline int copy_warp_words(int nsb, int k, bool picks_in_sme
 // PSMEM: uniform picks in shared memory (known at compile time, so LDS/STS instead of generic
 // 64-bit accesses); else in the global workspace
 template <int STRATEGY, bool VALID, int OUTX, bool PSMEM>
-__device__ __forceinline__ void copy_tile(const SampleParams& p) {
+__global__ void __launch_bounds__(kTile, OUTX == 2 ? 6 : (STRATEGY == TGL_MOST_RECENT ? TGL_COPY_MINB_MR : TGL_COPY_MINB)) copy_kernel(const __grid_constant__ SampleParams p) {
     constexpr bool EXTRA = OUTX == 1;   // per-output data for a following layer / dedup
     constexpr bool GATHER = OUTX == 2;  // fused row gather of the last layer's outputs
     extern __shared__ __align__(16) uint32_t smem[];
@@ -836,22 +827,6 @@ __device__ __forceinline__ void copy_tile(const SampleParams& p) {
     }
 }
 
-template <int STRATEGY, bool VALID, int OUTX, bool PSMEM>
-__global__ void __launch_bounds__(kTile, OUTX == 2 ? 6 : (STRATEGY == TGL_MOST_RECENT ? TGL_COPY_MINB_MR : TGL_COPY_MINB)) copy_kernel(const __grid_constant__ SampleParams p) {
-    copy_tile<STRATEGY, VALID, OUTX, PSMEM>(p);
-}
-
-// Small calls (one super tile: per-batch calls of <= 64 tiles, e.g. one 4,000-root batch = 16
-// tiles) run both phases in ONE cooperative kernel: the window phase, a grid-wide barrier (all of
-// the grid's tile totals are then final), the copy phase -- one launch instead of two.  Same
-// code, same bits.
-template <int STRATEGY, int OUTX, bool PSMEM>
-__global__ void __launch_bounds__(kTile, 6) small_call_kernel(const __grid_constant__ SampleParams p) {
-    window_tile<STRATEGY, false>(p);
-    cg::this_grid().sync();
-    copy_tile<STRATEGY, false, OUTX, PSMEM>(p);
-}
-
 // ---------------------------------------------------------------------------- K9 dedup (R#27)
 // Distinct (node, hop time) pairs of a block in order of first appearance (SPEC's MFG node lists):
 //   D1 insert: open addressing over 64-bit keys (node << 32 | time bits); the SLOT a key lands in
@@ -1059,58 +1034,12 @@ static void launch_copy(const SampleParams& sp, int64_t grid, size_t smem, cudaS
 
 // EXTRA: the chain writes per-output data for a following layer or the dedup (ts_edge, child
 // key / time / lower bound); the last layer's copy carries none of it
-template <int STRATEGY, int OUTX, bool PSMEM>
-static bool launch_small_ps(const SampleParams& sp, int64_t grid, size_t smem, cudaStream_t st) {
-    auto fn = small_call_kernel<STRATEGY, OUTX, PSMEM>;
-    if (smem + 1024 > 48 * 1024) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    // co-resident CTAs (the grid barrier needs the whole grid resident): the per-call dynamic shared
-    // memory is a multiple of one warp's words, so a grid of <= 64 CTAs fits whenever one CTA per
-    // SM does -- checked against the occupancy of this call's shared memory
-    static thread_local size_t cached_smem = ~size_t(0);
-    static thread_local int cached_fit = 0;  // co-resident CTAs on the device for cached_smem
-    if (cached_smem != smem) {
-        int mb = 0, sms = 0, dev = 0;
-        cudaGetDevice(&dev);
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&mb, fn, kTile, smem) != cudaSuccess ||
-            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
-            mb = sms = 0;
-        cached_smem = smem;
-        cached_fit = mb * sms;
-    }
-    if ((int64_t)cached_fit < grid) return false;
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3((unsigned)grid);
-    cfg.blockDim = dim3(kTile);
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = st;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeCooperative;  // capturable in CUDA graphs (per-batch replay)
-    at[0].val.cooperative = 1;
-    cfg.attrs = at;
-    cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, fn, sp) == cudaSuccess;
-}
-
-template <int STRATEGY, int OUTX>
-static bool launch_small(const SampleParams& sp, int64_t grid, size_t smem, cudaStream_t st) {
-    if (STRATEGY == TGL_UNIFORM && sp.picks_global == nullptr) return launch_small_ps<STRATEGY, OUTX, true>(sp, grid, smem, st);
-    return launch_small_ps<STRATEGY, OUTX, false>(sp, grid, smem, st);
-}
-
 template <int STRATEGY, bool VALID>
 static int launch_pair(const SampleParams& sp, int64_t grid, size_t smem, cudaStream_t st) {
+    window_kernel<STRATEGY, VALID><<<(unsigned)grid, kTile, 0, st>>>(sp);
     bool extra = false;
     for (int b = 0; b < sp.nsb; ++b)
         extra |= sp.out[b].ts_edge || sp.out[b].child_key || sp.out[b].child_t || sp.out[b].child_lo;
-    static const bool no_small = getenv("TGL_NO_SMALL_KERNEL") != nullptr;  // A/B knob
-    if (!VALID && !no_small && grid <= (1 << kSuperShift)) {
-        const bool done = extra ? launch_small<STRATEGY, 1>(sp, grid, smem, st)
-                                : (sp.fg.n > 0 ? launch_small<STRATEGY, 2>(sp, grid, smem, st)
-                                               : launch_small<STRATEGY, 0>(sp, grid, smem, st));
-        if (done) return cudaGetLastError() == cudaSuccess ? TGL_OK : TGL_ECUDA;
-        cudaGetLastError();  // not co-resident / not launched: the two-kernel path below
-    }
-    window_kernel<STRATEGY, VALID><<<(unsigned)grid, kTile, 0, st>>>(sp);
     if (extra)
         launch_copy<STRATEGY, VALID, 1>(sp, grid, smem, st);
     else if (!VALID && sp.fg.n > 0)  // fused gather: last-layer chains only (never with extra data)
