@@ -56,7 +56,7 @@ constexpr int kWarps = kTile / 32;
 constexpr int kCopyUnroll = TGL_COPY_UNROLL;  // outputs in flight per lane in the flat copy
 constexpr int kSuperShift = 6;  // 64 tiles per super tile (tile bases: super totals + tile totals)
 #ifndef TGL_INDEX_MIN
-#define TGL_INDEX_MIN 4096  // C4 A/B: 256 73.9, 1024 74.5, 4096 75.3 G edges/s; C5 unchanged
+#define TGL_INDEX_MIN 128  // r02 C4 window: 128 388 us, 512 401, 4096 407 (C5 unchanged); r01 kernels preferred 4096
 #endif
 constexpr uint32_t kIndexMin = TGL_INDEX_MIN;  // gaps longer than this descend the 16-ary index
 constexpr int kPicksSmemPerWarp = 8 * 1024;  // bytes of uniform picks kept in shared memory per warp
