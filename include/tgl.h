@@ -47,7 +47,7 @@ extern "C" {
 #define TGL_API
 #endif
 
-#define TGL_ABI_VERSION 2
+#define TGL_ABI_VERSION 3
 
 enum {
     TGL_OK = 0,
@@ -101,6 +101,12 @@ TGL_API int tgl_tcsr_build_workspace(int64_t n_edges, int32_t n_nodes, int add_r
  *   cut search), a 12-byte record {ts, nbr, eid} per slot (payload copy: one request per run)
  *   and a 64-byte record {lo, hi, 14 fence times} per node (list bounds and cut gaps in one
  *   load) -- DESIGN.md "Data layout".  Without it the sampler reads the separate arrays.
+ *   Time codec: when the T-CSR holds at most 255 distinct timestamps (all finite, >= +0; e.g.
+ *   MAG's publication years, P:L336 / P:L355) the aux build also writes a dictionary of the
+ *   sorted distinct times and a 1-byte code per slot; node records then carry 56 fence codes and,
+ *   when nbr / code / per-code eid offset fit 64 bits, slot records shrink to 8 bytes.  Lossless:
+ *   sampled blocks are bit-identical with and without it (tgl_tcsr_codec reports it).
+ *   The aux build blocks on `stream` (it reads the distinct-time count and the codec widths).
  * workspace: >= tgl_tcsr_build_workspace() bytes of device memory, 256-byte aligned.
  * Synchronous validation: the call blocks on `stream` once to read the device validation word;
  *   on ERANGE / EINVAL / EUNSORTED no handle is returned and outputs are unspecified.
@@ -115,7 +121,8 @@ TGL_API int tgl_tcsr_build(const int32_t *src, const int32_t *dst, const float *
 /* Bytes of the optional sampler aux buffer for a T-CSR of n_stored edges over n_nodes nodes. */
 TGL_API int tgl_tcsr_aux_bytes(int64_t n_stored, int32_t n_nodes, size_t *bytes /* host */);
 
-/* (Re)build the aux buffer over existing T-CSR arrays (e.g. ones received from another rank). */
+/* (Re)build the aux buffer over existing T-CSR arrays (e.g. ones received from another rank).
+ * Blocks on `stream` (codec detection); the buffer is complete when the call returns. */
 TGL_API int tgl_tcsr_aux_build(const int64_t *indptr, const float *ts, const int32_t *nbr, const int32_t *eid,
                        int32_t n_nodes, int64_t n_stored, void *aux, size_t aux_bytes, void *stream);
 
@@ -135,6 +142,11 @@ TGL_API int tgl_tcsr_set_node_base(tgl_tcsr *g, int64_t node_lo);
 
 /* Host query of a handle's sizes. */
 TGL_API int tgl_tcsr_info(const tgl_tcsr *g, int32_t *n_nodes /* host */, int64_t *n_stored /* host */);
+
+/* Host query of the handle's time codec (tgl_tcsr_build "aux"): *n_codes = number of distinct
+ * timestamps coded (0: no codec -- no aux, more than 255 distinct times, or -0.0 present);
+ * *packed = 1 when slot records are the 8-byte packed form.  Either pointer may be NULL. */
+TGL_API int tgl_tcsr_codec(const tgl_tcsr *g, int32_t *n_codes /* host */, int32_t *packed /* host */);
 
 /* ------------------------------------------------------------------ sampler (Alg. 1) */
 

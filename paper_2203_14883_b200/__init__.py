@@ -77,6 +77,13 @@ class TCSR:
     def handle(self):
         return self._h
 
+    @property
+    def codec(self) -> dict:
+        """tgl_tcsr_codec: {"n_codes": distinct times coded (0 = no time codec), "packed": 8-byte records}."""
+        n, pk = ctypes.c_int32(), ctypes.c_int32()
+        _rc(_L.tgl_tcsr_codec(self._h, ctypes.byref(n), ctypes.byref(pk)), "tgl_tcsr_codec")
+        return {"n_codes": n.value, "packed": bool(pk.value)}
+
     def __del__(self):
         h, self._h = getattr(self, "_h", None), None
         if h and _L is not None:

@@ -71,6 +71,7 @@ SIGNATURES = {
     "tgl_tcsr_wrap": (ctypes.c_int, [P, P, P, P, P, sz, i32, i64, ctypes.POINTER(P)]),
     "tgl_tcsr_destroy": (ctypes.c_int, [P]),
     "tgl_tcsr_info": (ctypes.c_int, [P, ctypes.POINTER(i32), ctypes.POINTER(i64)]),
+    "tgl_tcsr_codec": (ctypes.c_int, [P, ctypes.POINTER(i32), ctypes.POINTER(i32)]),
     "tgl_sample_capacity": (ctypes.c_int, [i64, i32, P, i32, ctypes.c_int, f32, P, P, ctypes.POINTER(sz)]),
     "tgl_sample": (ctypes.c_int, [P, P, P, i64, i32, P, ctypes.c_int, i32, f32, u64, u64, P, P, sz, P]),
     "tgl_sample_keyed": (ctypes.c_int, [P, P, P, P, i64, i32, P, ctypes.c_int, i32, f32, u64, P, P, sz, P]),

@@ -66,11 +66,34 @@ extern "C" int tgl_tcsr_wrap(const int64_t* indptr, const int32_t* nbr, const fl
     g->eid = eid;
     g->n_nodes = n_nodes;
     g->n_stored = n_stored;
-    g->index = static_cast<const float*>(aux);
+    const char* ab = static_cast<const char*>(aux);
+    g->index = aux ? reinterpret_cast<const float*>(ab + lay.index_off) : nullptr;
     g->n_levels = aux ? lay.index.n_levels : 0;
     for (int l = 0; l <= kMaxIndexLevels && l < 12; ++l) g->level_off[l] = lay.index.off[l];
-    g->recs = aux ? static_cast<const void*>(static_cast<const char*>(aux) + lay.rec_off) : nullptr;
-    g->nodes = aux ? static_cast<const void*>(static_cast<const char*>(aux) + lay.node_off) : nullptr;
+    g->recs = aux ? static_cast<const void*>(ab + lay.rec_off) : nullptr;
+    g->nodes = aux ? static_cast<const void*>(ab + lay.node_off) : nullptr;
+    if (aux) {
+        // the codec header written by the aux build (a synchronous read: the aux build has completed)
+        uint32_t hdr[5] = {0, 0, 0, 0, 0};
+        if (cudaMemcpy(hdr, aux, sizeof(hdr), cudaMemcpyDeviceToHost) != cudaSuccess) {
+            cudaFree(g->err_dev);
+            free(g);
+            return TGL_ECUDA;
+        }
+        if (hdr[0] != kDictMagic || hdr[1] > (uint32_t)kMaxCodes || hdr[2] > 1 || hdr[3] > 32 || hdr[4] > 8) {
+            cudaFree(g->err_dev);
+            free(g);
+            return TGL_EINVAL;  // not a buffer filled by tgl_tcsr_build / tgl_tcsr_aux_build
+        }
+        if (hdr[1] > 0) {
+            g->dict = aux;
+            g->codes = reinterpret_cast<const uint8_t*>(ab + lay.code_off);
+            g->n_codes = (int)hdr[1];
+            g->packed = (int)hdr[2];
+            g->bits_nbr = (int)hdr[3];
+            g->bits_code = (int)hdr[4];
+        }
+    }
     cudaGetDevice(&g->device);
     *out = g;
     return TGL_OK;
@@ -93,6 +116,13 @@ extern "C" int tgl_tcsr_info(const tgl_tcsr* g, int32_t* n_nodes, int64_t* n_sto
     if (!g) return TGL_EINVAL;
     if (n_nodes) *n_nodes = g->n_nodes;
     if (n_stored) *n_stored = g->n_stored;
+    return TGL_OK;
+}
+
+extern "C" int tgl_tcsr_codec(const tgl_tcsr* g, int32_t* n_codes, int32_t* packed) {
+    if (!g) return TGL_EINVAL;
+    if (n_codes) *n_codes = g->n_codes;
+    if (packed) *packed = g->packed;
     return TGL_OK;
 }
 

@@ -14,6 +14,8 @@
 //
 // Deterministic: no atomic decides an output position.
 #include <algorithm>
+#include <climits>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "radix.cuh"
@@ -111,26 +113,180 @@ extern "C" int tgl_tcsr_build_workspace(int64_t n_edges, int32_t n_nodes, int ad
 }
 
 namespace tgl {
-// aux buffer (tsindex.cuh): index levels L_l[j] = ts[j * 16^l] and the interleaved payload
+// ---------------------------------------------------------------------------- aux: time codec
+// (tsindex.cuh "time codes").  X1 collects the distinct timestamp bits (at most kMaxCodes; any
+// negative, -0, infinite or NaN time disables the codec): warp leaders of equal values
+// (__match_any_sync) insert into a per-CTA hash in shared memory, merged into a global hash at
+// the end.  X2 (one CTA) ranks them -- non-negative finite floats order like their bit patterns
+// -- into the sorted dictionary.  X3 writes every slot's code and the per-code eid range and the
+// largest neighbour id (the packed record widths).
+__device__ __forceinline__ uint32_t hash_bits(uint32_t x) {
+    x ^= x >> 16;
+    x *= 0x7feb352du;
+    x ^= x >> 15;
+    return x;
+}
+
+__global__ void __launch_bounds__(256) codec_collect_kernel(const float* __restrict__ ts, uint64_t n,
+                                                            CodecScratch* sc) {
+    __shared__ uint32_t h[512];
+    __shared__ uint32_t cnt;
+    for (int q = threadIdx.x; q < 512; q += blockDim.x) h[q] = 0xffffffffu;
+    if (threadIdx.x == 0) cnt = 0;
+    __syncthreads();
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    bool ovf = false;  // block-uniform (__syncthreads_or)
+    for (uint64_t j0 = (uint64_t)blockIdx.x * blockDim.x; j0 < n && !ovf; j0 += stride) {
+        const uint64_t j = j0 + threadIdx.x;
+        const bool live = j < n;
+        const uint32_t bits = live ? __float_as_uint(ts[j]) : 0xffffffffu;
+        bool bad = live && bits >= 0x7f800000u;  // +inf, NaN, or sign bit set (negative, -0)
+        const uint32_t peers = __match_any_sync(kFull, bits);
+        if (live && !bad && (__ffs(peers) - 1) == (int)(threadIdx.x & 31)) {
+            uint32_t slot = hash_bits(bits) & 511u;
+            bool done = false;
+            for (int probe = 0; probe < 512 && !done; ++probe) {
+                const uint32_t prev = atomicCAS(&h[slot], 0xffffffffu, bits);
+                if (prev == 0xffffffffu) {
+                    bad |= atomicAdd(&cnt, 1u) >= (uint32_t)kMaxCodes;
+                    done = true;
+                } else if (prev == bits) {
+                    done = true;
+                }
+                slot = (slot + 1) & 511u;
+            }
+            bad |= !done;
+        }
+        if (threadIdx.x == 0) bad |= *reinterpret_cast<volatile uint32_t*>(&sc->overflow) != 0u;
+        ovf = __syncthreads_or(bad) != 0;
+    }
+    if (ovf) {
+        if (threadIdx.x == 0) atomicOr(&sc->overflow, 1u);
+        return;
+    }
+    for (int q = threadIdx.x; q < 512; q += blockDim.x) {
+        const uint32_t bits = h[q];
+        if (bits == 0xffffffffu) continue;
+        uint32_t slot = hash_bits(bits) & 511u;
+        bool done = false;
+        for (int probe = 0; probe < 512 && !done; ++probe) {
+            const uint32_t prev = atomicCAS(&sc->hash[slot], 0xffffffffu, bits);
+            if (prev == 0xffffffffu) {
+                if (atomicAdd(&sc->count, 1u) >= (uint32_t)kMaxCodes) atomicOr(&sc->overflow, 1u);
+                done = true;
+            } else if (prev == bits) {
+                done = true;
+            }
+            slot = (slot + 1) & 511u;
+        }
+        if (!done) atomicOr(&sc->overflow, 1u);
+    }
+}
+
+__global__ void __launch_bounds__(512) codec_dict_kernel(CodecScratch* sc, TimeDict* dict) {
+    __shared__ uint32_t h[512];
+    const int q = threadIdx.x;
+    h[q] = sc->hash[q];
+    if (q < 256) {
+        dict->value[q] = INFINITY;
+        dict->eid_base[q] = 0;
+        sc->eid_min[q] = INT32_MAX;
+        sc->eid_max[q] = INT32_MIN;
+    }
+    __syncthreads();
+    const uint32_t b = h[q];
+    if (b != 0xffffffffu) {
+        uint32_t rank = 0;
+        for (int r = 0; r < 512; ++r) rank += h[r] != 0xffffffffu && h[r] < b;
+        dict->value[rank] = __uint_as_float(b);
+    }
+}
+
+__global__ void __launch_bounds__(256) codec_assign_kernel(const float* __restrict__ ts, const int32_t* __restrict__ nbr,
+                                                           const int32_t* __restrict__ eid, uint64_t n,
+                                                           const TimeDict* __restrict__ dict,
+                                                           uint8_t* __restrict__ codes, CodecScratch* sc) {
+    __shared__ float val[256];
+    __shared__ int32_t emin[256], emax[256];
+    __shared__ uint32_t nmax;
+    val[threadIdx.x] = dict->value[threadIdx.x];
+    emin[threadIdx.x] = INT32_MAX;
+    emax[threadIdx.x] = INT32_MIN;
+    if (threadIdx.x == 0) nmax = 0;
+    __syncthreads();
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    uint32_t my_nmax = 0;
+    for (uint64_t j0 = (uint64_t)blockIdx.x * blockDim.x; j0 < n; j0 += stride) {
+        const uint64_t j = j0 + threadIdx.x;
+        const bool live = j < n;
+        uint32_t c = 0xffffffffu;
+        int32_t e = 0;
+        if (live) {
+            const float t = ts[j];
+            uint32_t lo = 0;  // #values < t = the index of t (t is in the dictionary)
+#pragma unroll
+            for (int step = 128; step >= 1; step >>= 1)
+                if (val[lo + step - 1] < t) lo += step;
+            c = lo;
+            codes[j] = (uint8_t)c;
+            e = eid[j];
+            my_nmax = max(my_nmax, (uint32_t)nbr[j]);
+        }
+        const uint32_t peers = __match_any_sync(kFull, c);
+        const int32_t mn = __reduce_min_sync(peers, live ? e : INT32_MAX);
+        const int32_t mx = __reduce_max_sync(peers, live ? e : INT32_MIN);
+        if (live && (__ffs(peers) - 1) == (int)(threadIdx.x & 31)) {
+            atomicMin(&emin[c], mn);
+            atomicMax(&emax[c], mx);
+        }
+    }
+    my_nmax = __reduce_max_sync(kFull, my_nmax);
+    if ((threadIdx.x & 31) == 0) atomicMax(&nmax, my_nmax);
+    __syncthreads();
+    if (emin[threadIdx.x] != INT32_MAX) {
+        atomicMin(&sc->eid_min[threadIdx.x], emin[threadIdx.x]);
+        atomicMax(&sc->eid_max[threadIdx.x], emax[threadIdx.x]);
+    }
+    if (threadIdx.x == 0) atomicMax(&sc->nbr_max, nmax);
+}
+
+struct CodecArgs {
+    const uint8_t* codes;   // null: no codec
+    const int32_t* eid_base;
+    int packed, bn, bc;
+};
+
+// aux buffer (tsindex.cuh): index levels L_l[j] = ts[j * 16^l], the slot records (12-byte, or
+// 8-byte packed under the codec) and the node records (14 fence times, or 56 fence codes)
 __global__ void aux_build_kernel(const int64_t* __restrict__ indptr, const float* __restrict__ ts,
                                  const int32_t* __restrict__ nbr, const int32_t* __restrict__ eid, uint64_t n,
-                                 uint64_t n_nodes, char* __restrict__ aux, AuxLayout lay) {
+                                 uint64_t n_nodes, char* __restrict__ aux, AuxLayout lay, CodecArgs cx) {
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-    float* index = reinterpret_cast<float*>(aux);
+    float* index = reinterpret_cast<float*>(aux + lay.index_off);
     for (int l = 1; l <= lay.index.n_levels; ++l) {
         float* out = index + lay.index.off[l];
         const int sh = kIndexShift * l;
         for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < lay.index.len[l]; j += stride)
             out[j] = ts[j << sh];
     }
-    SlotRec* rec = reinterpret_cast<SlotRec*>(aux + lay.rec_off);
-    for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += stride) {
-        SlotRec r;
-        memset(&r, 0, sizeof(r));
-        r.ts = ts[j];
-        r.nbr = nbr[j];
-        r.eid = eid[j];
-        rec[j] = r;
+    if (cx.packed) {
+        uint2* rec = reinterpret_cast<uint2*>(aux + lay.rec_off);
+        for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += stride) {
+            const uint32_t c = cx.codes[j];
+            const uint64_t rel = (uint64_t)(uint32_t)(eid[j] - __ldg(cx.eid_base + c));
+            const uint64_t w = (uint64_t)(uint32_t)nbr[j] | ((uint64_t)c << cx.bn) | (rel << (cx.bn + cx.bc));
+            rec[j] = make_uint2((uint32_t)w, (uint32_t)(w >> 32));
+        }
+    } else {
+        SlotRec* rec = reinterpret_cast<SlotRec*>(aux + lay.rec_off);
+        for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += stride) {
+            SlotRec r;
+            memset(&r, 0, sizeof(r));
+            r.ts = ts[j];
+            r.nbr = nbr[j];
+            r.eid = eid[j];
+            rec[j] = r;
+        }
     }
     // node records: thread (v, q) writes the q-th 16-byte quarter of node v's record
     int4* node = reinterpret_cast<int4*>(aux + lay.node_off);
@@ -139,15 +295,43 @@ __global__ void aux_build_kernel(const int64_t* __restrict__ indptr, const float
         const int q = (int)(w & 3);
         const uint32_t lo = (uint32_t)indptr[v], hi = (uint32_t)indptr[v + 1], d = hi - lo;
         int32_t word[4];
+        if (cx.codes) {  // {lo, hi, 10 separators + 2 pads, 11 groups of 4} (tsindex.cuh)
 #pragma unroll
-        for (int e = 0; e < 4; ++e) {
-            const int j = 4 * q + e - 2;  // fence index of word e (words 0, 1 of quarter 0: lo, hi)
-            word[e] = j < 0 ? (int32_t)(j == -2 ? lo : hi)
-                            : __float_as_int(d ? ts[fence_pos(lo, d, j)] : INFINITY);
+            for (int e = 0; e < 4; ++e) {
+                const int wi = 4 * q + e;  // record word
+                if (wi < 2) {
+                    word[e] = (int32_t)(wi == 0 ? lo : hi);
+                    continue;
+                }
+                uint32_t x = 0;
+#pragma unroll
+                for (int b = 0; b < 4; ++b) {
+                    int j;  // fence index of byte b of word wi (-1: pad)
+                    if (wi < 5) {
+                        const int sep = 4 * (wi - 2) + b;
+                        j = sep < kCodeSeps ? 5 * sep + 4 : -1;
+                    } else {
+                        j = 5 * (wi - 5) + b;
+                    }
+                    const uint32_t c = (j < 0 || d == 0) ? kCodeInf : cx.codes[code_fence_pos(lo, d, j)];
+                    x |= c << (8 * b);
+                }
+                word[e] = (int32_t)x;
+            }
+        } else {
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const int j = 4 * q + e - 2;  // fence index of word e (words 0, 1 of quarter 0: lo, hi)
+                word[e] = j < 0 ? (int32_t)(j == -2 ? lo : hi)
+                                : __float_as_int(d ? ts[fence_pos(lo, d, j)] : INFINITY);
+            }
         }
         node[w] = make_int4(word[0], word[1], word[2], word[3]);
     }
 }
+
+static int bit_width(uint64_t x) { return x ? 64 - __builtin_clzll(x) : 0; }
+
 }  // namespace tgl
 
 extern "C" int tgl_tcsr_aux_bytes(int64_t n_stored, int32_t n_nodes, size_t* bytes) {
@@ -164,10 +348,57 @@ extern "C" int tgl_tcsr_aux_build(const int64_t* indptr, const float* ts, const 
     if (aux_bytes < lay.bytes) return TGL_EWORKSPACE;
     int rc = check_device();
     if (rc) return rc;
-    const int64_t blocks = std::min<int64_t>((int64_t)((std::max<int64_t>(n_stored, n_nodes) + 255) / 256), 148 * 16);
-    aux_build_kernel<<<(unsigned)std::max<int64_t>(blocks, 1), 256, 0, (cudaStream_t)stream>>>(
-        indptr, ts, nbr, eid, (uint64_t)n_stored, (uint64_t)n_nodes, static_cast<char*>(aux), lay);
-    return cudaGetLastError() == cudaSuccess ? TGL_OK : TGL_ECUDA;
+    cudaStream_t st = (cudaStream_t)stream;
+    char* ab = static_cast<char*>(aux);
+    TimeDict* dict = reinterpret_cast<TimeDict*>(ab);
+    CodecScratch* sc = reinterpret_cast<CodecScratch*>(ab + sizeof(TimeDict));
+    uint8_t* codes = reinterpret_cast<uint8_t*>(ab + lay.code_off);
+    const uint64_t n = (uint64_t)n_stored;
+    const unsigned grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((n + 255) / 256, 148 * 8));
+    // X1: distinct times (<= kMaxCodes)
+    if (cudaMemsetAsync(sc->hash, 0xff, sizeof(sc->hash), st) != cudaSuccess ||
+        cudaMemsetAsync(&sc->count, 0, 4 * sizeof(uint32_t), st) != cudaSuccess)
+        return TGL_ECUDA;
+    if (n > 0) codec_collect_kernel<<<grid, 256, 0, st>>>(ts, n, sc);
+    uint32_t cnt[2] = {0, 0};
+    if (cudaMemcpyAsync(cnt, &sc->count, sizeof(cnt), cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+        cudaStreamSynchronize(st) != cudaSuccess)
+        return TGL_ECUDA;
+    static const bool no_codec = getenv("TGL_NO_CODEC") != nullptr;  // A/B knob, read once
+    const uint32_t D = (n > 0 && !cnt[1] && !no_codec) ? cnt[0] : 0u;
+    uint32_t hdr[8] = {kDictMagic, D, 0, 0, 0, 0, 0, 0};
+    CodecArgs cx = {nullptr, nullptr, 0, 0, 0};
+    if (D > 0) {
+        // X2 dictionary, X3 codes + widths
+        codec_dict_kernel<<<1, 512, 0, st>>>(sc, dict);
+        if (cudaMemsetAsync(&sc->nbr_max, 0, sizeof(uint32_t), st) != cudaSuccess) return TGL_ECUDA;
+        codec_assign_kernel<<<grid, 256, 0, st>>>(ts, nbr, eid, n, dict, codes, sc);
+        int32_t emin[256], emax[256];
+        uint32_t nmax = 0;
+        if (cudaMemcpyAsync(emin, sc->eid_min, sizeof(emin), cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+            cudaMemcpyAsync(emax, sc->eid_max, sizeof(emax), cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+            cudaMemcpyAsync(&nmax, &sc->nbr_max, sizeof(nmax), cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+            cudaStreamSynchronize(st) != cudaSuccess)
+            return TGL_ECUDA;
+        uint64_t span = 0;
+        for (uint32_t c = 0; c < D; ++c) span = std::max<uint64_t>(span, (uint64_t)((int64_t)emax[c] - (int64_t)emin[c]));
+        const int bn = bit_width(nmax), bc = bit_width(D - 1), br = bit_width(span);
+        const bool packed = bn + bc + br <= 64;
+        hdr[2] = packed ? 1u : 0u;
+        hdr[3] = (uint32_t)bn;
+        hdr[4] = (uint32_t)bc;
+        if (cudaMemcpyAsync(dict->eid_base, emin, sizeof(emin), cudaMemcpyHostToDevice, st) != cudaSuccess)
+            return TGL_ECUDA;
+        cx = CodecArgs{codes, dict->eid_base, packed ? 1 : 0, bn, bc};
+    }
+    if (cudaMemcpyAsync(dict, hdr, sizeof(hdr), cudaMemcpyHostToDevice, st) != cudaSuccess) return TGL_ECUDA;
+    const int64_t blocks = std::min<int64_t>((int64_t)((std::max<int64_t>(n_stored, (int64_t)n_nodes * 4) + 255) / 256),
+                                             148 * 16);
+    aux_build_kernel<<<(unsigned)std::max<int64_t>(blocks, 1), 256, 0, st>>>(
+        indptr, ts, nbr, eid, n, (uint64_t)n_nodes, ab, lay, cx);
+    if (cudaGetLastError() != cudaSuccess) return TGL_ECUDA;
+    // the host copies above read stack memory: complete them (and the buffer) before returning
+    return cudaStreamSynchronize(st) == cudaSuccess ? TGL_OK : TGL_ECUDA;
 }
 
 extern "C" int tgl_tcsr_build(const int32_t* src, const int32_t* dst, const float* ts, const int32_t* eid,

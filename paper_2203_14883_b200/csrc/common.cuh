@@ -105,6 +105,10 @@ struct tgl_tcsr {
     int n_levels;
     uint64_t level_off[12];  // float offset of level l in index (levels <= 8)
     const void* recs;        // 12-byte slot records {ts, nbr, eid} (tsindex.cuh), or null
-    const void* nodes;       // 64-byte node records {lo, hi, 14 fences} (tsindex.cuh), or null
+    const void* nodes;       // 64-byte node records {lo, hi, 14 fence times | 56 fence codes}, or null
     int64_t node_lo;         // node-sharded handle: global id of local node 0
+    // time codec (tsindex.cuh "time codes"): on when n_codes > 0
+    const void* dict;        // TimeDict (device): sorted distinct times + per-code eid bases
+    const uint8_t* codes;    // per-slot time code
+    int n_codes, packed, bits_nbr, bits_code;
 };

@@ -101,6 +101,13 @@ struct SampleParams {
     const int4* nodes;                      // 64-byte node records {lo, hi, 14 fences} (tsindex.cuh), or null
     const float* lvl[kMaxIndexLevels + 1];  // lvl[l] = index level l (1-based)
     int32_t n_levels;                       // 0 -> no index
+    // time codec (tsindex.cuh "time codes"): node records hold 56 fence codes and the cut probes
+    // read 1-byte codes; packed: 8-byte slot records {nbr | code << bn | eid - eid_base[code]}
+    const uint8_t* codes;    // null -> no codec
+    const float* tval;       // [256] sorted distinct times (+inf padded)
+    const int32_t* tebase;   // [256] eid base per code
+    int32_t packed;
+    uint32_t bn, bc;
     int32_t n_nodes;
     int64_t node_lo;  // node-sharded handles: global id of local node 0 (0 otherwise)
     const int32_t* root_node;
@@ -159,6 +166,17 @@ __device__ __forceinline__ int4 ld_rand_v4(const int4* p) {
     int4 v;
     asm("ld.global.nc.L2::64B.v4.s32 {%0, %1, %2, %3}, [%4];"
         : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
+    return v;
+}
+
+__device__ __forceinline__ uint32_t ld_rand_u8(const uint8_t* p) {
+    uint16_t v;
+    asm("ld.global.nc.L2::64B.u8 %0, [%1];" : "=h"(v) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ uint2 ld_rand_v2(const uint2* p) {
+    uint2 v;
+    asm("ld.global.nc.L2::128B.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "l"(p));
     return v;
 }
 
@@ -231,6 +249,33 @@ __device__ __forceinline__ void lower_bound_multi(const SampleParams& p, uint32_
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
             const bool go = a[j] < b[j], lt = v[j] < x[j];
+            a[j] = go && lt ? mid[j] + 1 : a[j];
+            b[j] = go && !lt ? mid[j] : b[j];
+        }
+    }
+}
+
+// The same searches over the time codes: cut j = first slot in [a[j], b[j]] whose code is >= q[j]
+// (q[j] = #{dictionary times < x[j]}, so code < q[j] <=> ts < x[j]); 64 slots per 64-byte atom.
+__device__ __forceinline__ void lower_bound_multi_codes(const SampleParams& p, uint32_t (&a)[4], uint32_t (&b)[4],
+                                                        const float (&x)[4], uint32_t q4) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+        if (p.n_levels > 0 && b[j] - a[j] > kIndexMin) b[j] = a[j] = lower_bound_ts(p, a[j], b[j], x[j]);
+    uint32_t g = 0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) g = max(g, b[j] - a[j]);
+    const int steps = 32 - __clz((int)__reduce_max_sync(kFull, g));  // all 32 lanes call this
+    for (int it = 0; it < steps; ++it) {
+        uint32_t v[4], mid[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            mid[j] = a[j] + ((b[j] - a[j]) >> 1);
+            v[j] = a[j] < b[j] ? ld_rand_u8(p.codes + mid[j]) : 0u;
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const bool go = a[j] < b[j], lt = v[j] < ((q4 >> (8 * j)) & 0xffu);
             a[j] = go && lt ? mid[j] + 1 : a[j];
             b[j] = go && !lt ? mid[j] : b[j];
         }
@@ -325,15 +370,21 @@ __device__ __forceinline__ float rec_word(const float* rec, int sw, int w) {
 }
 
 // ---------------------------------------------------------------------------- K4a windows
-template <int STRATEGY, bool VALID>
+// TC: the graph has the time codec (node records with 56 fence codes, cut probes over codes)
+template <int STRATEGY, bool VALID, bool TC>
 __global__ void __launch_bounds__(kTile, VALID ? 6 : TGL_WINDOW_MINB) window_kernel(const __grid_constant__ SampleParams p) {
     __shared__ uint32_t s_red[TGL_MAX_SNAPSHOTS][kWarps];
     __shared__ int4 s_rec[kTile * 4];  // the tile's 64-byte node records (16 KB)
+    __shared__ float s_tval[TC ? 256 : 1];  // the codec's sorted distinct times (+inf padded)
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int64_t n = chain_roots(p);
     const int64_t tile = (int64_t)blockIdx.x;
     const int64_t base_i = tile * kTile;
     if (base_i >= n) return;  // capacity-sized grid (l >= 1): tiles past the end do nothing
+    if (TC) {
+        s_tval[threadIdx.x] = __ldg(p.tval + threadIdx.x);  // kTile == 256 entries
+        __syncthreads();
+    }
     const int64_t i = base_i + threadIdx.x;
     const bool valid = i < n;
     const int nsb = p.nsb;
@@ -373,6 +424,7 @@ __global__ void __launch_bounds__(kTile, VALID ? 6 : TGL_WINDOW_MINB) window_ker
     float x[4];
     cuts_of(t, lin, x);
     uint32_t lo = 0, hi = 0, ga[4], gb[4];  // cut j lies in [ga[j], gb[j]]
+    uint32_t xq = 0;                        // TC: code thresholds of x[j] (byte j)
     bool early;                             // some slot is earlier than t: the list must be searched
     if (p.nodes) {
         // 4 lanes read one 64-byte node record (one request per record): rounds q = 0..3 cover the
@@ -388,8 +440,10 @@ __global__ void __launch_bounds__(kTile, VALID ? 6 : TGL_WINDOW_MINB) window_ker
             const int src = q * 8 + quad;
             const int vq = __shfl_sync(kFull, v, src);
             const bool okq = __shfl_sync(kFull, ok, src);
+            // an invalid root reads as an empty list: lo = hi = 0, every fence +inf
+            constexpr int kInfW = TC ? 0x7f7f7f7f : 0x7f800000;
             ch[q] = okq ? ld_rand_v4(p.nodes + (size_t)vq * 4 + part)
-                        : make_int4(part ? 0x7f800000 : 0, part ? 0x7f800000 : 0, 0x7f800000, 0x7f800000);
+                        : make_int4(part ? kInfW : 0, part ? kInfW : 0, kInfW, kInfW);
         }
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
@@ -401,25 +455,65 @@ __global__ void __launch_bounds__(kTile, VALID ? 6 : TGL_WINDOW_MINB) window_ker
         const float* rec = reinterpret_cast<const float*>(wrec + lane * 4);
         lo = __float_as_uint(rec_word(rec, sw, 0));
         hi = __float_as_uint(rec_word(rec, sw, 1));
-        uint32_t packed = 0;
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            // number of fences f[0..13] (= words 2..15) below x[j]; positions >= 14 act as +inf
-            int c = 0;
-#pragma unroll
-            for (int step = 8; step >= 1; step >>= 1) {
-                const int e = min(c + step - 1, kFences);
-                const float f = rec_word(rec, sw, 2 + min(e, kFences - 1));
-                c += (e < kFences && f < x[j]) ? step : 0;
-            }
-            packed |= (uint32_t)c << (8 * j);
-        }
         const uint32_t d = hi - lo;
+        uint32_t packed = 0;
+        if (TC) {
+            // code thresholds q[j] = #{dictionary times < x[j]} (7 halvings over 128 padded
+            // entries).  Chronological roots give a warp one root time (and one inherited bound)
+            // in the usual case: then lanes 0..3 search one cut each and broadcast.
+            const float t0 = __shfl_sync(kFull, t, 0), l0 = __shfl_sync(kFull, lin, 0);
+            if (__all_sync(kFull, t == t0 && lin == l0)) {
+                const int jj = lane & 3;
+                const float xs = jj == 0 ? x[0] : jj == 1 ? x[1] : jj == 2 ? x[2] : x[3];
+                uint32_t qc = 0;
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            const int m = (int)((packed >> (8 * j)) & 0xffu);
-            ga[j] = m ? fence_pos(lo, d, m - 1) + 1 : lo;
-            gb[j] = m < kFences ? fence_pos(lo, d, m) : hi;
+                for (int step = 64; step >= 1; step >>= 1) qc += s_tval[qc + step - 1] < xs ? step : 0u;
+#pragma unroll
+                for (int j = 0; j < 4; ++j) xq |= __shfl_sync(kFull, qc, j) << (8 * j);
+            } else {
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    uint32_t qc = 0;
+#pragma unroll
+                    for (int step = 64; step >= 1; step >>= 1) qc += s_tval[qc + step - 1] < x[j] ? step : 0u;
+                    xq |= qc << (8 * j);
+                }
+            }
+            // #fences < q = 5 c1 + c2 (tsindex.cuh): SWAR byte compares of 7-bit codes -- byte b of
+            // (((q-1) x 0x01) | 0x80) - w keeps its high bit iff b < q, no borrow crosses bytes
+            constexpr uint32_t H = 0x80808080u;
+            const uint32_t s0 = __float_as_uint(rec_word(rec, sw, 2)), s1 = __float_as_uint(rec_word(rec, sw, 3)),
+                           s2 = __float_as_uint(rec_word(rec, sw, 4));
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const uint32_t qc = (xq >> (8 * j)) & 0xffu;
+                const uint32_t Qm = ((max(qc, 1u) - 1u) * 0x01010101u) | H;  // q = 0: masked below
+                const int c1 = __popc((Qm - s0) & H) + __popc((Qm - s1) & H) + __popc((Qm - s2) & H);
+                const uint32_t wg = __float_as_uint(rec_word(rec, sw, 5 + c1));
+                const int m = qc ? 5 * c1 + __popc((Qm - wg) & H) : 0;
+                packed |= (uint32_t)m << (8 * j);
+                ga[j] = m ? code_fence_pos(lo, d, m - 1) + 1 : lo;
+                gb[j] = m < kCodeFences ? code_fence_pos(lo, d, m) : hi;
+            }
+        } else {
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                // number of fences f[0..13] (= words 2..15) below x[j]; positions >= 14 act as +inf
+                int c = 0;
+#pragma unroll
+                for (int step = 8; step >= 1; step >>= 1) {
+                    const int e = min(c + step - 1, kFences);
+                    const float f = rec_word(rec, sw, 2 + min(e, kFences - 1));
+                    c += (e < kFences && f < x[j]) ? step : 0;
+                }
+                packed |= (uint32_t)c << (8 * j);
+            }
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const int m = (int)((packed >> (8 * j)) & 0xffu);
+                ga[j] = m ? fence_pos(lo, d, m - 1) + 1 : lo;
+                gb[j] = m < kFences ? fence_pos(lo, d, m) : hi;
+            }
         }
         early = (packed & 0xffu) != 0;  // f[0] = the first edge time < t
     } else {
@@ -440,7 +534,10 @@ __global__ void __launch_bounds__(kTile, VALID ? 6 : TGL_WINDOW_MINB) window_ker
 #pragma unroll
             for (int j = 0; j < 4; ++j) ga[j] = gb[j] = lo;
         }
-        lower_bound_multi(p, ga, gb, x);  // the whole warp: its step count is a warp reduction
+        if (TC && p.nodes)
+            lower_bound_multi_codes(p, ga, gb, x, xq);  // the whole warp: its step count is a warp reduction
+        else
+            lower_bound_multi(p, ga, gb, x);
 #pragma unroll
         for (int j = 0; j < 4; ++j) cut[j] = ga[j];
 #pragma unroll
@@ -579,7 +676,9 @@ __host__ __device__ inline int copy_warp_words(int nsb, int k, bool picks_in_sme
 
 // PSMEM: uniform picks in shared memory (known at compile time, so LDS/STS instead of generic
 // 64-bit accesses); else in the global workspace
-template <int STRATEGY, bool VALID, int OUTX, bool PSMEM>
+// PK: 8-byte packed slot records of the time codec (decoded through the dictionaries, which sit
+// behind the warps' areas in dynamic shared memory: 2 KB)
+template <int STRATEGY, bool VALID, int OUTX, bool PSMEM, bool PK>
 __global__ void __launch_bounds__(kTile, OUTX == 2 ? 6 : (STRATEGY == TGL_MOST_RECENT ? TGL_COPY_MINB_MR : TGL_COPY_MINB)) copy_kernel(const __grid_constant__ SampleParams p) {
     constexpr bool EXTRA = OUTX == 1;   // per-output data for a following layer / dedup
     constexpr bool GATHER = OUTX == 2;  // fused row gather of the last layer's outputs
@@ -615,6 +714,12 @@ __global__ void __launch_bounds__(kTile, OUTX == 2 ? 6 : (STRATEGY == TGL_MOST_R
         picks = picks_smem ? reinterpret_cast<uint32_t*>(wptr + 4 * nsb)
                            : p.picks_global + ((size_t)tile * kWarps + warp) * nsb * k * 32;
 
+    float* s_tv = reinterpret_cast<float*>(smem + kWarps * copy_warp_words(nsb, k, picks_smem));  // PK only
+    int32_t* s_te = reinterpret_cast<int32_t*>(s_tv + 256);
+    if (PK) {
+        s_tv[threadIdx.x] = __ldg(p.tval + threadIdx.x);  // kTile == 256 entries
+        s_te[threadIdx.x] = __ldg(p.tebase + threadIdx.x);
+    }
     const float t = valid ? p.root_ts[i] : 0.0f;
     troot[lane] = t;
     uint64_t rk = 0;
@@ -781,7 +886,13 @@ __global__ void __launch_bounds__(kTile, OUTX == 2 ? 6 : (STRATEGY == TGL_MOST_R
 #pragma unroll
         for (int u = 0; u < kCopyUnroll; ++u) {
             if (act[u]) {
-                if (p.recs) {
+                if (PK) {
+                    const uint2 v = ld_rand_v2(reinterpret_cast<const uint2*>(p.recs) + pos[u]);
+                    const uint64_t w = ((uint64_t)v.y << 32) | v.x;
+                    const uint32_t c = (uint32_t)(w >> p.bn) & ((1u << p.bc) - 1u);
+                    rec[u] = make_int4(__float_as_int(s_tv[c]), (int32_t)(uint32_t)(w & ((1ull << p.bn) - 1ull)),
+                                       s_te[c] + (int32_t)(uint32_t)(w >> (p.bn + p.bc)), 0);
+                } else if (p.recs) {
                     const int* w = reinterpret_cast<const int*>(p.recs + pos[u]);
                     rec[u] = make_int4(ld_rand_s32(w), ld_rand_s32(w + 1), ld_rand_s32(w + 2), 0);
                 } else {
@@ -889,6 +1000,32 @@ __global__ void dedup_emit_kernel(const int32_t* __restrict__ nbr, const float* 
             if (uniq_key) uniq_key[u] = child_key[i];
         }
     }
+}
+
+// the graph's arrays and aux structures in the kernel parameters.  The validity path (R#28) reads
+// neither codec structure: with the codec its node records are the plain indptr + ts search and
+// packed slot records fall back to the separate arrays
+static void set_graph(SampleParams& sp, const tgl_tcsr* g, bool use_recs, bool use_index, bool validity) {
+    sp.indptr = g->indptr;
+    sp.nbr = g->nbr;
+    sp.ts = g->ts;
+    sp.eid = g->eid;
+    const bool codec = use_recs && g->n_codes > 0;
+    sp.recs = use_recs && !(validity && g->packed) ? static_cast<const SlotRec*>(g->recs) : nullptr;
+    sp.nodes = use_recs && !(validity && codec) ? static_cast<const int4*>(g->nodes) : nullptr;
+    if (codec && !validity) {
+        const TimeDict* d = static_cast<const TimeDict*>(g->dict);
+        sp.codes = g->codes;
+        sp.tval = d->value;
+        sp.tebase = d->eid_base;
+        sp.packed = g->packed;
+        sp.bn = (uint32_t)g->bits_nbr;
+        sp.bc = (uint32_t)g->bits_code;
+    }
+    sp.n_levels = use_index && g->index ? g->n_levels : 0;
+    for (int q = 1; q <= sp.n_levels; ++q) sp.lvl[q] = g->index + g->level_off[q];
+    sp.n_nodes = g->n_nodes;
+    sp.node_lo = g->node_lo;
 }
 
 static bool picks_fit_smem(int nsb, int k) { return (size_t)nsb * k * 32 * 4 <= kPicksSmemPerWarp; }
@@ -999,16 +1136,17 @@ static int plan_sample(int64_t n_roots, int L, const int32_t* fanouts, int S, in
     return TGL_OK;
 }
 
-template <int STRATEGY, bool VALID, int OUTX, bool PSMEM>
-static void launch_copy_ps(const SampleParams& sp, int64_t grid, size_t smem, cudaStream_t st) {
+template <int STRATEGY, bool VALID, int OUTX, bool PSMEM, bool PK>
+static void launch_copy_pk(const SampleParams& sp, int64_t grid, size_t smem, cudaStream_t st) {
+    if (PK) smem += 256 * (sizeof(float) + sizeof(int32_t));  // the codec's dictionaries
     if (smem + 1024 > 48 * 1024)  // the dynamic part plus ~640 B of static shared memory
-        cudaFuncSetAttribute(copy_kernel<STRATEGY, VALID, OUTX, PSMEM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaFuncSetAttribute(copy_kernel<STRATEGY, VALID, OUTX, PSMEM, PK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)smem);
     // programmatic dependent launch (PDL): the copy grid is launched while the window grid's last
     // CTAs finish and waits in griddepcontrol.wait -- hides the launch gap between the two
     static const bool no_pdl = getenv("TGL_NO_PDL") != nullptr;  // A/B knob
     if (no_pdl) {
-        copy_kernel<STRATEGY, VALID, OUTX, PSMEM><<<(unsigned)grid, kTile, smem, st>>>(sp);
+        copy_kernel<STRATEGY, VALID, OUTX, PSMEM, PK><<<(unsigned)grid, kTile, smem, st>>>(sp);
         return;
     }
     cudaLaunchConfig_t cfg = {};
@@ -1021,7 +1159,16 @@ static void launch_copy_ps(const SampleParams& sp, int64_t grid, size_t smem, cu
     at[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    cudaLaunchKernelEx(&cfg, copy_kernel<STRATEGY, VALID, OUTX, PSMEM>, sp);
+    cudaLaunchKernelEx(&cfg, copy_kernel<STRATEGY, VALID, OUTX, PSMEM, PK>, sp);
+}
+
+// packed records exist only with the codec, which the validity path never uses
+template <int STRATEGY, bool VALID, int OUTX, bool PSMEM>
+static void launch_copy_ps(const SampleParams& sp, int64_t grid, size_t smem, cudaStream_t st) {
+    if (!VALID && sp.packed)
+        launch_copy_pk<STRATEGY, VALID, OUTX, PSMEM, !VALID>(sp, grid, smem, st);
+    else
+        launch_copy_pk<STRATEGY, VALID, OUTX, PSMEM, false>(sp, grid, smem, st);
 }
 
 template <int STRATEGY, bool VALID, int OUTX>
@@ -1036,7 +1183,10 @@ static void launch_copy(const SampleParams& sp, int64_t grid, size_t smem, cudaS
 // key / time / lower bound); the last layer's copy carries none of it
 template <int STRATEGY, bool VALID>
 static int launch_pair(const SampleParams& sp, int64_t grid, size_t smem, cudaStream_t st) {
-    window_kernel<STRATEGY, VALID><<<(unsigned)grid, kTile, 0, st>>>(sp);
+    if (!VALID && sp.codes)
+        window_kernel<STRATEGY, VALID, !VALID><<<(unsigned)grid, kTile, 0, st>>>(sp);
+    else
+        window_kernel<STRATEGY, VALID, false><<<(unsigned)grid, kTile, 0, st>>>(sp);
     bool extra = false;
     for (int b = 0; b < sp.nsb; ++b)
         extra |= sp.out[b].ts_edge || sp.out[b].child_key || sp.out[b].child_t || sp.out[b].child_lo;
@@ -1128,16 +1278,7 @@ int sample_chain(const tgl_tcsr* g, int layer, int snap0, int nsb, const int32_t
         return TGL_ECUDA;
     SampleParams sp;
     memset(&sp, 0, sizeof(sp));
-    sp.indptr = g->indptr;
-    sp.nbr = g->nbr;
-    sp.ts = g->ts;
-    sp.eid = g->eid;
-    sp.recs = static_cast<const SlotRec*>(g->recs);
-    sp.nodes = static_cast<const int4*>(g->nodes);
-    sp.n_levels = g->index ? g->n_levels : 0;
-    for (int q = 1; q <= sp.n_levels; ++q) sp.lvl[q] = g->index + g->level_off[q];
-    sp.n_nodes = g->n_nodes;
-    sp.node_lo = g->node_lo;
+    set_graph(sp, g, g->recs != nullptr, g->index != nullptr, false);
     sp.root_node = rn;
     sp.root_ts = rt;
     sp.root_key = rk;
@@ -1282,16 +1423,7 @@ static int sample_impl(const tgl_tcsr* g, const int32_t* roots, const float* roo
         cudaStream_t cst = fk && l > 0 ? fk->side[s] : st;
         SampleParams sp;
         memset(&sp, 0, sizeof(sp));
-        sp.indptr = g->indptr;
-        sp.nbr = g->nbr;
-        sp.ts = g->ts;
-        sp.eid = g->eid;
-        sp.recs = use_recs ? static_cast<const SlotRec*>(g->recs) : nullptr;
-        sp.nodes = use_recs ? static_cast<const int4*>(g->nodes) : nullptr;
-        sp.n_levels = use_index ? g->n_levels : 0;
-        for (int q = 1; q <= sp.n_levels; ++q) sp.lvl[q] = g->index + g->level_off[q];
-        sp.n_nodes = g->n_nodes;
-        sp.node_lo = g->node_lo;
+        set_graph(sp, g, use_recs, use_index, o.edge_valid != nullptr);
         if (l == 0) {
             sp.root_node = roots;
             sp.root_ts = root_ts;

@@ -78,20 +78,69 @@ __host__ __device__ inline uint32_t fence_pos(uint32_t lo, uint32_t d, int j) {
     return lo + (uint32_t)(((uint64_t)j * (uint64_t)(d - 1)) / (uint64_t)(kFences - 1));
 }
 
+// ---------------------------------------------------------------------------- time codes
+// When the T-CSR holds at most kMaxCodes distinct timestamps -- MAG's are publication years,
+// max(t) = 120 (Table 3) -- the aux build adds a lossless time codec: the sorted
+// distinct values value[0..D) (a dictionary) and per slot its code = index of its ts in value[].
+// Codes order like the times (ts < x  <=>  code < q(x), q(x) = #{values < x}), so the cut search
+// runs on 7-bit codes: a 64-byte node record holds 54 fence codes instead of 14 fence times (gaps
+// of d/53 slots instead of d/13), and a 64-byte probe atom covers 64 slots instead of 16.  When the
+// widths fit, the slot record shrinks to 8 bytes: nbr | code << bn | (eid - eid_base[code]) << (bn
+// + bc); the copy kernel decodes ts = value[code] (the exact stored float) and eid from
+// dictionaries in shared memory.  Requests per C5 root (tools/census_c5.py): probes 0.59 -> 0.19,
+// selected-record lines 1.01 -> 0.83.
+//
+// Node record under the codec (16 words): w0 = lo, w1 = hi, w2..w4 = 10 separator codes (+ 2 pad
+// bytes), w5..w15 = 11 groups of 4 codes.  Fence j = 5g + r (P_j = lo + floor(j (d-1) / 53)) is
+// byte r of group g for r < 4 and separator g for r = 4, so #fences < q = 5 c1 + c2 with c1 =
+// #separators < q and c2 = #codes < q in group c1 -- two SWAR byte compares (codes < 128: no
+// borrow crosses a byte) instead of a 6-step binary search.  Code 127 (pads, empty lists) is +inf.
+constexpr int kMaxCodes = 127;   // 7-bit codes, q(x) <= 127; code 127 = +inf
+constexpr int kCodeFences = 54;  // 10 separators + 11 groups of 4
+constexpr int kCodeSeps = 10;
+constexpr uint32_t kCodeInf = 127u;
+constexpr uint32_t kDictMagic = 0x54474344u;  // "TGCD"
+struct TimeDict {
+    uint32_t magic;
+    uint32_t n_codes;    // D (0: no codec: more than kMaxCodes distinct times, or -0 / non-finite)
+    uint32_t packed;     // 1: 8-byte packed slot records
+    uint32_t bits_nbr;   // bn
+    uint32_t bits_code;  // bc
+    uint32_t pad[3];
+    float value[256];       // sorted distinct timestamps, +inf beyond D
+    int32_t eid_base[256];  // smallest eid of each code (packed records)
+};
+// build scratch behind the dictionary (aux build only)
+struct CodecScratch {
+    uint32_t hash[512];  // distinct ts bits (open addressing, 0xffffffff = empty)
+    int32_t eid_min[256], eid_max[256];
+    uint32_t count, overflow, nbr_max, pad;
+};
+constexpr uint64_t kDictBytes = 8192;
+static_assert(sizeof(TimeDict) + sizeof(CodecScratch) <= kDictBytes, "dictionary region");
+
+__host__ __device__ inline uint32_t code_fence_pos(uint32_t lo, uint32_t d, int j) {
+    if (d <= (1u << 26)) return lo + ((uint32_t)j * (d - 1u)) / (uint32_t)(kCodeFences - 1);
+    return lo + (uint32_t)(((uint64_t)j * (uint64_t)(d - 1)) / (uint64_t)(kCodeFences - 1));
+}
+
 struct AuxLayout {
     IndexLayout index;
-    uint64_t rec_off = 0;   // byte offset of the SlotRec array
-    uint64_t node_off = 0;  // byte offset of the NodeRec array
+    uint64_t index_off = 0;  // byte offset of the index levels (after the dictionary region)
+    uint64_t rec_off = 0;    // byte offset of the slot records (12-byte SlotRec, or 8-byte packed)
+    uint64_t node_off = 0;   // byte offset of the NodeRec array
+    uint64_t code_off = 0;   // byte offset of the per-slot time codes (u8)
     uint64_t bytes = 0;
 };
 
 inline AuxLayout aux_layout(uint64_t n_stored, uint64_t n_nodes) {
     AuxLayout A;
     A.index = index_layout(n_stored);
-    A.rec_off = align_up(A.index.floats * sizeof(float), 256);
+    A.index_off = kDictBytes;
+    A.rec_off = align_up(A.index_off + A.index.floats * sizeof(float), 256);
     A.node_off = align_up(A.rec_off + n_stored * sizeof(SlotRec), 256);
-    A.bytes = align_up(A.node_off + n_nodes * sizeof(NodeRec), 256);
-    if (A.bytes < 256) A.bytes = 256;
+    A.code_off = align_up(A.node_off + n_nodes * sizeof(NodeRec), 256);
+    A.bytes = align_up(A.code_off + n_stored + 64, 256);  // + 64: whole-atom probe reads
     return A;
 }
 

@@ -37,7 +37,7 @@ def test_host_only_calls_without_gpu():
     """Calls that do no device work: version, strerror, capacity and workspace queries."""
     import paper_2203_14883_b200 as tgl
     L = tgl._L
-    assert L.tgl_abi_version() == 2
+    assert L.tgl_abi_version() == 3
     assert L.tgl_strerror(-2) == b"node or row id out of range"
     b = ctypes.c_size_t()
     assert L.tgl_tcsr_build_workspace(1000, 50, 1, ctypes.byref(b)) == 0 and b.value > 0

@@ -36,7 +36,8 @@ r, t = chunks[-1]
 lo = g.indptr[r.long()]
 hi = g.indptr[r.long() + 1]
 first = torch.where(hi > lo, g.ts[lo.clamp(max=g.ts.numel() - 1)], torch.full_like(t, float("inf")))
-print(json.dumps({"roots": int(r.numel()), "first_ge_t": float((first >= t).float().mean())}), flush=True)
+print(json.dumps({"roots": int(r.numel()), "first_ge_t": float((first >= t).float().mean()), "codec": g.codec}),
+      flush=True)
 
 for env in json.loads(args.settings):
     for k in [k for k in os.environ if k.startswith("TGL_") and k != "TGL_LIB_PATH"]:
