@@ -98,7 +98,7 @@ TGL_API int tgl_tcsr_build_workspace(int64_t n_edges, int32_t n_nodes, int add_r
  *   sampler reads timestamps in aligned 16-float (64-byte, one HBM atom) groups.
  * aux (optional, may be NULL): >= tgl_tcsr_aux_bytes(E_s, V) bytes, 256-byte aligned; filled with
  *   the sampler's acceleration structures over the T-CSR: the 16-ary index over ts_out (long-list
- *   cut search), a 12-byte record {ts, nbr, eid} per slot (payload copy: one request per run)
+ *   cut search), a 16-byte record {ts, nbr, eid, 0} per slot (payload copy: one load per output)
  *   and a 64-byte record {lo, hi, 14 fence times} per node (list bounds and cut gaps in one
  *   load) -- DESIGN.md "Data layout".  Without it the sampler reads the separate arrays.
  *   Time codec: when the T-CSR holds at most 255 distinct timestamps (all finite, >= +0; e.g.

@@ -22,7 +22,7 @@
 //                      uniform: Floyd's k-subset with Philox4x32-10 draws, ascending (R#5, R#6);
 //                      then the tile's outputs are copied as one flat range per snapshot -- lane o
 //                      finds its root by a 5-step search over the warp's inclusive counts -- loading
-//                      the selected 12-byte slot record {ts, nbr, eid} (one request per run of
+//                      the selected slot record {ts, nbr, eid} (16 bytes, or 8 packed: one load per output, one request per run of
 //                      slots) and storing (nbr, eid, dt[, ts_edge, child key, child lo]) as
 //                      coalesced runs (a9, a10; K6 fused).
 // dt = t_root (-) t_edge with __fsub_rn; window bounds with __fmul_rn / __fsub_rn (R#12).
@@ -97,7 +97,7 @@ struct SampleParams {
     const int32_t* nbr;
     const float* ts;
     const int32_t* eid;
-    const SlotRec* recs;                    // slot records {ts, nbr, eid[, 0]} (tsindex.cuh), or null
+    const SlotRec* recs;                    // slot records {ts, nbr, eid, 0} (tsindex.cuh), 8-byte packed, or null
     const int4* nodes;                      // 64-byte node records {lo, hi, 14 fences} (tsindex.cuh), or null
     const float* lvl[kMaxIndexLevels + 1];  // lvl[l] = index level l (1-based)
     int32_t n_levels;                       // 0 -> no index
@@ -155,11 +155,18 @@ __device__ __forceinline__ float ld_rand_f32(const float* p) {
     asm("ld.global.nc.L2::64B.f32 %0, [%1];" : "=f"(v) : "l"(p));
     return v;
 }
-// slot records (copy kernel): a run of <= k 12-byte records, 128-byte fills (64 / 256: +-1 %,
-// profiles/r02/experiments/recfill_ktime_C5.txt)
-__device__ __forceinline__ int32_t ld_rand_s32(const int32_t* p) {
-    int32_t v;
-    asm("ld.global.nc.L2::128B.s32 %0, [%1];" : "=r"(v) : "l"(p));
+// slot records (copy kernel), one aligned load per output: most_recent reads runs of <= k records
+// (128-byte fills; 64 / 256: +-1 %, profiles/r02/experiments/recfill_ktime_C5.txt), uniform reads
+// scattered single records (64-byte fills: half the DRAM bytes of a line per pick)
+template <bool RUNS>
+__device__ __forceinline__ int4 ld_rec16(const SlotRec* p) {
+    int4 v;
+    if (RUNS)
+        asm("ld.global.nc.L2::128B.v4.s32 {%0, %1, %2, %3}, [%4];"
+            : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
+    else
+        asm("ld.global.nc.L2::64B.v4.s32 {%0, %1, %2, %3}, [%4];"
+            : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
     return v;
 }
 __device__ __forceinline__ int4 ld_rand_v4(const int4* p) {
@@ -603,8 +610,9 @@ __global__ void __launch_bounds__(kTile, VALID ? 6 : TGL_WINDOW_MINB) window_ker
 // mod 4 of Philox4x32-10 at counter (j / 4, ctr1, rk); r_j = floor(x_j (m_j + 1) / 2^32),
 // m_j = c - k + j; pick j = r_j unless an earlier pick equals it, else m_j (> every earlier pick).
 // The picks are kept ascending (R#13) by a compare-exchange chain after each draw (static register
-// indices) and stored to the lane's column of picks (stride 32).  Same set and order as the
-// shared-memory insertion below -- which ran each draw's shift loop at the warp's slowest lane.
+// indices) and stored at pk[0..k) (the window's place in the warp's flat output order).  Same set
+// and order as the shared-memory insertion below -- which ran each draw's shift loop at the warp's
+// slowest lane.
 constexpr int kFloydRegs = 16;
 __device__ __forceinline__ void floyd_in_registers(uint32_t* pk, uint32_t len, int k, uint32_t ctr1, uint64_t rk,
                                                    uint32_t seed_lo, uint32_t seed_hi) {
@@ -634,7 +642,7 @@ __device__ __forceinline__ void floyd_in_registers(uint32_t* pk, uint32_t len, i
     }
 #pragma unroll
     for (int j = 0; j < kFloydRegs; ++j)
-        if (j < k) pk[j * 32] = a[j];
+        if (j < k) pk[j] = a[j];
 }
 
 // the fused gather of one group of (up to 32) outputs held one per lane
@@ -746,33 +754,37 @@ __global__ void __launch_bounds__(kTile, OUTX == 2 ? 6 : (STRATEGY == TGL_MOST_R
         const uint32_t wtot = __shfl_sync(kFull, x, 31);
         if (lane == 31) s_wsum[b][warp] = x;
         const uint32_t nz = __ballot_sync(kFull, take > 0);
+        const uint32_t fstart = flat + x - take;  // warp-flat index of this window's first output
         if (take > 0)
             seg[nseg + __popc(nz & lanemask_lt())] =
-                make_uint2(((flat + x - take) << 9) | ((uint32_t)b << 5) | (uint32_t)lane, first);
+                make_uint2((fstart << 9) | ((uint32_t)b << 5) | (uint32_t)lane, first);
         nseg += __popc(nz);
         flat += wtot;
         if (STRATEGY == TGL_UNIFORM && !VALID) {
-            uint32_t* pk = picks + (size_t)b * k * 32 + lane;  // pick q at pk[q * 32]
+            // pick q of this window at picks[fstart + q]: stored in the warp's flat output order, so
+            // the copy loop's 32 lanes read 32 consecutive words (the [q][root] layout put a root's
+            // picks in one bank: ~10-way conflicts per read, profiles/r02/c4)
+            uint32_t* pk = picks + fstart;
             const uint32_t ctr1 = ((uint32_t)p.layer << 16) | (uint32_t)(p.layer == 0 ? b : p.snap0);
             uint4 rnd = make_uint4(0u, 0u, 0u, 0u);
             if (!p.replacement && len <= (uint32_t)k) {
-                for (uint32_t q = 0; q < len; ++q) pk[q * 32] = q;
+                for (uint32_t q = 0; q < len; ++q) pk[q] = q;
             } else if (p.replacement) {
                 // with replacement (R#24): r_j uniform in [0, c) from the counter of Floyd's draw j
                 for (uint32_t j = 0; j < take; ++j) {
                     if ((j & 3u) == 0)
                         rnd = philox4x32_10(make_uint4(j >> 2, ctr1, (uint32_t)rk, (uint32_t)(rk >> 32)), p.seed_lo,
                                             p.seed_hi);
-                    pk[j * 32] = __umulhi(draw_word(rnd, j), len);
+                    pk[j] = __umulhi(draw_word(rnd, j), len);
                 }
                 for (int j = 1; j < (int)take; ++j) {  // ascending slot order (R#13)
-                    const uint32_t xj = pk[j * 32];
+                    const uint32_t xj = pk[j];
                     int q = j - 1;
-                    while (q >= 0 && pk[q * 32] > xj) {
-                        pk[(q + 1) * 32] = pk[q * 32];
+                    while (q >= 0 && pk[q] > xj) {
+                        pk[q + 1] = pk[q];
                         --q;
                     }
-                    pk[(q + 1) * 32] = xj;
+                    pk[q + 1] = xj;
                 }
             } else if (k <= kFloydRegs) {
                 // Floyd (R#5, R#6) with the picks in registers: the k draws and their membership
@@ -792,15 +804,15 @@ __global__ void __launch_bounds__(kTile, OUTX == 2 ? 6 : (STRATEGY == TGL_MOST_R
                     // the output -- is Floyd's; only the sort is merged into the draws.
                     int q = j - 1;
                     uint32_t v = 0;
-                    while (q >= 0 && (v = pk[q * 32]) > rr) {
-                        pk[(q + 1) * 32] = v;
+                    while (q >= 0 && (v = pk[q]) > rr) {
+                        pk[q + 1] = v;
                         --q;
                     }
                     if (q >= 0 && v == rr) {
-                        for (int u = q + 1; u < j; ++u) pk[u * 32] = pk[(u + 1) * 32];
-                        pk[j * 32] = m;
+                        for (int u = q + 1; u < j; ++u) pk[u] = pk[u + 1];
+                        pk[j] = m;
                     } else {
-                        pk[(q + 1) * 32] = rr;
+                        pk[q + 1] = rr;
                     }
                 }
             }
@@ -878,8 +890,7 @@ __global__ void __launch_bounds__(kTile, OUTX == 2 ? 6 : (STRATEGY == TGL_MOST_R
             } else if (STRATEGY == TGL_MOST_RECENT) {
                 pos[u] = sg.y + q;
             } else {
-                const uint32_t b = (sg.x >> 5) & 15u, r = sg.x & 31u;
-                pos[u] = act[u] ? sg.y + picks[((size_t)b * k + q) * 32 + r] : 0u;
+                pos[u] = act[u] ? sg.y + picks[o] : 0u;
             }
         }
         int4 rec[kCopyUnroll];
@@ -893,8 +904,7 @@ __global__ void __launch_bounds__(kTile, OUTX == 2 ? 6 : (STRATEGY == TGL_MOST_R
                     rec[u] = make_int4(__float_as_int(s_tv[c]), (int32_t)(uint32_t)(w & ((1ull << p.bn) - 1ull)),
                                        s_te[c] + (int32_t)(uint32_t)(w >> (p.bn + p.bc)), 0);
                 } else if (p.recs) {
-                    const int* w = reinterpret_cast<const int*>(p.recs + pos[u]);
-                    rec[u] = make_int4(ld_rand_s32(w), ld_rand_s32(w + 1), ld_rand_s32(w + 2), 0);
+                    rec[u] = ld_rec16<STRATEGY == TGL_MOST_RECENT && !VALID>(p.recs + pos[u]);
                 } else {
                     rec[u] = make_int4(__float_as_int(__ldg(p.ts + pos[u])), __ldg(p.nbr + pos[u]),
                                        __ldg(p.eid + pos[u]), 0);

@@ -47,14 +47,16 @@ inline IndexLayout index_layout(uint64_t n_stored) {
 }
 
 // The sampler's auxiliary ("aux") buffer: [ts atom index | slot records].  A slot record is the
-// 12-byte {ts, nbr, eid} of one T-CSR slot, so the cut search and the payload copy of the
-// selected slots read the SAME lines: one DRAM row activation per list instead of one per array
-// (HBM serves ~33 G random requests/s).
-constexpr int kRecWords = 3;  // {ts, nbr, eid}: 12 bytes (16-byte records: copy kernel 2.3 % slower)
+// {ts, nbr, eid} of one T-CSR slot, padded to 16 bytes so that the copy kernel reads it with ONE
+// aligned 16-byte load per output: three 4-byte loads per output kept the uniform copy kernel at
+// 94 % of its L1 throughput (C4 layer 1, profiles/r02/c4); 12- vs 16-byte records were within
+// 2.3 % on C5 runs, which now use the codec's 8-byte packed records.
+constexpr int kRecWords = 4;  // {ts, nbr, eid, 0}: 16 bytes
 struct SlotRec {
     float ts;
     int32_t nbr;
     int32_t eid;
+    int32_t pad;
 };
 static_assert(sizeof(SlotRec) == 4 * kRecWords, "slot record size");
 
@@ -127,7 +129,7 @@ __host__ __device__ inline uint32_t code_fence_pos(uint32_t lo, uint32_t d, int 
 struct AuxLayout {
     IndexLayout index;
     uint64_t index_off = 0;  // byte offset of the index levels (after the dictionary region)
-    uint64_t rec_off = 0;    // byte offset of the slot records (12-byte SlotRec, or 8-byte packed)
+    uint64_t rec_off = 0;    // byte offset of the slot records (16-byte SlotRec, or 8-byte packed)
     uint64_t node_off = 0;   // byte offset of the NodeRec array
     uint64_t code_off = 0;   // byte offset of the per-slot time codes (u8)
     uint64_t bytes = 0;
