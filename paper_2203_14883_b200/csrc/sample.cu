@@ -51,9 +51,11 @@ namespace tgl {
 constexpr int kTile = 256;  // roots per tile (one lane per root)
 constexpr int kWarps = kTile / 32;
 #ifndef TGL_COPY_UNROLL
-#define TGL_COPY_UNROLL 2
+#define TGL_COPY_UNROLL 2  // most_recent (C5: 1 / 3 / 4 slower, profiles/r02/experiments/codec_copy_unroll_C5.txt)
 #endif
-constexpr int kCopyUnroll = TGL_COPY_UNROLL;  // outputs in flight per lane in the flat copy
+#ifndef TGL_COPY_UNROLL_UNI
+#define TGL_COPY_UNROLL_UNI 2
+#endif
 constexpr int kSuperShift = 6;  // 64 tiles per super tile (tile bases: super totals + tile totals)
 #ifndef TGL_INDEX_MIN
 #define TGL_INDEX_MIN 128  // r02 C4 window: 128 388 us, 512 401, 4096 407 (C5 unchanged); r01 kernels preferred 4096
@@ -863,6 +865,7 @@ __global__ void __launch_bounds__(kTile, OUTX == 2 ? 6 : (STRATEGY == TGL_MOST_R
     const uint32_t total = flat;
     const uint32_t lemask = lanemask_lt() | (1u << lane);
     uint32_t hbase = 0;  // windows starting before o0
+    constexpr int kCopyUnroll = STRATEGY == TGL_MOST_RECENT ? TGL_COPY_UNROLL : TGL_COPY_UNROLL_UNI;  // outputs in flight per lane
     for (uint32_t o0 = 0; o0 < total; o0 += 32 * kCopyUnroll) {
         uint32_t pos[kCopyUnroll], info[kCopyUnroll], oo[kCopyUnroll];
         bool act[kCopyUnroll];
