@@ -189,6 +189,11 @@ __device__ __forceinline__ uint2 ld_rand_v2(const uint2* p) {
     return v;
 }
 
+template <typename T>
+__device__ __forceinline__ void st_global_u32(T* p, uint32_t v) {
+    asm volatile("st.global.u32 [%0], %1;" ::"l"(p), "r"(v));  // outputs are not re-read by the kernel
+}
+
 // ---------------------------------------------------------------------------- cut search
 // first slot in [a, b) with ts >= x, else b (R#2).  Long lists first descend the 16-ary index
 // (tsindex.cuh): per level a binary search over <= 16 consecutive index entries (one 64-byte
@@ -740,11 +745,35 @@ __global__ void __launch_bounds__(kTile, OUTX == 2 ? 6 : (STRATEGY == TGL_MOST_R
     // everything below reads the window kernel's outputs: wait for that grid (a no-op when the
     // copy kernel was launched without programmatic stream serialisation)
     asm volatile("griddepcontrol.wait;" ::: "memory");
+    // The prologue's loads -- this root's cuts and, in warps b < nsb, block b's tile-base totals --
+    // are issued together: one memory round trip instead of one per cut and per total level.  The
+    // copy kernel's CTAs are short (256 roots), so a chain of dependent prologue loads (8 round
+    // trips) was half of its time on C5 (208 of 409 us with the flat copy removed).
+    constexpr int kPre = 4;  // cuts c_0 .. c_3 prefetched (nsb <= 3: all of them)
+    uint32_t cpre[kPre];
+#pragma unroll
+    for (int j = 0; j < kPre; ++j) cpre[j] = (valid && j <= nsb) ? p.cuts[(size_t)j * p.roots_cap + i] : 0u;
+    uint64_t tb_acc = 0;  // warp b < nsb: block b's totals before this tile (lane partial sums)
+    {
+        const int b = warp;
+        if (b < nsb) {
+            const int64_t t = tile, sup = t >> kSuperShift, hyp = t >> (2 * kSuperShift);
+            // <= 63 super totals and <= 63 tile totals: two lanes' worth each, loaded at once
+            const int64_t s0 = (hyp << kSuperShift) + lane, t0 = (sup << kSuperShift) + lane;
+            const uint64_t* st = p.super_tot + (size_t)b * p.supers_cap;
+            const uint32_t* tt = p.tile_tot + (size_t)b * p.tiles_cap;
+            const uint64_t a0 = s0 < sup ? st[s0] : 0ull, a1 = s0 + 32 < sup ? st[s0 + 32] : 0ull;
+            const uint32_t a2 = t0 < t ? tt[t0] : 0u, a3 = t0 + 32 < t ? tt[t0 + 32] : 0u;
+            for (int64_t q = lane; q < hyp; q += 32) tb_acc += p.hyper_tot[(size_t)b * p.hypers_cap + q];
+            tb_acc += a0 + a1 + a2 + a3;
+        }
+    }
     // counts, warp-local prefix, the segment list; uniform picks
-    uint32_t cb = valid ? p.cuts[i] : 0u;  // c_b
-    uint32_t flat = 0, nseg = 0;           // warp outputs / non-empty windows of the blocks before b
+    uint32_t cb = cpre[0];       // c_b
+    uint32_t flat = 0, nseg = 0;  // warp outputs / non-empty windows of the blocks before b
     for (int b = 0; b < nsb; ++b) {
-        const uint32_t cn = valid ? p.cuts[(size_t)(b + 1) * p.roots_cap + i] : 0u;  // c_(b+1)
+        const uint32_t cn = b + 1 < kPre ? (b == 0 ? cpre[1] : b == 1 ? cpre[2] : cpre[3])
+                                         : (valid ? p.cuts[(size_t)(b + 1) * p.roots_cap + i] : 0u);  // c_(b+1)
         const uint32_t len = cb - cn;                                                 // window size c
         const uint32_t take = VALID ? (valid ? p.vtake[(size_t)b * p.roots_cap + i] : 0u)
                                     : (p.replacement ? (len ? (uint32_t)k : 0u) : (len < (uint32_t)k ? len : (uint32_t)k));
@@ -820,10 +849,16 @@ __global__ void __launch_bounds__(kTile, OUTX == 2 ? 6 : (STRATEGY == TGL_MOST_R
             }
         }
     }
-    // tile base per snapshot: warp b sums the hyper totals before this tile's hyper tile, the super
-    // totals before its super tile inside it and the tile totals before it inside its super tile
-    // (all final: the window kernel has completed)
-    for (int b = warp; b < nsb; b += kWarps) {
+    // tile base per snapshot (loaded above): warp b sums the hyper totals before this tile's hyper tile, the super totals
+    // before its super tile inside it and the tile totals before it inside its super tile (all
+    // final: the window kernel has completed); blocks beyond the warp count (nsb > 8) here
+    if (warp < nsb) {
+        uint64_t acc = tb_acc;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(kFull, acc, o);
+        if (lane == 0) s_tbase[warp] = acc;
+    }
+    for (int b = warp + kWarps; b < nsb; b += kWarps) {
         const int64_t t = tile, sup = t >> kSuperShift, hyp = t >> (2 * kSuperShift);
         uint64_t acc = 0;
         for (int64_t q = lane; q < hyp; q += 32) acc += p.hyper_tot[(size_t)b * p.hypers_cap + q];
@@ -922,9 +957,11 @@ __global__ void __launch_bounds__(kTile, OUTX == 2 ? 6 : (STRATEGY == TGL_MOST_R
             float* dtp = reinterpret_cast<float*>(wptr[b * 4 + 2]);
             const float tv = __int_as_float(rec[u].x);
             const float tr = troot[r];
-            reinterpret_cast<int32_t*>(pne.x)[oo[u]] = rec[u].y;
-            reinterpret_cast<int32_t*>(pne.y)[oo[u]] = rec[u].z;
-            dtp[oo[u]] = __fsub_rn(tr, tv);
+            // global-space stores (the pointers come from shared memory, so plain C++ stores compile
+            // to generic ST.E; measured neutral on C4 / C5, kept for the SASS)
+            st_global_u32(reinterpret_cast<int32_t*>(pne.x) + oo[u], (uint32_t)rec[u].y);
+            st_global_u32(reinterpret_cast<int32_t*>(pne.y) + oo[u], (uint32_t)rec[u].z);
+            st_global_u32(dtp + oo[u], __float_as_uint(__fsub_rn(tr, tv)));
             if (EXTRA) {
                 const BlockOut& o = p.out[b];
                 const uint64_t oi = (uint64_t)((reinterpret_cast<int32_t*>(pne.x) + oo[u]) - o.nbr);
