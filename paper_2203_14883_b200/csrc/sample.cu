@@ -395,22 +395,28 @@ __global__ void __launch_bounds__(kTile, VALID ? 6 : TGL_WINDOW_MINB) window_ker
     const int64_t tile = (int64_t)blockIdx.x;
     const int64_t base_i = tile * kTile;
     if (base_i >= n) return;  // capacity-sized grid (l >= 1): tiles past the end do nothing
-    if (TC) {
-        s_tval[threadIdx.x] = __ldg(p.tval + threadIdx.x);  // kTile == 256 entries
-        __syncthreads();
-    }
     const int64_t i = base_i + threadIdx.x;
     const bool valid = i < n;
     const int nsb = p.nsb;
     const uint32_t k = (uint32_t)p.k;
 
+    // the root loads are issued before the codec dictionary's barrier, so the two overlap
+    int32_t rn = 0;
+    float t = 0.0f, lin_raw = -INFINITY;
+    if (valid) {
+        rn = p.root_node[i];
+        t = p.root_ts[i];
+        if (p.layer > 0 && p.root_lo) lin_raw = p.root_lo[i];
+    }
+    if (TC) {
+        s_tval[threadIdx.x] = __ldg(p.tval + threadIdx.x);  // kTile == 256 entries
+        __syncthreads();
+    }
     int32_t v = 0;
-    float t = 0.0f;
     bool ok = false;
     if (valid) {
-        const int64_t vg = (int64_t)p.root_node[i] - p.node_lo;  // shard-local node id
+        const int64_t vg = (int64_t)rn - p.node_lo;  // shard-local node id
         v = (int32_t)vg;
-        t = p.root_ts[i];
         if (vg < 0 || vg >= (int64_t)p.n_nodes)
             atomicOr(p.err, kErrRange);
         else if (!isfinite(t))
@@ -418,8 +424,7 @@ __global__ void __launch_bounds__(kTile, VALID ? 6 : TGL_WINDOW_MINB) window_ker
         else
             ok = true;
     }
-    float lin = -INFINITY;
-    if (p.layer > 0 && p.root_lo && ok) lin = p.root_lo[i];
+    const float lin = ok ? lin_raw : -INFINITY;
     // the root key (R#7), needed here only by the validity path's uniform draws
     const uint64_t rk0 = (VALID && STRATEGY == TGL_UNIFORM && valid)
                              ? (p.root_key ? p.root_key[i] : p.root_key_base + (uint64_t)i) : 0ull;
