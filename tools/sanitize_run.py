@@ -43,6 +43,20 @@ def main():
             assert np.array_equal(off.cpu().numpy(), o["offsets"]) and np.array_equal(nbr.cpu().numpy(), o["nbr"])
         bounds = torch.tensor(list(range(0, r.numel() + 1, 5000)), dtype=torch.int64, device="cuda")
         tgl.block_digest(blocks[0], bounds)
+    assert g.codec["n_codes"] > 0  # integer times 0..50: the time codec (codes, packed records) runs
+    # a graph with real-valued times: no codec, 16-byte slot records
+    src2, dst2, ts2, _ = random_graph(12, V, E, integer_times=False)
+    g2 = tgl.build(*(torch.as_tensor(x).cuda() for x in (src2, dst2, ts2)), n_nodes=V, add_reverse=True)
+    assert g2.codec["n_codes"] == 0
+    go2 = oracle.build(src2, dst2, ts2, n_nodes=V, add_reverse=True)
+    roots2, rts2 = random_roots(6, V, 20_000 if small else 70_000, integer_times=False)
+    for fan, strat, S, tsl in (([10], "most_recent", 3, 5.0), ([6, 4], "uniform", 1, math.inf)):
+        blocks = tgl.sample(g2, torch.as_tensor(roots2).cuda(), torch.as_tensor(rts2).cuda(), fanouts=fan,
+                            strategy=strat, n_snapshots=S, snapshot_len=tsl, seed=5)
+        bo = oracle.sample(go2, roots2, rts2, fanouts=fan, strategy=0 if strat == "most_recent" else 1, n_snapshots=S,
+                           snapshot_len=tsl, seed=5)
+        for b, o in zip(blocks, bo):
+            assert np.array_equal(b.trimmed()[1].cpu().numpy(), o["nbr"])
     valid = torch.full(((E + 31) // 32,), -1, dtype=torch.int32, device="cuda")
     tgl.edge_valid_set(valid, torch.arange(0, E, 3, dtype=torch.int32, device="cuda"), False, n_bits=E)
     for strat in ("most_recent", "uniform"):
