@@ -74,27 +74,59 @@ __global__ void __launch_bounds__(1024) scan_partials_kernel(uint64_t* __restric
     if (threadIdx.x == 0 && total_out) *total_out = (OutT)carry;
 }
 
-// Downsweep: out[i] = partial[block] + exclusive prefix within the block.  Safe in place.
+// Downsweep: out[i] = partial[block] + exclusive prefix within the block.  Safe in place.  The
+// tile is staged through shared memory (padded: element e at e + e/32, conflict-free for both the
+// coalesced load and a thread's 16 consecutive elements), so global loads and stores are
+// coalesced; the in-tile prefixes go back through the same buffer (32-bit when the tile total
+// fits, else stored straight from registers).  Inputs are 32-bit.
 template <typename InT, typename OutT>
-__global__ void __launch_bounds__(kScanThreads) scan_down_kernel(const InT* __restrict__ in, OutT* __restrict__ out,
-                                                                 int64_t n, const uint64_t* __restrict__ partial) {
+__global__ void __launch_bounds__(kScanThreads) scan_down_kernel(const InT* in, OutT* out, int64_t n,
+                                                                 const uint64_t* __restrict__ partial) {
+    static_assert(sizeof(InT) == 4, "32-bit scan inputs");
     __shared__ uint64_t sm[33];
-    const int64_t base = (int64_t)blockIdx.x * kScanTile + (int64_t)threadIdx.x * kScanItems;
-    uint64_t v[kScanItems];
+    __shared__ uint32_t s_v[kScanTile + kScanTile / 32];
+    const int64_t tile0 = (int64_t)blockIdx.x * kScanTile;
+#pragma unroll
+    for (int j = 0; j < kScanItems; ++j) {
+        const int e = j * kScanThreads + threadIdx.x;
+        const int64_t i = tile0 + e;
+        s_v[e + (e >> 5)] = i < n ? (uint32_t)in[i] : 0u;
+    }
+    __syncthreads();
+    uint32_t v[kScanItems];
     uint64_t s = 0;
 #pragma unroll
     for (int j = 0; j < kScanItems; ++j) {
-        int64_t i = base + j;
-        v[j] = i < n ? (uint64_t)in[i] : 0;
+        const int e = threadIdx.x * kScanItems + j;
+        v[j] = s_v[e + (e >> 5)];
         s += v[j];
     }
     uint64_t tot;
-    uint64_t run = block_excl_scan_u64(s, &tot, sm) + partial[blockIdx.x];
+    const uint64_t ex = block_excl_scan_u64(s, &tot, sm);  // ends with a barrier: s_v is free
+    const uint64_t base = partial[blockIdx.x];
+    if (tot < (1ull << 32)) {  // block-uniform
+        uint32_t run = (uint32_t)ex;
 #pragma unroll
-    for (int j = 0; j < kScanItems; ++j) {
-        int64_t i = base + j;
-        if (i < n) out[i] = (OutT)run;
-        run += v[j];
+        for (int j = 0; j < kScanItems; ++j) {
+            const int e = threadIdx.x * kScanItems + j;
+            s_v[e + (e >> 5)] = run;
+            run += v[j];
+        }
+        __syncthreads();
+#pragma unroll
+        for (int j = 0; j < kScanItems; ++j) {
+            const int e = j * kScanThreads + threadIdx.x;
+            const int64_t i = tile0 + e;
+            if (i < n) out[i] = (OutT)(base + s_v[e + (e >> 5)]);
+        }
+    } else {
+        uint64_t run = base + ex;
+#pragma unroll
+        for (int j = 0; j < kScanItems; ++j) {
+            const int64_t i = tile0 + threadIdx.x * kScanItems + j;
+            if (i < n) out[i] = (OutT)run;
+            run += v[j];
+        }
     }
 }
 
