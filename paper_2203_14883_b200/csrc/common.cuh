@@ -2,6 +2,7 @@
 #pragma once
 
 #include <cuda_runtime.h>
+#include <cstdio>
 #include <nvtx3/nvToolsExt.h>
 #include <stdint.h>
 
@@ -10,6 +11,23 @@
 namespace tgl {
 
 constexpr uint32_t kFull = 0xffffffffu;
+
+// Device bounds checks of the sampler's computed indices, compiled in only with -DTGL_BOUNDS (a
+// debug build run by the GPU tests: compute-sanitizer is unavailable on the test pool).  A failed
+// check prints its line and traps, so the launch fails with a CUDA error.
+#ifdef TGL_BOUNDS
+#define TGL_CHECK(c)                                                          \
+    do {                                                                      \
+        if (!(c)) {                                                           \
+            printf("TGL_CHECK failed: %s (%s:%d)\n", #c, __FILE__, __LINE__); \
+            __trap();                                                         \
+        }                                                                     \
+    } while (0)
+#else
+#define TGL_CHECK(c) \
+    do {             \
+    } while (0)
+#endif
 
 // Sticky device error bits (one word per handle / one module-global word for gather).
 // Priority when mapping to a code: EINVAL > ERANGE > EUNSORTED (same order as the oracle's

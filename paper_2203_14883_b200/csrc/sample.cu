@@ -110,6 +110,7 @@ struct SampleParams {
     const int32_t* tebase;   // [256] eid base per code
     int32_t packed;
     uint32_t bn, bc;
+    uint32_t n_stored;  // E_s (slot count of the handle's lists)
     int32_t n_nodes;
     int64_t node_lo;  // node-sharded handles: global id of local node 0 (0 otherwise)
     const int32_t* root_node;
@@ -228,6 +229,7 @@ __device__ __forceinline__ uint32_t lower_bound_ts(const SampleParams& p, uint32
     uint32_t lo = (uint32_t)A, hi = (uint32_t)B;
     while (lo < hi) {
         const uint32_t mid = lo + ((hi - lo) >> 1);
+        TGL_CHECK(mid < p.n_stored);
         if (ld_rand_f32(p.ts + mid) < x)
             lo = mid + 1;
         else
@@ -258,6 +260,7 @@ __device__ __forceinline__ void lower_bound_multi(const SampleParams& p, uint32_
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
             mid[j] = a[j] + ((b[j] - a[j]) >> 1);
+            TGL_CHECK(a[j] >= b[j] || mid[j] < p.n_stored);
             v[j] = a[j] < b[j] ? ld_rand_f32(p.ts + mid[j]) : 0.0f;
         }
 #pragma unroll
@@ -285,6 +288,7 @@ __device__ __forceinline__ void lower_bound_multi_codes(const SampleParams& p, u
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
             mid[j] = a[j] + ((b[j] - a[j]) >> 1);
+            TGL_CHECK(a[j] >= b[j] || mid[j] < p.n_stored);
             v[j] = a[j] < b[j] ? ld_rand_u8(p.codes + mid[j]) : 0u;
         }
 #pragma unroll
@@ -558,7 +562,10 @@ __global__ void __launch_bounds__(kTile, VALID ? 6 : TGL_WINDOW_MINB) window_ker
         else
             lower_bound_multi(p, ga, gb, x);
 #pragma unroll
-        for (int j = 0; j < 4; ++j) cut[j] = ga[j];
+        for (int j = 0; j < 4; ++j) {
+            cut[j] = ga[j];
+            TGL_CHECK(!valid || (lo <= cut[j] && cut[j] <= hi && hi <= p.n_stored));
+        }
 #pragma unroll
         for (int b = 0; b < 3; ++b) {
             if (b >= nsb) break;
@@ -923,6 +930,7 @@ __global__ void __launch_bounds__(kTile, OUTX == 2 ? 6 : (STRATEGY == TGL_MOST_R
             act[u] = o < total;
             const uint32_t h = hbase + __popc(heads & lemask) - 1u;
             hbase += __popc(heads);
+            TGL_CHECK(!act[u] || h < nseg);
             const uint2 sg = seg[act[u] ? h : 0u];
             const uint32_t q = o - (sg.x >> 9);
             info[u] = sg.x;
@@ -941,12 +949,15 @@ __global__ void __launch_bounds__(kTile, OUTX == 2 ? 6 : (STRATEGY == TGL_MOST_R
         for (int u = 0; u < kCopyUnroll; ++u) {
             if (act[u]) {
                 if (PK) {
+                    TGL_CHECK(pos[u] < p.n_stored);
                     const uint2 v = ld_rand_v2(reinterpret_cast<const uint2*>(p.recs) + pos[u]);
                     const uint64_t w = ((uint64_t)v.y << 32) | v.x;
                     const uint32_t c = (uint32_t)(w >> p.bn) & ((1u << p.bc) - 1u);
+                    TGL_CHECK(c < (uint32_t)kMaxCodes);
                     rec[u] = make_int4(__float_as_int(s_tv[c]), (int32_t)(uint32_t)(w & ((1ull << p.bn) - 1ull)),
                                        s_te[c] + (int32_t)(uint32_t)(w >> (p.bn + p.bc)), 0);
                 } else if (p.recs) {
+                    TGL_CHECK(pos[u] < p.n_stored);
                     rec[u] = ld_rec16<STRATEGY == TGL_MOST_RECENT && !VALID>(p.recs + pos[u]);
                 } else {
                     rec[u] = make_int4(__float_as_int(__ldg(p.ts + pos[u])), __ldg(p.nbr + pos[u]),
@@ -1077,6 +1088,7 @@ static void set_graph(SampleParams& sp, const tgl_tcsr* g, bool use_recs, bool u
         sp.bn = (uint32_t)g->bits_nbr;
         sp.bc = (uint32_t)g->bits_code;
     }
+    sp.n_stored = (uint32_t)g->n_stored;
     sp.n_levels = use_index && g->index ? g->n_levels : 0;
     for (int q = 1; q <= sp.n_levels; ++q) sp.lvl[q] = g->index + g->level_off[q];
     sp.n_nodes = g->n_nodes;
