@@ -707,6 +707,9 @@ def run_ours(args):
         "gpu_launches": launches_per_step * args.steps,
         "clocks": clocks.summary(),
         "build_ms": build_ms, "generate_s": gen_s,
+        # the T-CSR aux layout of this graph: the lossless time codec when the
+        # graph has <= 127 distinct times (C5: publication years), 8-byte packed slot records
+        "tcsr_layout": {"time_codes": g.codec["n_codes"], "packed_slot_records": g.codec["packed"]},
         "edges_per_step": edges_total / args.steps, "roots_per_step": roots_total / args.steps,
         "device_error": int(err),
         **({"oversubscribed": f"{world} ranks on {n_dev} GPU(s): launcher test, not a scaling number"}

@@ -206,3 +206,26 @@ def test_codec_sticky_errors(tgl):
     _blocks_equal(b, bo, "out-of-range roots")  # a root at time -1 selects nothing, like a bad id
     tgl.sample(g, cu([0], torch.int32), cu([float("nan")], torch.float32), fanouts=[4])
     assert tgl.check(g) == tgl._lib.EINVAL
+
+
+def test_codec_empty_and_foreign_aux(tgl):
+    """an empty stream builds (no codec) and samples nothing; tgl_tcsr_wrap rejects an aux buffer
+    that no aux build filled (EINVAL), instead of reading garbage codec widths"""
+    import ctypes
+    from paper_2203_14883_b200 import _lib
+    e = np.zeros(0, np.int32)
+    g = tgl.build(cu(e, torch.int32), cu(e, torch.int32), cu(np.zeros(0, np.float32), torch.float32), n_nodes=5,
+                  add_reverse=True)
+    assert g.codec == {"n_codes": 0, "packed": False}
+    b = tgl.sample(g, cu([0, 4], torch.int32), cu([3.0, 7.0], torch.float32), fanouts=[4], n_snapshots=2,
+                   snapshot_len=1.0)
+    for x in b:
+        off, nbr, _, _, _ = x.trimmed()
+        assert off.cpu().tolist() == [0, 0, 0] and nbr.numel() == 0
+    src, dst, ts = _stream(15, 100, 1000, np.arange(5, dtype=np.float32))
+    g2 = tgl.build(cu(src, torch.int32), cu(dst, torch.int32), cu(ts, torch.float32), n_nodes=100, add_reverse=True)
+    junk = torch.full((g2.index.numel(),), 0x5A, dtype=torch.uint8, device="cuda")
+    h = ctypes.c_void_p()
+    rc = tgl._L.tgl_tcsr_wrap(g2.indptr.data_ptr(), g2.nbr.data_ptr(), g2.ts.data_ptr(), g2.eid.data_ptr(),
+                              junk.data_ptr(), junk.numel(), 100, g2.n_stored, ctypes.byref(h))
+    assert rc == _lib.EINVAL
