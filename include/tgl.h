@@ -145,7 +145,9 @@ TGL_API int tgl_tcsr_info(const tgl_tcsr *g, int32_t *n_nodes /* host */, int64_
 
 /* Host query of the handle's time codec (tgl_tcsr_build "aux"): *n_codes = number of distinct
  * timestamps coded (0: no codec -- no aux, more than 255 distinct times, or -0.0 present);
- * *packed = 1 when slot records are the 8-byte packed form.  Either pointer may be NULL. */
+ * *packed = 1 when slot records are the 8-byte form with time codes, 2 when they are the 8-byte form
+ * with integer times (no time codes: every time an integer below 2^24, e.g. GDELT's 15-minute ticks,
+ * and nbr / eid offset / time widths fit 64 bits), 0 otherwise.  Either pointer may be NULL. */
 TGL_API int tgl_tcsr_codec(const tgl_tcsr *g, int32_t *n_codes /* host */, int32_t *packed /* host */);
 
 /* ------------------------------------------------------------------ sampler (Alg. 1) */

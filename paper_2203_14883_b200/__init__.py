@@ -79,10 +79,11 @@ class TCSR:
 
     @property
     def codec(self) -> dict:
-        """tgl_tcsr_codec: {"n_codes": distinct times coded (0 = no time codec), "packed": 8-byte records}."""
+        """tgl_tcsr_codec: {"n_codes": distinct times coded (0 = no time codec), "packed": 8-byte slot
+        records -- 0 no, 1 with time codes, 2 with integer times (< 2^24, without time codes)}."""
         n, pk = ctypes.c_int32(), ctypes.c_int32()
         _rc(_L.tgl_tcsr_codec(self._h, ctypes.byref(n), ctypes.byref(pk)), "tgl_tcsr_codec")
-        return {"n_codes": n.value, "packed": bool(pk.value)}
+        return {"n_codes": n.value, "packed": pk.value}
 
     def __del__(self):
         h, self._h = getattr(self, "_h", None), None

@@ -74,13 +74,15 @@ extern "C" int tgl_tcsr_wrap(const int64_t* indptr, const int32_t* nbr, const fl
     g->nodes = aux ? static_cast<const void*>(ab + lay.node_off) : nullptr;
     if (aux) {
         // the codec header written by the aux build (a synchronous read: the aux build has completed)
-        uint32_t hdr[5] = {0, 0, 0, 0, 0};
+        uint32_t hdr[6] = {0, 0, 0, 0, 0, 0};
         if (cudaMemcpy(hdr, aux, sizeof(hdr), cudaMemcpyDeviceToHost) != cudaSuccess) {
             cudaFree(g->err_dev);
             free(g);
             return TGL_ECUDA;
         }
-        if (hdr[0] != kDictMagic || hdr[1] > (uint32_t)kMaxCodes || hdr[2] > 1 || hdr[3] > 32 || hdr[4] > 8) {
+        const bool bad = hdr[0] != kDictMagic || hdr[1] > (uint32_t)kMaxCodes || hdr[2] > 2 || hdr[3] > 32 ||
+                         (hdr[2] == 2 ? (hdr[1] != 0 || hdr[4] > 32 || hdr[3] + hdr[4] > 64) : hdr[4] > 8);
+        if (bad) {
             cudaFree(g->err_dev);
             free(g);
             return TGL_EINVAL;  // not a buffer filled by tgl_tcsr_build / tgl_tcsr_aux_build
@@ -92,6 +94,11 @@ extern "C" int tgl_tcsr_wrap(const int64_t* indptr, const int32_t* nbr, const fl
             g->packed = (int)hdr[2];
             g->bits_nbr = (int)hdr[3];
             g->bits_code = (int)hdr[4];
+        } else if (hdr[2] == 2) {  // integer-time packed records
+            g->packed = 2;
+            g->bits_nbr = (int)hdr[3];
+            g->bits_code = (int)hdr[4];
+            g->eid_base0 = (int32_t)hdr[5];
         }
     }
     cudaGetDevice(&g->device);

@@ -16,6 +16,7 @@
 #include <algorithm>
 #include <climits>
 #include <cstdlib>
+#include <cstring>
 
 #include "common.cuh"
 #include "radix.cuh"
@@ -250,10 +251,43 @@ __global__ void __launch_bounds__(256) codec_assign_kernel(const float* __restri
     if (threadIdx.x == 0) atomicMax(&sc->nbr_max, nmax);
 }
 
+// integer-time packing (packed = 2, tsindex.cuh): are all times integers in [0, 2^24), their
+// largest value, the eid range and the largest neighbour id
+__global__ void __launch_bounds__(256) inttime_scan_kernel(const float* __restrict__ ts, const int32_t* __restrict__ nbr,
+                                                           const int32_t* __restrict__ eid, uint64_t n,
+                                                           CodecScratch* sc) {
+    uint32_t tmax = 0, bad = 0, nmax = 0;
+    int32_t emn = INT32_MAX, emx = INT32_MIN;
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += stride) {
+        const float t = ts[j];
+        const uint32_t bits = __float_as_uint(t);
+        // integers in [0, 2^24): sign clear, below 2^24, no fraction
+        bad |= (bits >= 0x4b800000u || t != truncf(t)) ? 1u : 0u;
+        tmax = max(tmax, bits);
+        nmax = max(nmax, (uint32_t)nbr[j]);
+        emn = min(emn, eid[j]);
+        emx = max(emx, eid[j]);
+    }
+    tmax = __reduce_max_sync(kFull, tmax);
+    bad = __reduce_or_sync(kFull, bad);
+    nmax = __reduce_max_sync(kFull, nmax);
+    emn = __reduce_min_sync(kFull, emn);
+    emx = __reduce_max_sync(kFull, emx);
+    if ((threadIdx.x & 31) == 0) {
+        atomicMax(&sc->t_max_bits, tmax);
+        atomicOr(&sc->not_int, bad);
+        atomicMax(&sc->nbr_max, nmax);
+        atomicMin(&sc->e_min, emn);
+        atomicMax(&sc->e_max, emx);
+    }
+}
+
 struct CodecArgs {
     const uint8_t* codes;   // null: no codec
     const int32_t* eid_base;
-    int packed, bn, bc;
+    int packed, bn, bc;  // packed: 1 time codes, 2 integer times (bc = eid offset width)
+    int32_t ebase0;      // packed = 2: the smallest eid
 };
 
 // aux buffer (tsindex.cuh): index levels L_l[j] = ts[j * 16^l], the slot records (16-byte, or
@@ -269,12 +303,20 @@ __global__ void aux_build_kernel(const int64_t* __restrict__ indptr, const float
         for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < lay.index.len[l]; j += stride)
             out[j] = ts[j << sh];
     }
-    if (cx.packed) {
+    if (cx.packed == 1) {
         uint2* rec = reinterpret_cast<uint2*>(aux + lay.rec_off);
         for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += stride) {
             const uint32_t c = cx.codes[j];
             const uint64_t rel = (uint64_t)(uint32_t)(eid[j] - __ldg(cx.eid_base + c));
             const uint64_t w = (uint64_t)(uint32_t)nbr[j] | ((uint64_t)c << cx.bn) | (rel << (cx.bn + cx.bc));
+            rec[j] = make_uint2((uint32_t)w, (uint32_t)(w >> 32));
+        }
+    } else if (cx.packed == 2) {
+        uint2* rec = reinterpret_cast<uint2*>(aux + lay.rec_off);
+        for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += stride) {
+            const uint64_t rel = (uint64_t)(uint32_t)(eid[j] - cx.ebase0);
+            const uint64_t tint = (uint64_t)(uint32_t)ts[j];
+            const uint64_t w = (uint64_t)(uint32_t)nbr[j] | (rel << cx.bn) | (tint << (cx.bn + cx.bc));
             rec[j] = make_uint2((uint32_t)w, (uint32_t)(w >> 32));
         }
     } else {
@@ -367,7 +409,7 @@ extern "C" int tgl_tcsr_aux_build(const int64_t* indptr, const float* ts, const 
     static const bool no_codec = getenv("TGL_NO_CODEC") != nullptr;  // A/B knob, read once
     const uint32_t D = (n > 0 && !cnt[1] && !no_codec) ? cnt[0] : 0u;
     uint32_t hdr[8] = {kDictMagic, D, 0, 0, 0, 0, 0, 0};
-    CodecArgs cx = {nullptr, nullptr, 0, 0, 0};
+    CodecArgs cx = {nullptr, nullptr, 0, 0, 0, 0};
     if (D > 0) {
         // X2 dictionary, X3 codes + widths
         codec_dict_kernel<<<1, 512, 0, st>>>(sc, dict);
@@ -389,7 +431,33 @@ extern "C" int tgl_tcsr_aux_build(const int64_t* indptr, const float* ts, const 
         hdr[4] = (uint32_t)bc;
         if (cudaMemcpyAsync(dict->eid_base, emin, sizeof(emin), cudaMemcpyHostToDevice, st) != cudaSuccess)
             return TGL_ECUDA;
-        cx = CodecArgs{codes, dict->eid_base, packed ? 1 : 0, bn, bc};
+        cx = CodecArgs{codes, dict->eid_base, packed ? 1 : 0, bn, bc, 0};
+    } else if (n > 0 && !no_codec) {
+        // no time codes: integer times below 2^24 still pack (packed = 2, tsindex.cuh)
+        const uint32_t init[6] = {0u, 0u, 0u, 0u, (uint32_t)INT32_MAX, (uint32_t)INT32_MIN};  // t_max, not_int, e_min, e_max
+        if (cudaMemsetAsync(&sc->nbr_max, 0, sizeof(uint32_t), st) != cudaSuccess ||
+            cudaMemcpyAsync(&sc->t_max_bits, init, 2 * sizeof(uint32_t), cudaMemcpyHostToDevice, st) != cudaSuccess ||
+            cudaMemcpyAsync(&sc->e_min, init + 4, 2 * sizeof(uint32_t), cudaMemcpyHostToDevice, st) != cudaSuccess)
+            return TGL_ECUDA;
+        inttime_scan_kernel<<<grid, 256, 0, st>>>(ts, nbr, eid, n, sc);
+        uint32_t r[2] = {0, 0}, nmax = 0;
+        int32_t e[2] = {0, 0};
+        if (cudaMemcpyAsync(r, &sc->t_max_bits, sizeof(r), cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+            cudaMemcpyAsync(e, &sc->e_min, sizeof(e), cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+            cudaMemcpyAsync(&nmax, &sc->nbr_max, sizeof(nmax), cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+            cudaStreamSynchronize(st) != cudaSuccess)
+            return TGL_ECUDA;
+        float tmax = 0.0f;
+        memcpy(&tmax, &r[0], sizeof(tmax));
+        const int bn = bit_width(nmax), be = bit_width((uint64_t)((int64_t)e[1] - (int64_t)e[0])),
+                  bt = bit_width((uint64_t)tmax);
+        if (!r[1] && bn + be + bt <= 64) {
+            hdr[2] = 2u;
+            hdr[3] = (uint32_t)bn;
+            hdr[4] = (uint32_t)be;
+            hdr[5] = (uint32_t)e[0];
+            cx = CodecArgs{nullptr, nullptr, 2, bn, be, e[0]};
+        }
     }
     if (cudaMemcpyAsync(dict, hdr, sizeof(hdr), cudaMemcpyHostToDevice, st) != cudaSuccess) return TGL_ECUDA;
     const int64_t blocks = std::min<int64_t>((int64_t)((std::max<int64_t>(n_stored, (int64_t)n_nodes * 4) + 255) / 256),

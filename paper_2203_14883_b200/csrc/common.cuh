@@ -128,5 +128,6 @@ struct tgl_tcsr {
     // time codec (tsindex.cuh "time codes"): on when n_codes > 0
     const void* dict;        // TimeDict (device): sorted distinct times + per-code eid bases
     const uint8_t* codes;    // per-slot time code
-    int n_codes, packed, bits_nbr, bits_code;
+    int n_codes, packed, bits_nbr, bits_code;  // packed: 1 time codes, 2 integer times (tsindex.cuh)
+    int eid_base0;                             // packed = 2: the smallest eid
 };

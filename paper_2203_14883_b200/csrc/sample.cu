@@ -108,8 +108,9 @@ struct SampleParams {
     const uint8_t* codes;    // null -> no codec
     const float* tval;       // [256] sorted distinct times (+inf padded)
     const int32_t* tebase;   // [256] eid base per code
-    int32_t packed;
+    int32_t packed;  // 1: time codes; 2: integer times (tsindex.cuh)
     uint32_t bn, bc;
+    int32_t ebase0;  // packed = 2: the smallest eid
     uint32_t n_stored;  // E_s (slot count of the handle's lists)
     int32_t n_nodes;
     int64_t node_lo;  // node-sharded handles: global id of local node 0 (0 otherwise)
@@ -182,6 +183,11 @@ __device__ __forceinline__ int4 ld_rand_v4(const int4* p) {
 __device__ __forceinline__ uint32_t ld_rand_u8(const uint8_t* p) {
     uint16_t v;
     asm("ld.global.nc.L2::64B.u8 %0, [%1];" : "=h"(v) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ uint2 ld_rand_v2_64(const uint2* p) {  // scattered single records
+    uint2 v;
+    asm("ld.global.nc.L2::64B.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "l"(p));
     return v;
 }
 __device__ __forceinline__ uint2 ld_rand_v2(const uint2* p) {
@@ -705,7 +711,7 @@ __host__ __device__ inline int copy_warp_words(int nsb, int k, bool picks_in_sme
 // 64-bit accesses); else in the global workspace
 // PK: 8-byte packed slot records of the time codec (decoded through the dictionaries, which sit
 // behind the warps' areas in dynamic shared memory: 2 KB)
-template <int STRATEGY, bool VALID, int OUTX, bool PSMEM, bool PK>
+template <int STRATEGY, bool VALID, int OUTX, bool PSMEM, int PK>
 __global__ void __launch_bounds__(kTile, OUTX == 2 ? 6 : (STRATEGY == TGL_MOST_RECENT ? TGL_COPY_MINB_MR : TGL_COPY_MINB)) copy_kernel(const __grid_constant__ SampleParams p) {
     constexpr bool EXTRA = OUTX == 1;   // per-output data for a following layer / dedup
     constexpr bool GATHER = OUTX == 2;  // fused row gather of the last layer's outputs
@@ -743,7 +749,7 @@ __global__ void __launch_bounds__(kTile, OUTX == 2 ? 6 : (STRATEGY == TGL_MOST_R
 
     float* s_tv = reinterpret_cast<float*>(smem + kWarps * copy_warp_words(nsb, k, picks_smem));  // PK only
     int32_t* s_te = reinterpret_cast<int32_t*>(s_tv + 256);
-    if (PK) {
+    if (PK == 1) {
         s_tv[threadIdx.x] = __ldg(p.tval + threadIdx.x);  // kTile == 256 entries
         s_te[threadIdx.x] = __ldg(p.tebase + threadIdx.x);
     }
@@ -948,7 +954,7 @@ __global__ void __launch_bounds__(kTile, OUTX == 2 ? 6 : (STRATEGY == TGL_MOST_R
 #pragma unroll
         for (int u = 0; u < kCopyUnroll; ++u) {
             if (act[u]) {
-                if (PK) {
+                if (PK == 1) {
                     TGL_CHECK(pos[u] < p.n_stored);
                     const uint2 v = ld_rand_v2(reinterpret_cast<const uint2*>(p.recs) + pos[u]);
                     const uint64_t w = ((uint64_t)v.y << 32) | v.x;
@@ -956,6 +962,16 @@ __global__ void __launch_bounds__(kTile, OUTX == 2 ? 6 : (STRATEGY == TGL_MOST_R
                     TGL_CHECK(c < (uint32_t)kMaxCodes);
                     rec[u] = make_int4(__float_as_int(s_tv[c]), (int32_t)(uint32_t)(w & ((1ull << p.bn) - 1ull)),
                                        s_te[c] + (int32_t)(uint32_t)(w >> (p.bn + p.bc)), 0);
+                } else if (PK == 2) {  // integer times: ts = (float)time, exact below 2^24
+                    TGL_CHECK(pos[u] < p.n_stored);
+                    const uint2 v = STRATEGY == TGL_MOST_RECENT
+                                        ? ld_rand_v2(reinterpret_cast<const uint2*>(p.recs) + pos[u])
+                                        : ld_rand_v2_64(reinterpret_cast<const uint2*>(p.recs) + pos[u]);
+                    const uint64_t w = ((uint64_t)v.y << 32) | v.x;
+                    const uint32_t be = p.bc, sh = p.bn + p.bc;
+                    rec[u] = make_int4(__float_as_int((float)(uint32_t)(w >> sh)),
+                                       (int32_t)(uint32_t)(w & ((1ull << p.bn) - 1ull)),
+                                       p.ebase0 + (int32_t)(uint32_t)((w >> p.bn) & ((1ull << be) - 1ull)), 0);
                 } else if (p.recs) {
                     TGL_CHECK(pos[u] < p.n_stored);
                     rec[u] = ld_rec16<STRATEGY == TGL_MOST_RECENT && !VALID>(p.recs + pos[u]);
@@ -1087,6 +1103,11 @@ static void set_graph(SampleParams& sp, const tgl_tcsr* g, bool use_recs, bool u
         sp.packed = g->packed;
         sp.bn = (uint32_t)g->bits_nbr;
         sp.bc = (uint32_t)g->bits_code;
+    } else if (use_recs && g->packed == 2 && !validity) {
+        sp.packed = 2;
+        sp.bn = (uint32_t)g->bits_nbr;
+        sp.bc = (uint32_t)g->bits_code;
+        sp.ebase0 = g->eid_base0;
     }
     sp.n_stored = (uint32_t)g->n_stored;
     sp.n_levels = use_index && g->index ? g->n_levels : 0;
@@ -1203,9 +1224,9 @@ static int plan_sample(int64_t n_roots, int L, const int32_t* fanouts, int S, in
     return TGL_OK;
 }
 
-template <int STRATEGY, bool VALID, int OUTX, bool PSMEM, bool PK>
+template <int STRATEGY, bool VALID, int OUTX, bool PSMEM, int PK>
 static void launch_copy_pk(const SampleParams& sp, int64_t grid, size_t smem, cudaStream_t st) {
-    if (PK) smem += 256 * (sizeof(float) + sizeof(int32_t));  // the codec's dictionaries
+    if (PK == 1) smem += 256 * (sizeof(float) + sizeof(int32_t));  // the codec's dictionaries
     if (smem + 1024 > 48 * 1024)  // the dynamic part plus ~640 B of static shared memory
         cudaFuncSetAttribute(copy_kernel<STRATEGY, VALID, OUTX, PSMEM, PK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)smem);
@@ -1232,10 +1253,12 @@ static void launch_copy_pk(const SampleParams& sp, int64_t grid, size_t smem, cu
 // packed records exist only with the codec, which the validity path never uses
 template <int STRATEGY, bool VALID, int OUTX, bool PSMEM>
 static void launch_copy_ps(const SampleParams& sp, int64_t grid, size_t smem, cudaStream_t st) {
-    if (!VALID && sp.packed)
-        launch_copy_pk<STRATEGY, VALID, OUTX, PSMEM, !VALID>(sp, grid, smem, st);
+    if (!VALID && sp.packed == 1)
+        launch_copy_pk<STRATEGY, VALID, OUTX, PSMEM, VALID ? 0 : 1>(sp, grid, smem, st);
+    else if (!VALID && sp.packed == 2)
+        launch_copy_pk<STRATEGY, VALID, OUTX, PSMEM, VALID ? 0 : 2>(sp, grid, smem, st);
     else
-        launch_copy_pk<STRATEGY, VALID, OUTX, PSMEM, false>(sp, grid, smem, st);
+        launch_copy_pk<STRATEGY, VALID, OUTX, PSMEM, 0>(sp, grid, smem, st);
 }
 
 template <int STRATEGY, bool VALID, int OUTX>

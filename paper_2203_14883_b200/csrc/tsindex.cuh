@@ -102,13 +102,18 @@ constexpr int kCodeFences = 54;  // 10 separators + 11 groups of 4
 constexpr int kCodeSeps = 10;
 constexpr uint32_t kCodeInf = 127u;
 constexpr uint32_t kDictMagic = 0x54474344u;  // "TGCD"
+// Without the codec (more distinct times), slot records still pack into 8 bytes when every time is
+// an integer below 2^24 -- GDELT's 15-minute ticks to 1.8e5 (Table 3) -- and the widths
+// fit: packed = 2, {nbr | (eid - eid_base[0]) << bn | time << (bn + be)} with be = bits_code; the
+// copy kernel decodes ts = (float)time, exact below 2^24.
 struct TimeDict {
     uint32_t magic;
     uint32_t n_codes;    // D (0: no codec: more than kMaxCodes distinct times, or -0 / non-finite)
-    uint32_t packed;     // 1: 8-byte packed slot records
+    uint32_t packed;     // 1: 8-byte records with time codes; 2: 8-byte records with integer times
     uint32_t bits_nbr;   // bn
-    uint32_t bits_code;  // bc
-    uint32_t pad[3];
+    uint32_t bits_code;  // bc (packed = 1) / be, the eid offset width (packed = 2)
+    int32_t eid_base0;   // packed = 2: the smallest eid
+    uint32_t pad[2];
     float value[256];       // sorted distinct timestamps, +inf beyond D
     int32_t eid_base[256];  // smallest eid of each code (packed records)
 };
@@ -117,6 +122,8 @@ struct CodecScratch {
     uint32_t hash[512];  // distinct ts bits (open addressing, 0xffffffff = empty)
     int32_t eid_min[256], eid_max[256];
     uint32_t count, overflow, nbr_max, pad;
+    uint32_t t_max_bits, not_int;  // integer-time packing: largest time (float bits), any non-integer
+    int32_t e_min, e_max;
 };
 constexpr uint64_t kDictBytes = 8192;
 static_assert(sizeof(TimeDict) + sizeof(CodecScratch) <= kDictBytes, "dictionary region");

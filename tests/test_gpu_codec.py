@@ -98,17 +98,18 @@ def test_codec_fractional_times(tgl):
 
 
 def test_codec_off_at_128_and_minus_zero(tgl):
-    """128 distinct times, or a -0.0 time: no codec, same blocks"""
+    """128 distinct times: no time codes, but integer times pack (packed = 2); a -0.0 time: neither;
+    same blocks"""
     values = np.arange(128, dtype=np.float32)
     src, dst, ts = _stream(7, 1500, 20_000, values)
     ts[:128] = values  # every value present
     ts = np.sort(ts)
     roots, rts = random_roots(7, 1500, 4000, t_max=128.0)
-    _check(tgl, src, dst, ts, None, 1500, True, roots, rts, expect_codes=0)
+    g = _check(tgl, src, dst, ts, None, 1500, True, roots, rts, expect_codes=0, expect_packed=2)
     src, dst, ts = _stream(8, 800, 5000, np.arange(10, dtype=np.float32))
     ts[: np.sum(ts == 0)] = np.float32(-0.0)  # the zeros become -0.0 (still chronological)
     roots, rts = random_roots(8, 800, 2000, t_max=10.0)
-    _check(tgl, src, dst, ts, None, 800, True, roots, rts, expect_codes=0)
+    _check(tgl, src, dst, ts, None, 800, True, roots, rts, expect_codes=0, expect_packed=0)
 
 
 def test_codec_fence_boundaries(tgl):
@@ -216,7 +217,7 @@ def test_codec_empty_and_foreign_aux(tgl):
     e = np.zeros(0, np.int32)
     g = tgl.build(cu(e, torch.int32), cu(e, torch.int32), cu(np.zeros(0, np.float32), torch.float32), n_nodes=5,
                   add_reverse=True)
-    assert g.codec == {"n_codes": 0, "packed": False}
+    assert g.codec == {"n_codes": 0, "packed": 0}
     b = tgl.sample(g, cu([0, 4], torch.int32), cu([3.0, 7.0], torch.float32), fanouts=[4], n_snapshots=2,
                    snapshot_len=1.0)
     for x in b:
@@ -229,3 +230,21 @@ def test_codec_empty_and_foreign_aux(tgl):
     rc = tgl._L.tgl_tcsr_wrap(g2.indptr.data_ptr(), g2.nbr.data_ptr(), g2.ts.data_ptr(), g2.eid.data_ptr(),
                               junk.data_ptr(), junk.numel(), 100, g2.n_stored, ctypes.byref(h))
     assert rc == _lib.EINVAL
+
+
+def test_integer_time_packing(tgl):
+    """GDELT-like integer ticks (more than 127 distinct): 8-byte records with integer times
+    (packed = 2) -- uniform 2-layer and most_recent S = 3 equal the oracle; real-valued times or a
+    time >= 2^24 do not pack"""
+    rng = np.random.default_rng(21)
+    for vmax, expect in ((180_000, 2), (2**24 + 50, 0)):
+        src = rng.integers(0, 700, 30_000).astype(np.int32)
+        dst = rng.integers(0, 700, 30_000).astype(np.int32)
+        ts = np.sort(rng.integers(0, vmax, 30_000)).astype(np.float32)
+        ts[-1] = np.float32(vmax)  # the largest time present (2^24 + 50 -> 2^24 + 50 rounds to an even float)
+        roots, rts = src[::7].copy(), (ts[::7] + 1).astype(np.float32)
+        _check(tgl, src, dst, ts, None, 700, False, roots, rts, expect_codes=0, expect_packed=expect,
+               cases=(([10, 10], 1, 1, math.inf), ([10], 0, 3, 5000.0), ([4, 3], 0, 1, math.inf)))
+    src, dst, ts = _stream(22, 500, 8000, np.float32(0.5) + np.arange(300, dtype=np.float32))
+    roots, rts = random_roots(22, 500, 3000, t_max=300.0)
+    _check(tgl, src, dst, ts, None, 500, True, roots, rts, expect_codes=0, expect_packed=0)
