@@ -101,11 +101,13 @@ TGL_API int tgl_tcsr_build_workspace(int64_t n_edges, int32_t n_nodes, int add_r
  *   cut search), a 16-byte record {ts, nbr, eid, 0} per slot (payload copy: one load per output)
  *   and a 64-byte record {lo, hi, 14 fence times} per node (list bounds and cut gaps in one
  *   load) -- DESIGN.md "Data layout".  Without it the sampler reads the separate arrays.
- *   Time codec: when the T-CSR holds at most 255 distinct timestamps (all finite, >= +0; e.g.
+ *   Time codec: when the T-CSR holds at most 127 distinct timestamps (all finite, >= +0; e.g.
  *   MAG's publication years, P:L336 / P:L355) the aux build also writes a dictionary of the
- *   sorted distinct times and a 1-byte code per slot; node records then carry 56 fence codes and,
- *   when nbr / code / per-code eid offset fit 64 bits, slot records shrink to 8 bytes.  Lossless:
- *   sampled blocks are bit-identical with and without it (tgl_tcsr_codec reports it).
+ *   sorted distinct times and a 7-bit code per slot; node records then carry 54 fence codes and,
+ *   when nbr / code / per-code eid offset fit 64 bits, slot records shrink to 8 bytes.  Without
+ *   codes, slot records still shrink to 8 bytes when every time is an integer below 2^24 and nbr /
+ *   eid offset / time fit 64 bits (e.g. GDELT's 15-minute ticks).  Lossless: sampled blocks are
+ *   bit-identical with and without either form (tgl_tcsr_codec reports them).
  *   The aux build blocks on `stream` (it reads the distinct-time count and the codec widths).
  * workspace: >= tgl_tcsr_build_workspace() bytes of device memory, 256-byte aligned.
  * Synchronous validation: the call blocks on `stream` once to read the device validation word;
@@ -144,7 +146,7 @@ TGL_API int tgl_tcsr_set_node_base(tgl_tcsr *g, int64_t node_lo);
 TGL_API int tgl_tcsr_info(const tgl_tcsr *g, int32_t *n_nodes /* host */, int64_t *n_stored /* host */);
 
 /* Host query of the handle's time codec (tgl_tcsr_build "aux"): *n_codes = number of distinct
- * timestamps coded (0: no codec -- no aux, more than 255 distinct times, or -0.0 present);
+ * timestamps coded (0: no codec -- no aux, more than 127 distinct times, or -0.0 present);
  * *packed = 1 when slot records are the 8-byte form with time codes, 2 when they are the 8-byte form
  * with integer times (no time codes: every time an integer below 2^24, e.g. GDELT's 15-minute ticks,
  * and nbr / eid offset / time widths fit 64 bits), 0 otherwise.  Either pointer may be NULL. */

@@ -291,7 +291,7 @@ struct CodecArgs {
 };
 
 // aux buffer (tsindex.cuh): index levels L_l[j] = ts[j * 16^l], the slot records (16-byte, or
-// 8-byte packed under the codec) and the node records (14 fence times, or 56 fence codes)
+// 8-byte packed) and the node records (14 fence times, or 54 fence codes under the time codec)
 __global__ void aux_build_kernel(const int64_t* __restrict__ indptr, const float* __restrict__ ts,
                                  const int32_t* __restrict__ nbr, const int32_t* __restrict__ eid, uint64_t n,
                                  uint64_t n_nodes, char* __restrict__ aux, AuxLayout lay, CodecArgs cx) {

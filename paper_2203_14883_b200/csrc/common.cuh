@@ -123,7 +123,7 @@ struct tgl_tcsr {
     int n_levels;
     uint64_t level_off[12];  // float offset of level l in index (levels <= 8)
     const void* recs;        // slot records {ts, nbr, eid, 0} (16 bytes) or codec-packed (8), or null
-    const void* nodes;       // 64-byte node records {lo, hi, 14 fence times | 56 fence codes}, or null
+    const void* nodes;       // 64-byte node records {lo, hi, 14 fence times | 54 fence codes}, or null
     int64_t node_lo;         // node-sharded handle: global id of local node 0
     // time codec (tsindex.cuh "time codes"): on when n_codes > 0
     const void* dict;        // TimeDict (device): sorted distinct times + per-code eid bases

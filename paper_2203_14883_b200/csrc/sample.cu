@@ -103,7 +103,7 @@ struct SampleParams {
     const int4* nodes;                      // 64-byte node records {lo, hi, 14 fences} (tsindex.cuh), or null
     const float* lvl[kMaxIndexLevels + 1];  // lvl[l] = index level l (1-based)
     int32_t n_levels;                       // 0 -> no index
-    // time codec (tsindex.cuh "time codes"): node records hold 56 fence codes and the cut probes
+    // time codec (tsindex.cuh "time codes"): node records hold 54 fence codes and the cut probes
     // read 1-byte codes; packed: 8-byte slot records {nbr | code << bn | eid - eid_base[code]}
     const uint8_t* codes;    // null -> no codec
     const float* tval;       // [256] sorted distinct times (+inf padded)
@@ -394,7 +394,7 @@ __device__ __forceinline__ float rec_word(const float* rec, int sw, int w) {
 }
 
 // ---------------------------------------------------------------------------- K4a windows
-// TC: the graph has the time codec (node records with 56 fence codes, cut probes over codes)
+// TC: the graph has the time codec (node records with 54 fence codes, cut probes over codes)
 template <int STRATEGY, bool VALID, bool TC>
 __global__ void __launch_bounds__(kTile, VALID ? 6 : TGL_WINDOW_MINB) window_kernel(const __grid_constant__ SampleParams p) {
     __shared__ uint32_t s_red[TGL_MAX_SNAPSHOTS][kWarps];
